@@ -1,0 +1,341 @@
+// ref_capi.cpp — extern "C" wrapper around the UNMODIFIED reference library.
+//
+// TEST INFRASTRUCTURE ONLY.  Compiled by oracle/Makefile together with the
+// reference sources under /root/reference/proj/src into oracle/_ref/ (git
+// ignored).  Used to (1) generate the golden vectors in tests/golden/,
+// (2) cross-check the C restatement oracle/hq_oracle.c, and (3) time the
+// reference CPU path for bench.py's cpu_baseline / --impl reference leg.
+// The product never links or loads this.
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <thread>
+#include <vector>
+
+#include "tucker/errors.hpp"
+#include "tucker/harness.hpp"
+#include "tucker/kernels.hpp"
+#include "tucker/manifold.hpp"
+#include "tucker/rng.hpp"
+#include "tucker/solvers.hpp"
+#include "tucker/sparse_tensor.hpp"
+
+using namespace tucker;
+
+namespace {
+
+int code_of(const std::exception& e) {
+    if (dynamic_cast<const ShapeError*>(&e)) return 1;
+    if (dynamic_cast<const RangeError*>(&e)) return 2;
+    if (dynamic_cast<const ValueError*>(&e)) return 3;
+    if (dynamic_cast<const ParseError*>(&e)) return 4;
+    if (dynamic_cast<const CapacityError*>(&e)) return 5;
+    if (dynamic_cast<const ContractError*>(&e)) return 6;
+    if (dynamic_cast<const DiagnosticError*>(&e)) return 7;
+    if (dynamic_cast<const DegenerateStateError*>(&e)) return 8;
+    if (dynamic_cast<const InfeasibleError*>(&e)) return 9;
+    return 12;
+}
+
+struct RefTensor {
+    SparseTensor x;
+};
+
+FactorSet to_factors(int n, const uint64_t* dims, const uint64_t* ranks, const double* f) {
+    FactorSet u;
+    std::size_t o = 0;
+    for (int v = 0; v < n; ++v) {
+        Matrix m(dims[v], ranks[v]);
+        std::memcpy(m.data.data(), f + o, sizeof(double) * dims[v] * ranks[v]);
+        o += dims[v] * ranks[v];
+        u.factors.push_back(std::move(m));
+    }
+    return u;
+}
+
+void from_factors(const FactorSet& u, double* out) {
+    std::size_t o = 0;
+    for (const Matrix& m : u.factors) {
+        std::memcpy(out + o, m.data.data(), sizeof(double) * m.data.size());
+        o += m.data.size();
+    }
+}
+
+thread_local int64_t g_payload = 0;
+
+}  // namespace
+
+extern "C" {
+
+int64_t ref_last_payload() { return g_payload; }
+
+// SparseTensor ctor (sparse_tensor.cpp:18-41).  Handle owns the tensor.
+int ref_tensor_create(int n, const uint64_t* dims, uint64_t nnz, const uint32_t* coords,
+                      const double* vals, void** out) {
+    try {
+        std::vector<std::size_t> d(dims, dims + n);
+        std::vector<index_t> c(coords, coords + nnz * n);
+        std::vector<double> v(vals, vals + nnz);
+        *out = new RefTensor{SparseTensor(std::move(d), std::move(c), std::move(v))};
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+int ref_gen_synthetic(int n, const uint64_t* dims, uint64_t nnz, uint64_t seed, void** out) {
+    try {
+        std::vector<std::size_t> d(dims, dims + n);
+        *out = new RefTensor{gen_synthetic(d, nnz, seed)};
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+void ref_tensor_destroy(void* h) { delete static_cast<RefTensor*>(h); }
+
+uint64_t ref_tensor_nnz(void* h) { return static_cast<RefTensor*>(h)->x.nnz(); }
+
+void ref_tensor_export(void* h, uint32_t* coords, double* vals) {
+    const SparseTensor& x = static_cast<RefTensor*>(h)->x;
+    for (std::size_t e = 0; e < x.nnz(); ++e) {
+        vals[e] = x.value(e);
+        for (std::size_t m = 0; m < x.order(); ++m) coords[e * x.order() + m] = x.coord(e, m);
+    }
+}
+
+void ref_tensor_buckets(void* h, int mode, uint64_t* offsets, uint64_t* entries) {
+    const SparseTensor& x = static_cast<RefTensor*>(h)->x;
+    const auto& b = x.mode_bucket(mode);
+    for (std::size_t i = 0; i < b.offsets.size(); ++i) offsets[i] = b.offsets[i];
+    for (std::size_t i = 0; i < b.entries.size(); ++i) entries[i] = b.entries[i];
+}
+
+double ref_norm_sq(void* h) { return norm_sq(static_cast<RefTensor*>(h)->x); }
+
+int ref_ttmc_core(void* h, const uint64_t* ranks, const double* factors, double* core) {
+    try {
+        const SparseTensor& x = static_cast<RefTensor*>(h)->x;
+        const int n = static_cast<int>(x.order());
+        std::vector<uint64_t> dims(x.dims().begin(), x.dims().end());
+        CoreTensor g = ttmc_core(x, to_factors(n, dims.data(), ranks, factors));
+        std::memcpy(core, g.data.data(), sizeof(double) * g.data.size());
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+// variant 0: ttmctc_elementwise with precomputed core (or none if core==NULL)
+// variant 1: ttmctc_matrix
+int ref_ttmctc(void* h, const uint64_t* ranks, const double* factors, int mode,
+               const double* core, int variant, double* a_out) {
+    try {
+        const SparseTensor& x = static_cast<RefTensor*>(h)->x;
+        const int n = static_cast<int>(x.order());
+        std::vector<uint64_t> dims(x.dims().begin(), x.dims().end());
+        FactorSet u = to_factors(n, dims.data(), ranks, factors);
+        Matrix a;
+        if (variant == 1) {
+            a = ttmctc_matrix(x, u, mode);
+        } else if (core) {
+            CoreTensor g(std::vector<std::size_t>(ranks, ranks + n));
+            std::memcpy(g.data.data(), core, sizeof(double) * g.data.size());
+            a = ttmctc_elementwise(x, u, mode, &g);
+        } else {
+            a = ttmctc_elementwise(x, u, mode);
+        }
+        std::memcpy(a_out, a.data.data(), sizeof(double) * a.data.size());
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+int ref_qr(uint64_t rows, uint64_t cols, const double* a, double* q) {
+    try {
+        Matrix m(rows, cols);
+        std::memcpy(m.data.data(), a, sizeof(double) * rows * cols);
+        Matrix r = qr_orthonormal(m);
+        std::memcpy(q, r.data.data(), sizeof(double) * rows * cols);
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+double ref_subspace_distance(uint64_t rows, uint64_t cols, const double* u, const double* v) {
+    Matrix a(rows, cols), b(rows, cols);
+    std::memcpy(a.data.data(), u, sizeof(double) * rows * cols);
+    std::memcpy(b.data.data(), v, sizeof(double) * rows * cols);
+    return subspace_distance(a, b);
+}
+
+int ref_random_factors(int n, const uint64_t* dims, const uint64_t* ranks, uint64_t seed,
+                       double* out) {
+    try {
+        FactorSet u = random_factors(std::vector<std::size_t>(dims, dims + n),
+                                     std::vector<std::size_t>(ranks, ranks + n), seed);
+        from_factors(u, out);
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+void ref_raw_stream(uint64_t seed, uint64_t n, uint64_t* out) {
+    Rng r(seed);
+    for (uint64_t i = 0; i < n; ++i) out[i] = r.raw();
+}
+
+void ref_normal_stream(uint64_t seed, uint64_t n, double* out) {
+    Rng r(seed);
+    for (uint64_t i = 0; i < n; ++i) out[i] = r.normal();
+}
+
+uint64_t ref_mix_seed(uint64_t seed, uint64_t salt) { return mix_seed(seed, salt); }
+
+// tucker::hoqri (solvers.cpp:217-219) with random init from `seed`.  Fills the
+// final model and the per-sweep trace.  kernel: 0 element-wise, 1 matrix.
+int ref_hoqri(void* h, const uint64_t* ranks, uint64_t max_sweeps, double tol, uint64_t seed,
+              int kernel, double* factors_out, double* core_out, uint64_t* sweeps_done,
+              double* initial_objective, double* objective, double* fit, double* drift,
+              double* elapsed_s) {
+    try {
+        const SparseTensor& x = static_cast<RefTensor*>(h)->x;
+        SolverConfig cfg;
+        cfg.ranks.assign(ranks, ranks + x.order());
+        cfg.max_sweeps = max_sweeps;
+        cfg.tol_fit_change = tol;
+        cfg.seed = seed;
+        cfg.kernel = kernel ? KernelVariant::kMatrix : KernelVariant::kElementwise;
+        SolveResult r = hoqri(x, cfg);
+        from_factors(r.model.factors, factors_out);
+        std::memcpy(core_out, r.model.core.data.data(), sizeof(double) * r.model.core.size());
+        *sweeps_done = r.trace.sweeps.size();
+        *initial_objective = r.trace.initial_objective;
+        for (std::size_t s = 0; s < r.trace.sweeps.size(); ++s) {
+            objective[s] = r.trace.sweeps[s].objective;
+            fit[s] = r.trace.sweeps[s].fit;
+            elapsed_s[s] = r.trace.sweeps[s].elapsed_s;
+            for (std::size_t m = 0; m < x.order(); ++m)
+                drift[s * x.order() + m] = r.trace.sweeps[s].drift[m];
+        }
+        return 0;
+    } catch (const DegenerateStateError& e) {
+        g_payload = static_cast<int64_t>(e.mode);
+        return 8;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+// Per-update replay with the reference's own kernels (the acceptance.cpp:268-304
+// pattern), recording the core and factors after every sweep.  Starts from the
+// given factors.
+int ref_hoqri_replay(void* h, const uint64_t* ranks, const double* init_factors,
+                     uint64_t sweeps, double* core_snap, double* factor_snap, double* drift) {
+    try {
+        const SparseTensor& x = static_cast<RefTensor*>(h)->x;
+        const int n = static_cast<int>(x.order());
+        std::vector<uint64_t> dims(x.dims().begin(), x.dims().end());
+        FactorSet u = to_factors(n, dims.data(), ranks, init_factors);
+        CoreTensor core = ttmc_core(x, u);
+        std::size_t ftotal = 0;
+        for (int v = 0; v < n; ++v) ftotal += dims[v] * ranks[v];
+        for (uint64_t s = 0; s < sweeps; ++s) {
+            for (int m = 0; m < n; ++m) {
+                Matrix a = ttmctc_elementwise(x, u, m, &core);
+                if (max_abs(a) == 0.0) {
+                    g_payload = m + 1;
+                    return 8;
+                }
+                Matrix old = std::move(u.factors[m]);
+                u.factors[m] = qr_orthonormal(a);
+                drift[s * n + m] = subspace_distance(u.factors[m], old);
+                core = ttmc_core(x, u);
+            }
+            std::memcpy(core_snap + s * core.size(), core.data.data(),
+                        sizeof(double) * core.size());
+            from_factors(u, factor_snap + s * ftotal);
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+// ---- timing helpers for the CPU baseline (bench.py) -------------------------
+// Times `reps` calls of ttmctc_elementwise(x, u, mode, &g) and of ttmc_core on
+// `threads` host threads.  With threads > 1 the nonzeros are split into
+// contiguous lexicographic slices, one reference SparseTensor per thread
+// (built before timing), and each thread calls the unmodified reference
+// kernel on its slice: the row/entry partitioning the reference's parallelism
+// contract allows.  Returns seconds per call (wall clock).
+struct RefSlices {
+    std::vector<SparseTensor> parts;
+};
+
+void* ref_slices_create(void* h, int threads) {
+    const SparseTensor& x = static_cast<RefTensor*>(h)->x;
+    auto* s = new RefSlices;
+    const std::size_t n = x.order(), nnz = x.nnz();
+    for (int t = 0; t < threads; ++t) {
+        std::size_t b = nnz * t / threads, e = nnz * (t + 1) / threads;
+        std::vector<index_t> c;
+        std::vector<double> v;
+        c.reserve((e - b) * n);
+        v.reserve(e - b);
+        for (std::size_t i = b; i < e; ++i) {
+            for (std::size_t m = 0; m < n; ++m) c.push_back(x.coord(i, m));
+            v.push_back(x.value(i));
+        }
+        s->parts.emplace_back(x.dims(), std::move(c), std::move(v));
+    }
+    return s;
+}
+
+void ref_slices_destroy(void* s) { delete static_cast<RefSlices*>(s); }
+
+// what: 0 = ttmctc_elementwise(mode, core given), 1 = ttmc_core
+double ref_slices_time(void* s, const uint64_t* ranks, const double* factors,
+                       const double* core, int mode, int what, int reps) {
+    auto* sl = static_cast<RefSlices*>(s);
+    const SparseTensor& x0 = sl->parts[0];
+    const int n = static_cast<int>(x0.order());
+    std::vector<uint64_t> dims(x0.dims().begin(), x0.dims().end());
+    FactorSet u = to_factors(n, dims.data(), ranks, factors);
+    CoreTensor g(std::vector<std::size_t>(ranks, ranks + n));
+    std::memcpy(g.data.data(), core, sizeof(double) * g.data.size());
+    auto t0 = std::chrono::steady_clock::now();
+    for (int r = 0; r < reps; ++r) {
+        std::vector<std::thread> th;
+        for (std::size_t t = 0; t < sl->parts.size(); ++t)
+            th.emplace_back([&, t] {
+                if (what == 0)
+                    (void)ttmctc_elementwise(sl->parts[t], u, mode, &g);
+                else
+                    (void)ttmc_core(sl->parts[t], u);
+            });
+        for (auto& t : th) t.join();
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    return std::chrono::duration<double>(t1 - t0).count() / reps;
+}
+
+double ref_time_qr(uint64_t rows, uint64_t cols, const double* a, int reps) {
+    Matrix m(rows, cols);
+    std::memcpy(m.data.data(), a, sizeof(double) * rows * cols);
+    auto t0 = std::chrono::steady_clock::now();
+    for (int r = 0; r < reps; ++r) {
+        Matrix q = qr_orthonormal(m);
+        Matrix d = matmul_tn(q, m);  // the drift product of subspace_distance
+        (void)nuclear_norm(d);
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    return std::chrono::duration<double>(t1 - t0).count() / reps;
+}
+
+}  // extern "C"

@@ -1,0 +1,176 @@
+/*
+ * hoqri_b200.h — the C-ABI of the B200 HOQRI engine (libhoqri_b200.so).
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * (arxiv 2510.16930, /root/reference/proj) is a C++ static library whose
+ * callers link `tucker::` symbols directly; it has no FFI.  Every entry point
+ * below replaces one reference function (cited as file:line, relative to
+ * /root/reference/proj).  The C++ shim libtucker_b200.so
+ * (paper_2510_16930_b200/csrc/tucker_shim.cpp) re-exposes the reference's
+ * `tucker::` signatures on top of this ABI, and the Python mirror
+ * (paper_2510_16930_b200/__init__.py) binds it with ctypes.
+ *
+ * Rules:
+ *  - Plain pointers and sizes only.  Pointers are HOST pointers unless the
+ *    name ends in `_dev`.  Sizes are uint64_t / int64_t.
+ *  - No exception crosses this boundary.  Every call returns an hq_status;
+ *    hq_last_error() holds a thread-local message and hq_last_error_payload()
+ *    the 1-based mode of a DEGENERATE error (errors.hpp:73-80) or the line of
+ *    a PARSE error (errors.hpp:17-22).
+ *  - Matrices are row-major (dense_core.hpp:10-22); factor sets are passed as
+ *    an array of N pointers, factor n of shape dims[n] x ranks[n]; the core is
+ *    K_1 x ... x K_N with the last mode fastest (dense_core.hpp:33-43).
+ *  - `stream` is a cudaStream_t passed as an opaque pointer (NULL = the
+ *    library's default stream).  Calls that return host results synchronise
+ *    that stream before returning.
+ */
+#ifndef HOQRI_B200_H
+#define HOQRI_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* errors.hpp:9-70 taxonomy, plus device failures */
+typedef enum hq_status {
+    HQ_OK = 0,
+    HQ_ERR_SHAPE = 1,       /* ShapeError */
+    HQ_ERR_RANGE = 2,       /* RangeError */
+    HQ_ERR_VALUE = 3,       /* ValueError */
+    HQ_ERR_PARSE = 4,       /* ParseError (payload: line) */
+    HQ_ERR_CAPACITY = 5,    /* CapacityError */
+    HQ_ERR_CONTRACT = 6,    /* ContractError */
+    HQ_ERR_DIAGNOSTIC = 7,  /* DiagnosticError */
+    HQ_ERR_DEGENERATE = 8,  /* DegenerateStateError (payload: mode, 1-based) */
+    HQ_ERR_INFEASIBLE = 9,  /* InfeasibleError */
+    HQ_ERR_CUDA = 10,       /* CUDA runtime / kernel failure */
+    HQ_ERR_NCCL = 11,       /* NCCL failure (multi-GPU) */
+    HQ_ERR_INTERNAL = 12
+} hq_status;
+
+const char* hq_last_error(void);
+int64_t hq_last_error_payload(void);
+const char* hq_version(void);
+
+/* ---------------------------------------------------------------- tensor --
+ * Device-resident mirror of tucker::SparseTensor.  Creation validates the
+ * input (sparse_tensor.cpp:22-38: RANGE for a coordinate >= extent, VALUE for
+ * a non-finite value, SHAPE for order 0 / zero extent / size mismatch), sorts
+ * the entries lexicographically, merges duplicates by summing
+ * (sparse_tensor.cpp:43-71), builds every mode's buckets
+ * (sparse_tensor.cpp:73-89) and the mode-sorted streams the kernels read.
+ * All of it runs on the device.  Replaces SparseTensor::SparseTensor
+ * (sparse_tensor.hpp:37-38). */
+typedef struct hq_tensor hq_tensor;
+
+int hq_tensor_create(int order, const uint64_t* dims, uint64_t nnz, const uint32_t* coords,
+                     const double* values, void* stream, hq_tensor** out);
+/* same, but coords/values already in device memory (not modified) */
+int hq_tensor_create_dev(int order, const uint64_t* dims, uint64_t nnz,
+                         const uint32_t* coords_dev, const double* values_dev, void* stream,
+                         hq_tensor** out);
+int hq_tensor_destroy(hq_tensor* t);
+/* order, nnz after merging (sparse_tensor.hpp:40-42) */
+int hq_tensor_info(const hq_tensor* t, int* order, uint64_t* dims, uint64_t* nnz);
+/* sorted, merged entries (sparse_tensor.hpp:44-51): coords nnz*order, values nnz */
+int hq_tensor_export(const hq_tensor* t, uint32_t* coords, double* values);
+/* ModeBuckets (sparse_tensor.hpp:25-32): offsets dims[mode]+1, entries nnz */
+int hq_tensor_buckets(const hq_tensor* t, int mode, uint64_t* offsets, uint64_t* entries);
+/* norm_sq(const SparseTensor&) (sparse_tensor.hpp:69; sparse_tensor.cpp:91-95) */
+int hq_tensor_norm_sq(const hq_tensor* t, double* out);
+
+/* --------------------------------------------------------------- kernels --
+ * ttmc_core (kernels.hpp:46; kernels.cpp:40-84): core = X x {U^T}. */
+int hq_ttmc_core(const hq_tensor* t, const double* const* factors, const uint64_t* ranks,
+                 double* core_out);
+/* ttmctc_elementwise (kernels.hpp:52-54) and ttmctc_matrix (kernels.hpp:59-60):
+ * A = Y_(n) G_(n)^T.  `core` may be NULL (then it is computed from the factors,
+ * kernels.cpp:92-101).  `variant` 0 = element-wise, 1 = matrix; both map to
+ * the same device kernel (same linear map, results agree to 1e-11,
+ * kernels_test.cpp:167-190). */
+int hq_ttmctc(const hq_tensor* t, const double* const* factors, const uint64_t* ranks,
+              int mode, const double* core, int variant, double* a_out);
+
+/* ------------------------------------------------------------ dense core --
+ * qr_orthonormal (dense_core.hpp:60; dense_core.cpp:127-198): orthonormal basis
+ * of col(A) with R_kk >= 0.  CholeskyQR2 on the device; a device Householder
+ * QR with the reference's seeded rank-deficiency fill when CholeskyQR2 would
+ * lose accuracy.  SHAPE if rows < cols. */
+int hq_qr_orthonormal(uint64_t rows, uint64_t cols, const double* a, double* q_out);
+/* subspace_distance (manifold.hpp:34-36; manifold.cpp:55-60) */
+int hq_subspace_distance(uint64_t rows, uint64_t cols, const double* u, const double* v,
+                         double* out);
+/* random_factors (solvers.hpp:72-73; solvers.cpp:182-195): seeded Gaussian
+ * (bit-exact tucker::Rng stream, generated on the host), QR on the device. */
+int hq_random_factors(int order, const uint64_t* dims, const uint64_t* ranks, uint64_t seed,
+                      double* const* factors_out);
+
+/* ---------------------------------------------------------------- solver --
+ * SolverConfig (solvers.hpp:17-28).  init: 0 random (seeded), 1 HOSVD (not
+ * supported on this engine: returns CAPACITY beyond the desk-scale cap and
+ * SHAPE otherwise... see DESIGN.md), 2 caller-supplied factors. */
+typedef struct hq_config {
+    int order;
+    uint64_t ranks[8];
+    uint64_t max_sweeps;      /* default 100 */
+    double tol_fit_change;    /* default 1e-12 */
+    uint64_t seed;
+    int init;                 /* 0 random, 2 = use init_factors */
+    int kernel;               /* 0 element-wise, 1 matrix (same device path) */
+    int trace_gradients;      /* per-update diagnostics (ModeUpdateRecord) */
+    double tol_grad;          /* gradient stop, implies tracing */
+} hq_config;
+
+void hq_config_default(hq_config* cfg);
+
+/* IterationTrace (solvers.hpp:37-63), caller-allocated for max_sweeps sweeps */
+typedef struct hq_trace {
+    double data_norm_sq;
+    double initial_objective;
+    uint64_t sweeps;           /* filled */
+    double* objective;         /* [max_sweeps] */
+    double* fit;               /* [max_sweeps] */
+    double* drift;             /* [max_sweeps * order] */
+    double* grad_norm_sq;      /* [max_sweeps * order] or NULL */
+    double* elapsed_s;         /* [max_sweeps] or NULL: cumulative device time */
+} hq_trace;
+
+/* hoqri (solvers.hpp:80; solvers.cpp:50-178, 217-219): the whole solve on the
+ * device.  factors_out: N host buffers; core_out: prod K doubles. */
+int hq_hoqri(const hq_tensor* t, const hq_config* cfg, const double* const* init_factors,
+             double* const* factors_out, double* core_out, hq_trace* trace);
+
+/* fit_error (solvers.hpp:87; solvers.cpp:225-236) */
+int hq_fit_error(double data_norm_sq, uint64_t core_size, const double* core, double* out);
+
+/* ------------------------------------------------ device-resident solver --
+ * The same solve, split so that a benchmark can keep every operand in HBM and
+ * time sweeps and single kernels on its own stream. */
+typedef struct hq_solver hq_solver;
+
+int hq_solver_create(const hq_tensor* t, const hq_config* cfg,
+                     const double* const* init_factors, void* stream, hq_solver** out);
+int hq_solver_destroy(hq_solver* s);
+/* runs `sweeps` sweeps asynchronously on the solver's stream (CUDA graph) */
+int hq_solver_run(hq_solver* s, uint64_t sweeps);
+/* waits, checks the device status word, and reports a DEGENERATE error */
+int hq_solver_sync(hq_solver* s);
+/* launches only the fused sparse mode pass (TTMcTC + Gram + core projection)
+ * for `mode` on the solver's stream: the dominant kernel, for timing */
+int hq_solver_launch_mode_pass(hq_solver* s, int mode);
+/* launches only the TTMcTC kernel for `mode` (A written to device scratch) */
+int hq_solver_launch_ttmctc(hq_solver* s, int mode);
+/* number of device kernels one sweep launches */
+int hq_solver_launches_per_sweep(const hq_solver* s, uint64_t* out);
+int hq_solver_download(hq_solver* s, double* const* factors_out, double* core_out, hq_trace* trace);
+/* algorithmic work of one mode pass: flops and bytes (DESIGN.md roofline) */
+int hq_solver_mode_pass_work(const hq_solver* s, int mode, double* flops, double* bytes);
+int hq_solver_ttmctc_work(const hq_solver* s, int mode, double* flops, double* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HOQRI_B200_H */

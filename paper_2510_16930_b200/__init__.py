@@ -1,0 +1,623 @@
+"""B200-native HOQRI engine: Python mirror of the reference's `tucker::` API.
+
+The reference (arxiv 2510.16930, /root/reference/proj) is a C++ library whose
+public API is proj/include/tucker/*.hpp.  This module binds the engine's C-ABI
+(include/hoqri_b200.h, lib/libhoqri_b200.so) with ctypes and exposes the same
+names, argument meanings and error types, so the parity tests read like the
+reference's own tests:
+
+    SparseTensor(dims, coords, values)        sparse_tensor.hpp:37-57
+    load_tns / write_tns                      sparse_tensor.hpp:76-83
+    norm_sq(SparseTensor | CoreTensor)        sparse_tensor.hpp:69, dense_core.hpp:48
+    ttmc_core(x, u)                           kernels.hpp:46
+    ttmctc_elementwise(x, u, mode, core)      kernels.hpp:52-54
+    ttmctc_matrix(x, u, mode)                 kernels.hpp:59-60
+    qr_orthonormal(a)                         dense_core.hpp:60
+    subspace_distance(u, v)                   manifold.hpp:34-36
+    random_factors(dims, ranks, seed)         solvers.hpp:72-73
+    hoqri(x, config)                          solvers.hpp:80
+    fit_error(x, model)                       solvers.hpp:87
+
+All compute runs in the CUDA engine.  There is no CPU fallback: importing
+works without a GPU (so the C-ABI can be inspected), but every compute call
+raises when the engine cannot run.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import os
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "lib", "libhoqri_b200.so")
+
+# ---------------------------------------------------------------- errors --
+# errors.hpp:9-70
+
+
+class Error(RuntimeError):
+    pass
+
+
+class ShapeError(Error):
+    pass
+
+
+class RangeError(Error):
+    pass
+
+
+class ValueError_(Error):
+    pass
+
+
+class ParseError(Error):
+    def __init__(self, what, line_number=0):
+        super().__init__(f"line {line_number}: {what}" if line_number else what)
+        self.line_number = line_number
+
+
+class CapacityError(Error):
+    pass
+
+
+class ContractError(Error):
+    pass
+
+
+class DiagnosticError(Error):
+    pass
+
+
+class DegenerateStateError(Error):
+    def __init__(self, mode_1based, what=None):
+        super().__init__(what or f"degenerate state: TTMcTC output is identically zero for mode {mode_1based}")
+        self.mode = mode_1based
+
+
+class InfeasibleError(Error):
+    pass
+
+
+class DeviceError(Error):
+    """CUDA / NCCL failure inside the engine."""
+
+
+_STATUS = {1: ShapeError, 2: RangeError, 3: ValueError_, 5: CapacityError, 6: ContractError, 7: DiagnosticError,
+           9: InfeasibleError, 10: DeviceError, 11: DeviceError, 12: Error}
+
+# ----------------------------------------------------------------- C-ABI --
+_u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+_u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+
+
+class HqConfig(C.Structure):
+    _fields_ = [("order", C.c_int), ("ranks", C.c_uint64 * 8), ("max_sweeps", C.c_uint64),
+                ("tol_fit_change", C.c_double), ("seed", C.c_uint64), ("init", C.c_int), ("kernel", C.c_int),
+                ("trace_gradients", C.c_int), ("tol_grad", C.c_double)]
+
+
+class HqTrace(C.Structure):
+    _fields_ = [("data_norm_sq", C.c_double), ("initial_objective", C.c_double), ("sweeps", C.c_uint64),
+                ("objective", C.c_void_p), ("fit", C.c_void_p), ("drift", C.c_void_p),
+                ("grad_norm_sq", C.c_void_p), ("elapsed_s", C.c_void_p)]
+
+
+EXPORTED_SYMBOLS = [
+    "hq_last_error", "hq_last_error_payload", "hq_version",
+    "hq_tensor_create", "hq_tensor_create_dev", "hq_tensor_destroy", "hq_tensor_info", "hq_tensor_export",
+    "hq_tensor_buckets", "hq_tensor_norm_sq",
+    "hq_ttmc_core", "hq_ttmctc", "hq_qr_orthonormal", "hq_subspace_distance", "hq_random_factors",
+    "hq_config_default", "hq_hoqri", "hq_fit_error",
+    "hq_solver_create", "hq_solver_destroy", "hq_solver_run", "hq_solver_sync", "hq_solver_launch_mode_pass",
+    "hq_solver_launch_ttmctc", "hq_solver_launches_per_sweep", "hq_solver_download", "hq_solver_mode_pass_work",
+    "hq_solver_ttmctc_work",
+]
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> C.CDLL:
+    """Loads lib/libhoqri_b200.so (builds it in-tree first if it is missing)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        from . import build
+        build.build_engine()
+    L = C.CDLL(path)
+    vp, pp = C.c_void_p, C.POINTER(C.c_void_p)
+    L.hq_last_error.restype = C.c_char_p
+    L.hq_last_error_payload.restype = C.c_int64
+    L.hq_version.restype = C.c_char_p
+    L.hq_tensor_create.argtypes = [C.c_int, _u64p, C.c_uint64, vp, vp, vp, pp]
+    L.hq_tensor_create_dev.argtypes = [C.c_int, _u64p, C.c_uint64, vp, vp, vp, pp]
+    L.hq_tensor_destroy.argtypes = [vp]
+    L.hq_tensor_info.argtypes = [vp, C.POINTER(C.c_int), _u64p, C.POINTER(C.c_uint64)]
+    L.hq_tensor_export.argtypes = [vp, vp, vp]
+    L.hq_tensor_buckets.argtypes = [vp, C.c_int, _u64p, vp]
+    L.hq_tensor_norm_sq.argtypes = [vp, C.POINTER(C.c_double)]
+    L.hq_ttmc_core.argtypes = [vp, vp, _u64p, _f64p]
+    L.hq_ttmctc.argtypes = [vp, vp, _u64p, C.c_int, vp, C.c_int, _f64p]
+    L.hq_qr_orthonormal.argtypes = [C.c_uint64, C.c_uint64, _f64p, _f64p]
+    L.hq_subspace_distance.argtypes = [C.c_uint64, C.c_uint64, _f64p, _f64p, C.POINTER(C.c_double)]
+    L.hq_random_factors.argtypes = [C.c_int, _u64p, _u64p, C.c_uint64, vp]
+    L.hq_config_default.argtypes = [C.POINTER(HqConfig)]
+    L.hq_config_default.restype = None
+    L.hq_hoqri.argtypes = [vp, C.POINTER(HqConfig), vp, vp, vp, C.POINTER(HqTrace)]
+    L.hq_fit_error.argtypes = [C.c_double, C.c_uint64, _f64p, C.POINTER(C.c_double)]
+    L.hq_solver_create.argtypes = [vp, C.POINTER(HqConfig), vp, vp, pp]
+    L.hq_solver_destroy.argtypes = [vp]
+    L.hq_solver_run.argtypes = [vp, C.c_uint64]
+    L.hq_solver_sync.argtypes = [vp]
+    L.hq_solver_launch_mode_pass.argtypes = [vp, C.c_int]
+    L.hq_solver_launch_ttmctc.argtypes = [vp, C.c_int]
+    L.hq_solver_launches_per_sweep.argtypes = [vp, C.POINTER(C.c_uint64)]
+    L.hq_solver_download.argtypes = [vp, vp, vp, C.POINTER(HqTrace)]
+    L.hq_solver_mode_pass_work.argtypes = [vp, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.hq_solver_ttmctc_work.argtypes = [vp, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status == 0:
+        return
+    L = load_library()
+    msg = L.hq_last_error().decode(errors="replace")
+    payload = int(L.hq_last_error_payload())
+    if status == 8:
+        raise DegenerateStateError(payload, msg)
+    if status == 4:
+        raise ParseError(msg, payload)
+    raise _STATUS.get(status, Error)(msg)
+
+
+def _ptr_array(arrs):
+    a = (C.c_void_p * max(1, len(arrs)))()
+    for i, x in enumerate(arrs):
+        a[i] = x.ctypes.data
+    return a
+
+
+# ----------------------------------------------------------------- types --
+@dataclasses.dataclass
+class CoreTensor:
+    """Dense core, lexicographic layout with the last mode fastest (dense_core.hpp:33-43)."""
+    ranks: List[int]
+    data: np.ndarray
+
+    def order(self):
+        return len(self.ranks)
+
+    def size(self):
+        return int(self.data.size)
+
+    def as_array(self):
+        return self.data.reshape(tuple(self.ranks))
+
+
+@dataclasses.dataclass
+class FactorSet:
+    """Per-mode factors, factor n of shape I_n x K_n (dense_core.hpp:45-54)."""
+    factors: List[np.ndarray]
+
+    def order(self):
+        return len(self.factors)
+
+    def orthonormality_defect(self):
+        worst = 0.0
+        for u in self.factors:
+            g = u.T @ u
+            worst = max(worst, float(np.abs(g - np.eye(g.shape[0])).max()) if g.size else 0.0)
+        return worst
+
+
+class SparseTensor:
+    """Device-resident COO tensor (sparse_tensor.hpp:20-66).  Construction
+    validates, sorts, merges duplicates and builds all mode layouts on the GPU."""
+
+    def __init__(self, dims: Sequence[int], coords, values, *, _handle=None):
+        L = load_library()
+        self._dims = [int(d) for d in dims]
+        if _handle is not None:
+            self._h = _handle
+        else:
+            d = np.ascontiguousarray(np.asarray(self._dims, dtype=np.uint64))
+            c = np.ascontiguousarray(np.asarray(coords, dtype=np.uint32)).reshape(-1)
+            v = np.ascontiguousarray(np.asarray(values, dtype=np.float64)).reshape(-1)
+            n = len(self._dims)
+            if n == 0:
+                raise ShapeError("sparse tensor needs at least one mode")
+            if c.size != v.size * n:
+                raise ShapeError("coordinate array does not match entry count")
+            h = C.c_void_p()
+            _check(L.hq_tensor_create(n, d, v.size, c.ctypes.data if c.size else None,
+                                      v.ctypes.data if v.size else None, None, C.byref(h)))
+            self._h = h
+        order = C.c_int(0)
+        nnz = C.c_uint64(0)
+        dd = np.zeros(8, np.uint64)
+        _check(L.hq_tensor_info(self._h, C.byref(order), dd, C.byref(nnz)))
+        self._nnz = int(nnz.value)
+        self._coords = None
+        self._values = None
+
+    @classmethod
+    def from_device(cls, dims, coords_ptr: int, values_ptr: int, nnz: int, stream: int = 0):
+        """Builds from COO already in device memory (e.g. torch tensors' data_ptr())."""
+        L = load_library()
+        d = np.ascontiguousarray(np.asarray(dims, dtype=np.uint64))
+        h = C.c_void_p()
+        _check(L.hq_tensor_create_dev(d.size, d, nnz, coords_ptr, values_ptr, stream or None, C.byref(h)))
+        return cls(dims, None, None, _handle=h)
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                load_library().hq_tensor_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def order(self):
+        return len(self._dims)
+
+    def dims(self):
+        return list(self._dims)
+
+    def nnz(self):
+        return self._nnz
+
+    def _export(self):
+        if self._coords is None:
+            c = np.empty(max(1, self._nnz * self.order()), np.uint32)
+            v = np.empty(max(1, self._nnz), np.float64)
+            _check(load_library().hq_tensor_export(self._h, c.ctypes.data, v.ctypes.data))
+            self._coords = c[: self._nnz * self.order()].reshape(self._nnz, self.order())
+            self._values = v[: self._nnz]
+        return self._coords, self._values
+
+    def values(self):
+        return self._export()[1]
+
+    def coords(self):
+        return self._export()[0]
+
+    def value(self, e):
+        return float(self.values()[e])
+
+    def coord(self, e, mode):
+        return int(self.coords()[e, mode])
+
+    def coord_row(self, e):
+        return self.coords()[e]
+
+    def buckets_built(self):
+        return True
+
+    def mode_bucket(self, mode):
+        """(offsets[I_n + 1], entries[nnz]) as in ModeBuckets (sparse_tensor.hpp:25-32)."""
+        off = np.empty(self._dims[mode] + 1, np.uint64)
+        ent = np.empty(max(1, self._nnz), np.uint64)
+        _check(load_library().hq_tensor_buckets(self._h, mode, off, ent.ctypes.data))
+        return off, ent[: self._nnz]
+
+
+def norm_sq(x):
+    if isinstance(x, SparseTensor):
+        out = C.c_double(0)
+        _check(load_library().hq_tensor_norm_sq(x.handle, C.byref(out)))
+        return out.value
+    if isinstance(x, CoreTensor):
+        return float(np.dot(x.data, x.data))
+    raise TypeError("norm_sq expects a SparseTensor or CoreTensor")
+
+
+def _factors_of(u):
+    fs = u.factors if isinstance(u, FactorSet) else list(u)
+    return [np.ascontiguousarray(np.asarray(f, dtype=np.float64)) for f in fs]
+
+
+def _check_factors(x: SparseTensor, fs):
+    # kernels.cpp:12-22
+    if len(fs) != x.order():
+        raise ShapeError("factor count does not match tensor order")
+    for n, f in enumerate(fs):
+        if f.ndim != 2 or f.shape[0] != x.dims()[n]:
+            raise ShapeError(f"factor {n + 1} has {f.shape[0]} rows, tensor extent is {x.dims()[n]}")
+        if f.shape[1] == 0:
+            raise ShapeError("factor with zero columns")
+
+
+def ttmc_core(x: SparseTensor, u) -> CoreTensor:
+    fs = _factors_of(u)
+    _check_factors(x, fs)
+    ranks = np.array([f.shape[1] for f in fs], np.uint64)
+    out = np.empty(int(np.prod(ranks)), np.float64)
+    _check(load_library().hq_ttmc_core(x.handle, _ptr_array(fs), ranks, out))
+    return CoreTensor([int(r) for r in ranks], out)
+
+
+def ttmctc_elementwise(x: SparseTensor, u, mode: int, precomputed_core: Optional[CoreTensor] = None,
+                       ws=None) -> np.ndarray:
+    fs = _factors_of(u)
+    _check_factors(x, fs)
+    if mode < 0 or mode >= x.order():
+        raise RangeError("ttmctc: mode out of range")
+    ranks = np.array([f.shape[1] for f in fs], np.uint64)
+    core_ptr = None
+    if precomputed_core is not None:
+        if list(precomputed_core.ranks) != [int(r) for r in ranks]:
+            raise ShapeError("precomputed core ranks do not match the factors")
+        cd = np.ascontiguousarray(precomputed_core.data, dtype=np.float64)
+        core_ptr = cd.ctypes.data
+    a = np.empty((x.dims()[mode], int(ranks[mode])), np.float64)
+    _check(load_library().hq_ttmctc(x.handle, _ptr_array(fs), ranks, mode, core_ptr, 0, a.reshape(-1)))
+    return a
+
+
+def ttmctc_matrix(x: SparseTensor, u, mode: int, ws=None) -> np.ndarray:
+    fs = _factors_of(u)
+    _check_factors(x, fs)
+    if mode < 0 or mode >= x.order():
+        raise RangeError("ttmctc: mode out of range")
+    ranks = np.array([f.shape[1] for f in fs], np.uint64)
+    a = np.empty((x.dims()[mode], int(ranks[mode])), np.float64)
+    _check(load_library().hq_ttmctc(x.handle, _ptr_array(fs), ranks, mode, None, 1, a.reshape(-1)))
+    return a
+
+
+def qr_orthonormal(a) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if a.ndim != 2:
+        raise ShapeError("qr_orthonormal: matrix expected")
+    q = np.empty_like(a)
+    if a.shape[1] == 0:
+        if a.shape[0] < a.shape[1]:
+            raise ShapeError("qr_orthonormal: need rows >= cols")
+        return q
+    _check(load_library().hq_qr_orthonormal(a.shape[0], a.shape[1], a.reshape(-1), q.reshape(-1)))
+    return q
+
+
+def subspace_distance(u, v) -> float:
+    u = np.ascontiguousarray(np.asarray(u, dtype=np.float64))
+    v = np.ascontiguousarray(np.asarray(v, dtype=np.float64))
+    if u.shape != v.shape:
+        raise ShapeError("subspace_distance: shapes differ")
+    out = C.c_double(0)
+    _check(load_library().hq_subspace_distance(u.shape[0], u.shape[1], u.reshape(-1), v.reshape(-1), C.byref(out)))
+    return out.value
+
+
+def random_factors(dims, ranks, seed) -> FactorSet:
+    if len(dims) != len(ranks):
+        raise ShapeError("random_factors: dims/ranks length mismatch")
+    d = np.ascontiguousarray(np.asarray(dims, np.uint64))
+    r = np.ascontiguousarray(np.asarray(ranks, np.uint64))
+    fs = [np.empty((int(a), int(b)), np.float64) for a, b in zip(d, r)]
+    _check(load_library().hq_random_factors(d.size, d, r, int(seed) & (2**64 - 1), _ptr_array(fs)))
+    return FactorSet(fs)
+
+
+# ---------------------------------------------------------------- solver --
+INIT_RANDOM, INIT_HOSVD, INIT_GIVEN = 0, 1, 2
+KERNEL_ELEMENTWISE, KERNEL_MATRIX = 0, 1
+
+
+@dataclasses.dataclass
+class SolverConfig:
+    """solvers.hpp:17-28"""
+    ranks: List[int]
+    max_sweeps: int = 100
+    tol_fit_change: float = 1e-12
+    seed: int = 0
+    init: int = INIT_RANDOM
+    trace_gradients: bool = False
+    kernel: int = KERNEL_ELEMENTWISE
+    tol_grad: float = 0.0
+
+    def to_c(self, order):
+        c = HqConfig()
+        load_library().hq_config_default(C.byref(c))
+        c.order = order
+        for i, k in enumerate(self.ranks):
+            c.ranks[i] = int(k)
+        c.max_sweeps = int(self.max_sweeps)
+        c.tol_fit_change = float(self.tol_fit_change)
+        c.seed = int(self.seed) & (2**64 - 1)
+        c.init = int(self.init)
+        c.kernel = int(self.kernel)
+        c.trace_gradients = int(bool(self.trace_gradients))
+        c.tol_grad = float(self.tol_grad)
+        return c
+
+
+@dataclasses.dataclass
+class TuckerModel:
+    factors: FactorSet
+    core: CoreTensor
+    data_norm_sq: float = 0.0
+
+
+@dataclasses.dataclass
+class SweepRecord:
+    sweep: int
+    elapsed_s: float
+    objective: float
+    fit: float
+    total_grad_norm_sq: float
+    grad_norm_sq: List[float]
+    drift: List[float]
+
+
+@dataclasses.dataclass
+class IterationTrace:
+    data_norm_sq: float
+    initial_objective: float
+    sweeps: List[SweepRecord]
+    updates: list
+
+
+@dataclasses.dataclass
+class SolveResult:
+    model: TuckerModel
+    trace: IterationTrace
+
+
+def _check_ranks(x: SparseTensor, ranks):
+    # solvers.cpp:22-30
+    if len(ranks) != x.order():
+        raise ShapeError("rank count does not match tensor order")
+    for n, k in enumerate(ranks):
+        if k < 1 or k > x.dims()[n]:
+            raise ShapeError(f"rank for mode {n + 1} must lie in [1, {x.dims()[n]}]")
+
+
+class _TraceBuffers:
+    def __init__(self, sweeps, order):
+        self.obj = np.zeros(max(1, sweeps))
+        self.fit = np.zeros(max(1, sweeps))
+        self.drift = np.zeros(max(1, sweeps * order))
+        self.grad = np.zeros(max(1, sweeps * order))
+        self.el = np.zeros(max(1, sweeps))
+        self.c = HqTrace(0.0, 0.0, 0, self.obj.ctypes.data, self.fit.ctypes.data, self.drift.ctypes.data,
+                         self.grad.ctypes.data, self.el.ctypes.data)
+
+    def to_trace(self, order):
+        s = int(self.c.sweeps)
+        recs = []
+        for i in range(s):
+            g = [float(v) for v in self.grad[i * order:(i + 1) * order]]
+            recs.append(SweepRecord(i + 1, float(self.el[i]), float(self.obj[i]), float(self.fit[i]), float(sum(g)), g,
+                                    [float(v) for v in self.drift[i * order:(i + 1) * order]]))
+        return IterationTrace(float(self.c.data_norm_sq), float(self.c.initial_objective), recs, [])
+
+
+def hoqri(x: SparseTensor, config: SolverConfig, init_factors: Optional[Sequence[np.ndarray]] = None) -> SolveResult:
+    """tucker::hoqri (solvers.hpp:80; solvers.cpp:50-178, 217-219), on the device."""
+    _check_ranks(x, config.ranks)
+    if config.max_sweeps < 1:
+        raise ShapeError("max_sweeps must be at least 1")
+    if config.tol_fit_change < 0:
+        raise ShapeError("tolerance must be nonnegative")
+    L = load_library()
+    n = x.order()
+    cfg = config.to_c(n)
+    init_arr = None
+    if init_factors is not None:
+        fs0 = _factors_of(init_factors)
+        _check_factors(x, fs0)
+        cfg.init = INIT_GIVEN
+        init_arr = _ptr_array(fs0)
+    fs = [np.empty((x.dims()[v], int(config.ranks[v])), np.float64) for v in range(n)]
+    core = np.empty(int(np.prod(config.ranks)), np.float64)
+    tb = _TraceBuffers(int(config.max_sweeps), n)
+    _check(L.hq_hoqri(x.handle, C.byref(cfg), init_arr, _ptr_array(fs), core.ctypes.data, C.byref(tb.c)))
+    trace = tb.to_trace(n)
+    model = TuckerModel(FactorSet(fs), CoreTensor([int(k) for k in config.ranks], core), trace.data_norm_sq)
+    return SolveResult(model, trace)
+
+
+def fit_error(x: SparseTensor, model: TuckerModel) -> float:
+    """solvers.cpp:225-236"""
+    if model.factors.order() != x.order():
+        raise ShapeError("fit_error: model order does not match the tensor")
+    out = C.c_double(0)
+    d = np.ascontiguousarray(model.core.data, dtype=np.float64)
+    _check(load_library().hq_fit_error(float(model.data_norm_sq), d.size, d, C.byref(out)))
+    return out.value
+
+
+# ---------------------------------------------------- device-resident API --
+class Solver:
+    """Device-resident solve for benchmarks: every operand stays in HBM; sweeps
+    and single kernels are launched on `stream` (a cudaStream_t as int)."""
+
+    def __init__(self, x: SparseTensor, config: SolverConfig, init_factors=None, stream: int = 0):
+        L = load_library()
+        self.x = x
+        self.n = x.order()
+        self.config = config
+        cfg = config.to_c(self.n)
+        arr = None
+        if init_factors is not None:
+            fs0 = _factors_of(init_factors)
+            cfg.init = INIT_GIVEN
+            arr = _ptr_array(fs0)
+            self._keep = fs0
+        h = C.c_void_p()
+        _check(L.hq_solver_create(x.handle, C.byref(cfg), arr, stream or None, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                load_library().hq_solver_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    def run(self, sweeps):
+        _check(load_library().hq_solver_run(self._h, int(sweeps)))
+
+    def sync(self):
+        _check(load_library().hq_solver_sync(self._h))
+
+    def launch_mode_pass(self, mode):
+        _check(load_library().hq_solver_launch_mode_pass(self._h, mode))
+
+    def launches_per_sweep(self):
+        out = C.c_uint64(0)
+        _check(load_library().hq_solver_launches_per_sweep(self._h, C.byref(out)))
+        return int(out.value)
+
+    def mode_pass_work(self, mode):
+        f, b = C.c_double(0), C.c_double(0)
+        _check(load_library().hq_solver_mode_pass_work(self._h, mode, C.byref(f), C.byref(b)))
+        return f.value, b.value
+
+    def ttmctc_work(self, mode):
+        f, b = C.c_double(0), C.c_double(0)
+        _check(load_library().hq_solver_ttmctc_work(self._h, mode, C.byref(f), C.byref(b)))
+        return f.value, b.value
+
+    def download(self):
+        fs = [np.empty((self.x.dims()[v], int(self.config.ranks[v])), np.float64) for v in range(self.n)]
+        core = np.empty(int(np.prod(self.config.ranks)), np.float64)
+        tb = _TraceBuffers(int(self.config.max_sweeps), self.n)
+        _check(load_library().hq_solver_download(self._h, _ptr_array(fs), core.ctypes.data, C.byref(tb.c)))
+        trace = tb.to_trace(self.n)
+        return SolveResult(TuckerModel(FactorSet(fs), CoreTensor(list(self.config.ranks), core), trace.data_norm_sq),
+                           trace)
+
+
+# ------------------------------------------------------------- .tns I/O --
+def load_tns(source, dims_override: Optional[Sequence[int]] = None) -> SparseTensor:
+    """sparse_tensor.cpp:136-215: text parse on the host, build on the device."""
+    from .tns import parse_tns
+    dims, coords, vals = parse_tns(source, dims_override)
+    return SparseTensor(dims, coords, vals)
+
+
+def write_tns(out, x: SparseTensor):
+    """sparse_tensor.cpp:224-235"""
+    c, v = x._export()
+    lines = ["dims: " + " ".join(str(d) for d in x.dims())]
+    for e in range(x.nnz()):
+        lines.append(" ".join(str(int(i) + 1) for i in c[e]) + " " + ("%.17g" % v[e]))
+    text = "\n".join(lines) + "\n"
+    if hasattr(out, "write"):
+        out.write(text)
+    else:
+        with open(out, "w") as f:
+            f.write(text)

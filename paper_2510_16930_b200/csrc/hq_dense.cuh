@@ -1,0 +1,76 @@
+// hq_dense.cuh — tall-skinny orthogonalisation and the K x K steps.
+#pragma once
+
+#include "hq_plan.cuh"
+
+namespace hq {
+
+constexpr int kMaxRank = 32;
+constexpr int kAcc = (kMaxRank * kMaxRank + 255) / 256;  // K*K entries per thread (256 threads)
+
+// CholeskyQR2 of A (rows x K) with fused side products, all on the device.
+// Scratch owned by the caller (sizes from dense_scratch_doubles()).
+struct QrScratch {
+    double* wpart;   // [dense slots][K*K]
+    double* w;       // K*K
+    double* r1inv;   // K*K
+    double* rinv;    // K*K
+    double* ppart;   // [dense slots][K*K]
+    double* maxv;    // 1
+    double* hh;      // Householder workspace: rows*K + rows (reflectors) + K
+};
+
+int dense_slots();
+
+// W = sum of `nslots` partial K*K slots (fixed order) and max over max partials
+void launch_reduce_pass(const double* mpart, int mlen, const double* wpart, int wlen, const double* maxpart,
+                        int nslots, double* m_out, double* w_out, double* max_out, const DevStatus* st, int run_if,
+                        cudaStream_t s);
+// W = A^T A and max|A| for a standalone QR
+void launch_gram(const double* A, uint64_t rows, int K, double* wpart, double* maxpart, const DevStatus* st,
+                 int run_if, cudaStream_t s);
+// degeneracy test (max|A| == 0 -> abort with the 1-based mode when
+// degenerate_mode > 0), Cholesky of W, inverse of R1; sets st->fallback when
+// CholeskyQR2 would lose accuracy
+void launch_chol1(const double* w, const double* maxv, int K, double* r1inv, DevStatus* st, int degenerate_mode,
+                  cudaStream_t s);
+// W2 partials of (A R1^-1)^T (A R1^-1)
+void launch_gram2(const double* A, uint64_t rows, int K, const double* r1inv, double* wpart, const DevStatus* st,
+                  cudaStream_t s);
+// Cholesky of W2 (reduced from partials), Rinv = R1inv R2inv; if m != null,
+// G_(n) = Rinv^T M refolded into the core layout (core_out)
+void launch_chol2(const double* wpart, int nslots, int K, const double* r1inv, double* rinv, const double* m,
+                  const ModeShape* sh, double* core_out, DevStatus* st, cudaStream_t s);
+// U = A Rinv (written to u_out when non-null); P partials of U^T U_old when
+// u_old non-null.  apply=false: U read from u_out (fallback drift).
+void launch_apply(const double* A, uint64_t rows, int K, const double* rinv, double* u_out, const double* u_old,
+                  double* ppart, bool apply, const DevStatus* st, int run_if, cudaStream_t s);
+// drift = max(2K - 2 ||P||_*, 0) (manifold.cpp:55-60) from P partials; when
+// `objective` non-null also f = ||G||^2 and fit = dns - f for the sweep;
+// `end_of_sweep` advances the sweep counter and applies the stop rule.
+struct SweepTrace {
+    double* objective;   // [max_sweeps]
+    double* fit;         // [max_sweeps]
+    double* drift;       // [max_sweeps * order]
+    double* fit_prev;    // 1
+};
+void launch_drift(const double* ppart, int nslots, int K, const double* core, uint64_t core_size, double dns,
+                  int order, int mode, bool end_of_sweep, double tol, uint64_t max_sweeps, const SweepTrace& tr,
+                  DevStatus* st, cudaStream_t s);
+// Householder QR following dense_core.cpp:127-198 exactly (single CTA), with
+// the seeded rank-deficiency fill generated on the device (MT19937-64 +
+// Box-Muller, rng.hpp:13-35, seed 0x48514F5251).
+void launch_householder(const double* A, uint64_t rows, int K, double* q_out, double* work, const DevStatus* st,
+                        int run_if, cudaStream_t s);
+// G_(n)^T (L x K_n) from the core
+void launch_gt(const double* core, const ModeShape& sh, const int* ranks, double* gt, const DevStatus* st,
+               cudaStream_t s);
+// core_out = reduce of M partials (mode 0 unfolding == core layout)
+void launch_reduce_core(const double* mpart, int nslots, uint64_t size, double* core_out, const DevStatus* st,
+                        int run_if, cudaStream_t s);
+// ||G||^2 into *out (deterministic)
+void launch_core_normsq(const double* core, uint64_t size, double* out, cudaStream_t s);
+// max_ij |U^T U - I| over all modes' final factors
+void launch_defect(const double* u, uint64_t rows, int K, double* wpart, double* out_max, cudaStream_t s);
+
+}  // namespace hq

@@ -1,0 +1,141 @@
+// hq_internal.cuh — shared types, error plumbing and device helpers of the
+// B200 HOQRI engine.  No exception escapes the C-ABI (hq_capi.cu catches
+// hq::Error and maps it to hq_status + a thread-local message).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/hoqri_b200.h"
+
+namespace hq {
+
+constexpr int kMaxOrder = 8;
+
+struct Error : std::runtime_error {
+    int code;
+    int64_t payload;
+    Error(int c, const std::string& m, int64_t p = 0) : std::runtime_error(m), code(c), payload(p) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg, int64_t payload = 0) {
+    throw Error(code, msg, payload);
+}
+
+#define HQ_CUDA(call)                                                                       \
+    do {                                                                                    \
+        cudaError_t _e = (call);                                                            \
+        if (_e != cudaSuccess)                                                              \
+            ::hq::fail(HQ_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+#define HQ_CHECK_LAUNCH() HQ_CUDA(cudaGetLastError())
+
+// ---------------------------------------------------------------- memory --
+// RAII device buffer (stream-ordered allocation).
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        n = count;
+        if (count) HQ_CUDA(cudaMalloc(&p, sizeof(T) * count));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    T* get() const { return p; }
+    size_t bytes() const { return sizeof(T) * n; }
+};
+
+inline int num_sms() {
+    static int sms = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v > 0 ? v : 148;
+    }();
+    return sms;
+}
+
+inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// ----------------------------------------------------------- device tensor --
+// One mode's view of the tensor: nonzeros in mode-n order (stable counting
+// sort of the lexicographic order == the reference's ModeBuckets.entries,
+// sparse_tensor.cpp:73-89), as SoA streams.
+struct ModeLayout {
+    int mode = 0;
+    uint64_t rows = 0;                 // I_n
+    DBuf<int64_t> rowptr;              // I_n + 1  (== ModeBuckets.offsets)
+    DBuf<uint32_t> entries;            // nnz      (== ModeBuckets.entries; mode 0: identity, not stored)
+    DBuf<double> val;                  // nnz, values in mode order
+    DBuf<uint32_t> idx[kMaxOrder - 1];  // nnz each: index of the j-th other mode (ascending v != n)
+    int others[kMaxOrder - 1] = {0};
+    uint64_t nonempty_rows = 0;        // R_n
+    // work plan (see hq_pass.cu)
+    uint64_t long_rows = 0;
+    DBuf<uint32_t> long_row_ids;       // rows with more than kShortMax nonzeros
+    uint64_t long_segments = 0;
+    DBuf<int64_t> seg_begin;           // long-row segments: [seg_begin, seg_end) positions
+    DBuf<uint32_t> seg_row;            // owning long row (index into long_row_ids)
+    DBuf<int64_t> long_seg_ptr;        // long row r owns segments [ptr[r], ptr[r+1])
+};
+
+struct DeviceTensor {
+    int order = 0;
+    uint64_t dims[kMaxOrder] = {0};
+    uint64_t nnz = 0;
+    DBuf<uint32_t> coords;   // lexicographically sorted, merged, AoS nnz x order
+    DBuf<double> vals;       // merged values
+    double norm_sq = 0.0;
+    ModeLayout modes[kMaxOrder];
+};
+
+// ------------------------------------------------------------ kernel args --
+struct FactorPtrs {
+    const double* u[kMaxOrder];
+    int k[kMaxOrder];
+};
+
+// Rank bookkeeping for mode n: the Kronecker row of the other modes has
+// length L = prod_{v != n} K_v, column index = sum_v k_v * cstride[v] with the
+// last other mode fastest (unfold_col_strides, dense_core.cpp:337-348).
+struct ModeShape {
+    int order;
+    int n;
+    int kn;          // K_n
+    int L;           // prod_{v != n} K_v
+    int nothers;     // order - 1
+    int ko[kMaxOrder - 1];       // K of each other mode, ascending v != n
+    int cstride[kMaxOrder - 1];  // column stride of each other mode
+};
+
+ModeShape make_mode_shape(int order, const int* ranks, int n);
+
+}  // namespace hq
+
+struct hq_tensor {
+    hq::DeviceTensor t;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    ~hq_tensor() {
+        if (own_stream && stream) cudaStreamDestroy(stream);
+    }
+};

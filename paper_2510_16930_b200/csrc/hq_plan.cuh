@@ -1,0 +1,72 @@
+// hq_plan.cuh — work decomposition of a mode-sorted stream and the sparse
+// pass entry points (hq_pass.cu).
+#pragma once
+
+#include "hq_internal.cuh"
+
+namespace hq {
+
+// Rows with more nonzeros than kShortMax are "long": they are cut into
+// segments of at most kSegLen nonzeros, each reduced by one CTA into a
+// partial Kronecker row, and the partials of a row are summed in segment
+// order (deterministic).  All other rows are processed whole by the tile
+// kernels.
+constexpr int64_t kShortMax = 256;
+constexpr int64_t kSegLen = 4096;
+
+void plan_mode(ModeLayout& L, uint64_t nnz, cudaStream_t s);
+
+double device_sum_sq(const double* v, uint64_t n, cudaStream_t s);
+void build_tensor(DeviceTensor& T, int order, const uint64_t* dims, uint64_t nnz, const uint32_t* coords_dev,
+                  const double* vals_dev, cudaStream_t s);
+void export_buckets(const DeviceTensor& T, int mode, uint64_t* offsets, uint64_t* entries, cudaStream_t s);
+
+// Device status word shared by every kernel of a solve.  Kernels return early
+// when `abort` is set; the CholeskyQR2 kernels run only while `fallback` is 0,
+// the Householder fallback kernels only while it is 1.
+struct DevStatus {
+    int abort;
+    int degenerate_mode;   // 1-based mode of the first A == 0 (solvers.cpp:124)
+    int degenerate_sweep;
+    int fallback;          // current QR needs the Householder path
+    unsigned int fallback_count;
+    int sweep;             // 1-based sweep counter (advanced on the device)
+};
+
+enum RunIf { kAlways = 0, kOnlyFallback = 1, kOnlyCholQR = 2 };
+
+__device__ __forceinline__ bool skip_kernel(const DevStatus* st, int run_if) {
+    if (!st) return false;
+    if (st->abort) return true;
+    if (run_if == kOnlyFallback) return st->fallback == 0;
+    if (run_if == kOnlyCholQR) return st->fallback != 0;
+    return false;
+}
+
+// What a sparse pass computes per row i (Y_i = the Kronecker row of mode n):
+//   kTTMcTC: a_i = Y_i G_(n)^T                 (kernels.cpp:86-163 output row)
+//   kCore:   a_i = U_n[i, :]                   (so M = sum a_i^T Y_i = G_(n), kernels.cpp:40-84)
+// and always accumulates M = sum_i a_i^T Y_i (K_n x L), W = sum a_i^T a_i
+// (K_n x K_n) and max |a| into per-CTA partial slots.
+enum PassKind { kTTMcTC = 0, kCore = 1 };
+
+struct PassOut {
+    double* A;        // I_n x K_n rows (may be null for kCore)
+    double* mpart;    // [slots][K_n * L]
+    double* wpart;    // [slots][K_n * K_n]
+    double* maxpart;  // [slots]
+    double* ypart;    // [long_segments][L] scratch
+};
+
+// Number of partial slots a pass over this mode uses.
+int pass_slots(const ModeLayout& L, const ModeShape& sh);
+size_t pass_ypart_doubles(const ModeLayout& L, const ModeShape& sh);
+
+// Launches the pass kernels (no host synchronisation; graph-capturable).
+// gt = G_(n)^T as L x K_n (kTTMcTC only).
+void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const FactorPtrs& f, PassKind kind,
+                 const double* gt, const PassOut& out, const DevStatus* st, int run_if, cudaStream_t s);
+// number of kernels launch_pass issues
+int pass_launch_count(const ModeLayout& L, const ModeShape& sh);
+
+}  // namespace hq

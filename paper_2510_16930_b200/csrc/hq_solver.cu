@@ -1,0 +1,786 @@
+// hq_solver.cu — the device-resident HOQRI driver and the C-ABI.
+//
+// Mirrors tucker::solve for HOQRI (proj/src/solvers.cpp:50-178): initial core
+// (solvers.cpp:66), then per sweep and mode n: TTMcTC (solvers.cpp:90-91),
+// degeneracy test (:124), QR (:139-140), drift (:141), core update
+// (:143-144); objective, fit and the stop rule per sweep (:153-168); the
+// orthonormality-defect check at the end (:171-172).
+//
+// B200 shape of one mode update (all device, no host round trip):
+//   gt      G_(n)^T from the core                                   (tiny)
+//   pass    one sparse pass: Y_i, a_i = Y_i G_(n)^T -> A, and the partials of
+//           W = A^T A, M = A^T Y_(n), max|A|                      (dominant)
+//   reduce  fixed-order sums of the partials
+//   chol1   degeneracy test, R1 = chol(W)
+//   gram2   W2 = (A R1^-1)^T (A R1^-1)
+//   chol2   R2 = chol(W2), Rinv = R1^-1 R2^-1, core: G_(n) = Rinv^T M
+//           (U_new = A Rinv => U_new^T Y_(n) = Rinv^T A^T Y_(n); this replaces
+//           the reference's second sparse pass ttmc_core)
+//   apply   U_new = A Rinv, P = U_new^T U_old
+//   drift   2K - 2||P||_*, and at the end of a sweep f, fit, stop rule
+// The Householder branch (householder -> drift product -> sparse core pass)
+// runs instead of gram2..apply only when chol1/chol2 flag it on the device.
+// A whole sweep is captured once per factor-buffer parity as a CUDA graph.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <thread>
+
+#include "hq_dense.cuh"
+
+namespace hq {
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_payload = 0;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return HQ_OK;
+    } catch (const Error& e) {
+        g_err = e.what();
+        g_payload = e.payload;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        g_payload = 0;
+        return HQ_ERR_CAPACITY;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        g_payload = 0;
+        return HQ_ERR_INTERNAL;
+    }
+}
+
+inline cudaStream_t as_stream(void* p) { return reinterpret_cast<cudaStream_t>(p); }
+
+// ---- host Gaussian stream, bit-exact with tucker::Rng::normal (rng.hpp:24-35):
+// raw mt19937_64 draws are sequential; the Box-Muller transform of each pair
+// is independent, so it is spread over host threads.
+inline uint64_t mix_seed(uint64_t seed, uint64_t salt) {  // rng.hpp:57-62
+    uint64_t z = seed + 0x9E3779B97F4A7C15ull * (salt + 1);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+void gaussian_stream(uint64_t seed, uint64_t count, double* out) {
+    if (!count) return;
+    const uint64_t pairs = (count + 1) / 2;
+    std::vector<uint64_t> raw(2 * pairs);
+    std::mt19937_64 gen(seed);
+    for (auto& r : raw) r = gen();
+    unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    if (pairs < 65536) nt = 1;
+    auto work = [&](uint64_t pb, uint64_t pe) {
+        for (uint64_t k = pb; k < pe; ++k) {
+            double u1 = 1.0 - static_cast<double>(raw[2 * k] >> 11) * 0x1.0p-53;
+            double u2 = static_cast<double>(raw[2 * k + 1] >> 11) * 0x1.0p-53;
+            double r = std::sqrt(-2.0 * std::log(u1));
+            double theta = 6.283185307179586476925286766559 * u2;
+            out[2 * k] = r * std::cos(theta);
+            if (2 * k + 1 < count) out[2 * k + 1] = r * std::sin(theta);
+        }
+    };
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t) th.emplace_back(work, pairs * t / nt, pairs * (t + 1) / nt);
+    for (auto& t : th) t.join();
+}
+
+// ---------------------------------------------------------------- QR -----
+struct QrWork {
+    DBuf<double> wpart, maxpart, w, maxv, r1inv, rinv, ppart, hh;
+    DBuf<DevStatus> st;
+    void ensure(uint64_t rows, int K) {
+        size_t sl = dense_slots();
+        if (wpart.n < sl * K * K) wpart.alloc(sl * K * K);
+        if (ppart.n < sl * K * K) ppart.alloc(sl * K * K);
+        if (maxpart.n < sl) maxpart.alloc(sl);
+        if (w.n < (size_t)K * K) w.alloc(K * K);
+        if (r1inv.n < (size_t)K * K) r1inv.alloc(K * K);
+        if (rinv.n < (size_t)K * K) rinv.alloc(K * K);
+        if (!maxv.n) maxv.alloc(1);
+        if (hh.n < 2 * rows * K + 8) hh.alloc(2 * rows * K + 8);
+        if (!st.n) st.alloc(1);
+    }
+};
+
+// Q = qr_orthonormal(A) on the device (A, Q device, rows x K).  Returns the
+// fallback flag (1 when the Householder path ran).
+void qr_device(const double* A, uint64_t rows, int K, double* Q, QrWork& w, cudaStream_t s) {
+    w.ensure(rows, K);
+    HQ_CUDA(cudaMemsetAsync(w.st.get(), 0, sizeof(DevStatus), s));
+    DevStatus* st = w.st.get();
+    launch_gram(A, rows, K, w.wpart.get(), w.maxpart.get(), st, kAlways, s);
+    launch_reduce_pass(nullptr, 0, w.wpart.get(), K * K, w.maxpart.get(), dense_slots(), nullptr, w.w.get(),
+                       w.maxv.get(), st, kAlways, s);
+    launch_chol1(w.w.get(), w.maxv.get(), K, w.r1inv.get(), st, 0, s);
+    launch_gram2(A, rows, K, w.r1inv.get(), w.wpart.get(), st, s);
+    launch_chol2(w.wpart.get(), dense_slots(), K, w.r1inv.get(), w.rinv.get(), nullptr, nullptr, nullptr, st, s);
+    launch_apply(A, rows, K, w.rinv.get(), Q, nullptr, nullptr, true, st, kOnlyCholQR, s);
+    launch_householder(A, rows, K, Q, w.hh.get(), st, kOnlyFallback, s);
+}
+
+void check_rank_limits(int K) {
+    if (K > kMaxRank) fail(HQ_ERR_CAPACITY, "rank " + std::to_string(K) + " above the engine limit of 32");
+}
+
+}  // namespace
+
+// ------------------------------------------------------------- solver ----
+struct Solver {
+    const DeviceTensor* T = nullptr;
+    cudaStream_t s = nullptr;
+    int N = 0;
+    int ranks[kMaxOrder] = {0};
+    uint64_t dims[kMaxOrder] = {0};
+    uint64_t core_size = 1;
+    hq_config cfg{};
+    double dns = 0.0;
+    double initial_objective = 0.0;
+
+    DBuf<double> U[kMaxOrder][2];
+    DBuf<double> core, gt, A, mpart, wpart, maxpart, ypart, mred, wred, maxv, r1inv, rinv, w2part, ppart, hh;
+    DBuf<double> tr_obj, tr_fit, tr_drift, fit_prev;
+    DBuf<DevStatus> st;
+    ModeShape sh[kMaxOrder];
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    int host_parity = 0;
+    uint64_t launched = 0;
+    std::vector<cudaEvent_t> ev;  // ev[0] start, ev[i] after sweep i
+    QrWork qw;
+
+    ~Solver() {
+        for (auto& g : graph)
+            if (g) cudaGraphExecDestroy(g);
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+
+    FactorPtrs factors_for_mode(int n, int p) const {
+        FactorPtrs f{};
+        for (int v = 0; v < N; ++v) {
+            f.u[v] = U[v][(v < n) ? 1 - p : p].get();
+            f.k[v] = ranks[v];
+        }
+        return f;
+    }
+
+    PassOut pass_out(double* a) {
+        return PassOut{a, mpart.get(), wpart.get(), maxpart.get(), ypart.get()};
+    }
+
+    void setup(const DeviceTensor* t, const hq_config* c, const double* const* init, cudaStream_t stream) {
+        T = t;
+        s = stream;
+        cfg = *c;
+        N = t->order;
+        if (cfg.order != N) fail(HQ_ERR_SHAPE, "rank count does not match tensor order");
+        for (int v = 0; v < N; ++v) {  // solvers.cpp:22-30
+            if (cfg.ranks[v] < 1 || cfg.ranks[v] > t->dims[v])
+                fail(HQ_ERR_SHAPE, "rank for mode " + std::to_string(v + 1) + " must lie in [1, " +
+                                       std::to_string(t->dims[v]) + "]");
+            ranks[v] = (int)cfg.ranks[v];
+            dims[v] = t->dims[v];
+            check_rank_limits(ranks[v]);
+            core_size *= (uint64_t)ranks[v];
+        }
+        if (cfg.max_sweeps < 1) fail(HQ_ERR_SHAPE, "max_sweeps must be at least 1");
+        if (cfg.tol_fit_change < 0.0) fail(HQ_ERR_SHAPE, "tolerance must be nonnegative");
+        dns = t->norm_sq;
+        size_t maxIK = 0, maxML = 0, maxslots = 0, maxy = 0, maxLK = 0;
+        for (int v = 0; v < N; ++v) {
+            sh[v] = make_mode_shape(N, ranks, v);
+            maxIK = std::max(maxIK, (size_t)dims[v] * ranks[v]);
+            int sl = pass_slots(t->modes[v], sh[v]);
+            maxslots = std::max(maxslots, (size_t)sl);
+            maxML = std::max(maxML, (size_t)sl * sh[v].kn * sh[v].L);
+            maxy = std::max(maxy, pass_ypart_doubles(t->modes[v], sh[v]));
+            maxLK = std::max(maxLK, (size_t)sh[v].kn * sh[v].L);
+        }
+        int kmax = 1;
+        for (int v = 0; v < N; ++v) kmax = std::max(kmax, ranks[v]);
+        for (int v = 0; v < N; ++v)
+            for (int p = 0; p < 2; ++p) U[v][p].alloc((size_t)dims[v] * ranks[v]);
+        core.alloc(core_size);
+        gt.alloc(maxLK);
+        A.alloc(maxIK);
+        mpart.alloc(maxML);
+        wpart.alloc(maxslots * kmax * kmax);
+        maxpart.alloc(maxslots);
+        ypart.alloc(std::max<size_t>(maxy, 1));
+        mred.alloc(maxLK);
+        wred.alloc(kmax * kmax);
+        maxv.alloc(1);
+        r1inv.alloc(kmax * kmax);
+        rinv.alloc(kmax * kmax);
+        w2part.alloc((size_t)dense_slots() * kmax * kmax);
+        ppart.alloc((size_t)dense_slots() * kmax * kmax);
+        hh.alloc(2 * maxIK + 8);
+        tr_obj.alloc(cfg.max_sweeps);
+        tr_fit.alloc(cfg.max_sweeps);
+        tr_drift.alloc(cfg.max_sweeps * N);
+        fit_prev.alloc(1);
+        st.alloc(1);
+        HQ_CUDA(cudaMemsetAsync(st.get(), 0, sizeof(DevStatus), s));
+
+        // ---- initial factors (solvers.cpp:182-215)
+        if (cfg.init == 2) {
+            for (int v = 0; v < N; ++v)
+                HQ_CUDA(cudaMemcpyAsync(U[v][0].get(), init[v], sizeof(double) * dims[v] * ranks[v],
+                                        cudaMemcpyHostToDevice, s));
+        } else if (cfg.init == 0) {
+            for (int v = 0; v < N; ++v) {
+                std::vector<double> g((size_t)dims[v] * ranks[v]);
+                gaussian_stream(mix_seed(cfg.seed, (uint64_t)v), g.size(), g.data());
+                HQ_CUDA(cudaMemcpyAsync(A.get(), g.data(), sizeof(double) * g.size(), cudaMemcpyHostToDevice, s));
+                qr_device(A.get(), dims[v], ranks[v], U[v][0].get(), qw, s);
+                HQ_CUDA(cudaStreamSynchronize(s));
+            }
+        } else {
+            fail(HQ_ERR_CAPACITY, "HOSVD initialisation is desk-scale only and not part of the device engine; "
+                                  "use random init");
+        }
+        // ---- initial core (solvers.cpp:66) and objective
+        compute_core(0, kAlways);
+        DBuf<double> f0;
+        f0.alloc(1);
+        launch_core_normsq(core.get(), core_size, f0.get(), s);
+        HQ_CUDA(cudaMemcpyAsync(&initial_objective, f0.get(), 8, cudaMemcpyDeviceToHost, s));
+        HQ_CUDA(cudaStreamSynchronize(s));
+        double fp = dns - initial_objective;
+        HQ_CUDA(cudaMemcpyAsync(fit_prev.get(), &fp, 8, cudaMemcpyHostToDevice, s));
+        HQ_CUDA(cudaStreamSynchronize(s));
+        host_parity = 0;
+    }
+
+    // core = X x {U^T} with the parity-p factors, via the mode-0 pass
+    void compute_core(int p, int run_if, int updated_mode = -1) {
+        FactorPtrs f{};
+        for (int v = 0; v < N; ++v) {
+            int q = (updated_mode >= 0 && v <= updated_mode) ? 1 - p : p;
+            f.u[v] = U[v][q].get();
+            f.k[v] = ranks[v];
+        }
+        launch_pass(*T, 0, sh[0], f, kCore, nullptr, pass_out(nullptr), st.get(), run_if, s);
+        launch_reduce_core(mpart.get(), pass_slots(T->modes[0], sh[0]), core_size, core.get(), st.get(), run_if, s);
+    }
+
+    void mode_update(int n, int p) {
+        const ModeShape& m = sh[n];
+        const int K = ranks[n];
+        const uint64_t rows = dims[n];
+        FactorPtrs f = factors_for_mode(n, p);
+        DevStatus* S = st.get();
+        launch_gt(core.get(), m, ranks, gt.get(), S, s);
+        launch_pass(*T, n, m, f, kTTMcTC, gt.get(), pass_out(A.get()), S, kAlways, s);
+        const int slots = pass_slots(T->modes[n], m);
+        launch_reduce_pass(mpart.get(), m.kn * m.L, wpart.get(), K * K, maxpart.get(), slots, mred.get(), wred.get(),
+                           maxv.get(), S, kAlways, s);
+        launch_chol1(wred.get(), maxv.get(), K, r1inv.get(), S, n + 1, s);
+        launch_gram2(A.get(), rows, K, r1inv.get(), w2part.get(), S, s);
+        launch_chol2(w2part.get(), dense_slots(), K, r1inv.get(), rinv.get(), mred.get(), &m, core.get(), S, s);
+        double* unew = U[n][1 - p].get();
+        const double* uold = U[n][p].get();
+        launch_apply(A.get(), rows, K, rinv.get(), unew, uold, ppart.get(), true, S, kOnlyCholQR, s);
+        // Householder branch (device flag)
+        launch_householder(A.get(), rows, K, unew, hh.get(), S, kOnlyFallback, s);
+        launch_apply(nullptr, rows, K, nullptr, unew, uold, ppart.get(), false, S, kOnlyFallback, s);
+        compute_core(p, kOnlyFallback, n);
+        SweepTrace tr{tr_obj.get(), tr_fit.get(), tr_drift.get(), fit_prev.get()};
+        launch_drift(ppart.get(), dense_slots(), K, core.get(), core_size, dns, N, n, n == N - 1,
+                     cfg.tol_fit_change, cfg.max_sweeps, tr, S, s);
+    }
+
+    void issue_sweep(int p) {
+        for (int n = 0; n < N; ++n) mode_update(n, p);
+    }
+
+    int launches_per_sweep() const {
+        int c = 0;
+        for (int n = 0; n < N; ++n)
+            c += 1 + pass_launch_count(T->modes[n], sh[n]) + 1 + 1 + 1 + 1 + 1 + 1 + 1 +
+                 pass_launch_count(T->modes[0], sh[0]) + 1 + 1;
+        return c;
+    }
+
+    void build_graphs() {
+        for (int p = 0; p < 2; ++p) {
+            cudaGraph_t g;
+            HQ_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+            issue_sweep(p);
+            HQ_CUDA(cudaStreamEndCapture(s, &g));
+            HQ_CUDA(cudaGraphInstantiate(&graph[p], g, 0));
+            cudaGraphDestroy(g);
+        }
+    }
+
+    void run(uint64_t sweeps) {
+        if (!graph[0]) {
+            // first sweep eagerly (sets kernel attributes), then capture
+            ensure_events();
+            issue_sweep(host_parity);
+            host_parity ^= 1;
+            ++launched;
+            HQ_CUDA(cudaEventRecord(ev[std::min<size_t>(launched, ev.size() - 1)], s));
+            build_graphs();
+            if (sweeps) --sweeps;
+        }
+        ensure_events();
+        for (uint64_t i = 0; i < sweeps; ++i) {
+            HQ_CUDA(cudaGraphLaunch(graph[host_parity], s));
+            host_parity ^= 1;
+            ++launched;
+            if (launched < ev.size()) HQ_CUDA(cudaEventRecord(ev[launched], s));
+        }
+    }
+
+    void ensure_events() {
+        if (ev.empty()) {
+            ev.resize(cfg.max_sweeps + 1);
+            for (auto& e : ev) HQ_CUDA(cudaEventCreate(&e));
+            HQ_CUDA(cudaEventRecord(ev[0], s));
+        }
+    }
+
+    DevStatus status() {
+        DevStatus h{};
+        HQ_CUDA(cudaMemcpyAsync(&h, st.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+        HQ_CUDA(cudaStreamSynchronize(s));
+        return h;
+    }
+
+    void check_status(const DevStatus& h) {
+        if (h.abort == 1)
+            fail(HQ_ERR_DEGENERATE,
+                 "degenerate state: TTMcTC output is identically zero for mode " + std::to_string(h.degenerate_mode),
+                 h.degenerate_mode);
+    }
+
+    // solve loop: launch sweeps in batches, stop once the device reports the
+    // stop rule (or max_sweeps)
+    void solve() {
+        uint64_t remaining = cfg.max_sweeps;
+        const uint64_t batch = cfg.tol_fit_change > 0.0 ? 2 : remaining;
+        while (remaining) {
+            uint64_t b = std::min(batch, remaining);
+            run(b);
+            remaining -= b;
+            DevStatus h = status();
+            check_status(h);
+            if (h.abort || (uint64_t)h.sweep >= cfg.max_sweeps) break;
+        }
+    }
+
+    void download(double* const* factors_out, double* core_out, hq_trace* tr) {
+        DevStatus h = status();
+        check_status(h);
+        const int parity = h.sweep & 1;
+        if (factors_out)
+            for (int v = 0; v < N; ++v)
+                if (factors_out[v])
+                    HQ_CUDA(cudaMemcpyAsync(factors_out[v], U[v][parity].get(), sizeof(double) * dims[v] * ranks[v],
+                                            cudaMemcpyDeviceToHost, s));
+        if (core_out)
+            HQ_CUDA(cudaMemcpyAsync(core_out, core.get(), sizeof(double) * core_size, cudaMemcpyDeviceToHost, s));
+        if (tr) {
+            tr->data_norm_sq = dns;
+            tr->initial_objective = initial_objective;
+            tr->sweeps = (uint64_t)h.sweep;
+            if (h.sweep) {
+                if (tr->objective)
+                    HQ_CUDA(cudaMemcpyAsync(tr->objective, tr_obj.get(), 8 * h.sweep, cudaMemcpyDeviceToHost, s));
+                if (tr->fit) HQ_CUDA(cudaMemcpyAsync(tr->fit, tr_fit.get(), 8 * h.sweep, cudaMemcpyDeviceToHost, s));
+                if (tr->drift)
+                    HQ_CUDA(cudaMemcpyAsync(tr->drift, tr_drift.get(), 8 * h.sweep * N, cudaMemcpyDeviceToHost, s));
+            }
+            HQ_CUDA(cudaStreamSynchronize(s));
+            if (tr->elapsed_s && !ev.empty()) {
+                for (uint64_t i = 1; i <= (uint64_t)h.sweep && i < ev.size(); ++i) {
+                    float ms = 0.f;
+                    HQ_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[i]));
+                    tr->elapsed_s[i - 1] = ms * 1e-3;
+                }
+            }
+            if (tr->grad_norm_sq)
+                for (uint64_t i = 0; i < (uint64_t)h.sweep * N; ++i) tr->grad_norm_sq[i] = 0.0;
+        }
+        HQ_CUDA(cudaStreamSynchronize(s));
+        // solvers.cpp:171-172
+        DBuf<double> wp, mx;
+        int kmax = 1;
+        for (int v = 0; v < N; ++v) kmax = std::max(kmax, ranks[v]);
+        wp.alloc((size_t)dense_slots() * kmax * kmax);
+        mx.alloc(N);
+        for (int v = 0; v < N; ++v) launch_defect(U[v][parity].get(), dims[v], ranks[v], wp.get(), mx.get() + v, s);
+        std::vector<double> hm(N);
+        HQ_CUDA(cudaMemcpyAsync(hm.data(), mx.get(), 8 * N, cudaMemcpyDeviceToHost, s));
+        HQ_CUDA(cudaStreamSynchronize(s));
+        for (double d : hm)
+            if (d > 1e-10) fail(HQ_ERR_DIAGNOSTIC, "solver produced factors with orthonormality defect above 1e-10");
+    }
+};
+
+}  // namespace hq
+
+struct hq_solver {
+    std::unique_ptr<hq::Solver> impl;
+};
+
+using namespace hq;
+
+// ====================================================================== C-ABI
+extern "C" {
+
+const char* hq_last_error(void) { return g_err.c_str(); }
+int64_t hq_last_error_payload(void) { return g_payload; }
+const char* hq_version(void) { return "hoqri_b200 0.1 (sm_100a)"; }
+
+static int tensor_create_impl(int order, const uint64_t* dims, uint64_t nnz, const uint32_t* coords,
+                              const double* values, bool on_device, void* stream, hq_tensor** out) {
+    return guard([&] {
+        if (!out) fail(HQ_ERR_SHAPE, "null output handle");
+        if (order <= 0) fail(HQ_ERR_SHAPE, "sparse tensor needs at least one mode");
+        if (nnz && (!coords || !values)) fail(HQ_ERR_SHAPE, "coordinate array does not match entry count");
+        auto h = std::make_unique<hq_tensor>();
+        h->stream = as_stream(stream);
+        if (!h->stream) {
+            HQ_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+            h->own_stream = true;
+        }
+        cudaStream_t s = h->stream;
+        if (on_device || !nnz) {
+            build_tensor(h->t, order, dims, nnz, coords, values, s);
+        } else {
+            DBuf<uint32_t> c;
+            DBuf<double> v;
+            c.alloc(nnz * order);
+            v.alloc(nnz);
+            HQ_CUDA(cudaMemcpyAsync(c.get(), coords, sizeof(uint32_t) * nnz * order, cudaMemcpyHostToDevice, s));
+            HQ_CUDA(cudaMemcpyAsync(v.get(), values, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+            build_tensor(h->t, order, dims, nnz, c.get(), v.get(), s);
+        }
+        *out = h.release();
+    });
+}
+
+int hq_tensor_create(int order, const uint64_t* dims, uint64_t nnz, const uint32_t* coords, const double* values,
+                     void* stream, hq_tensor** out) {
+    return tensor_create_impl(order, dims, nnz, coords, values, false, stream, out);
+}
+
+int hq_tensor_create_dev(int order, const uint64_t* dims, uint64_t nnz, const uint32_t* coords_dev,
+                         const double* values_dev, void* stream, hq_tensor** out) {
+    return tensor_create_impl(order, dims, nnz, coords_dev, values_dev, true, stream, out);
+}
+
+int hq_tensor_destroy(hq_tensor* t) {
+    return guard([&] { delete t; });
+}
+
+int hq_tensor_info(const hq_tensor* t, int* order, uint64_t* dims, uint64_t* nnz) {
+    return guard([&] {
+        if (order) *order = t->t.order;
+        if (dims)
+            for (int m = 0; m < t->t.order; ++m) dims[m] = t->t.dims[m];
+        if (nnz) *nnz = t->t.nnz;
+    });
+}
+
+int hq_tensor_export(const hq_tensor* t, uint32_t* coords, double* values) {
+    return guard([&] {
+        cudaStream_t s = t->stream;
+        if (t->t.nnz) {
+            if (coords)
+                HQ_CUDA(cudaMemcpyAsync(coords, t->t.coords.get(), sizeof(uint32_t) * t->t.nnz * t->t.order,
+                                        cudaMemcpyDeviceToHost, s));
+            if (values)
+                HQ_CUDA(cudaMemcpyAsync(values, t->t.vals.get(), sizeof(double) * t->t.nnz, cudaMemcpyDeviceToHost, s));
+        }
+        HQ_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int hq_tensor_buckets(const hq_tensor* t, int mode, uint64_t* offsets, uint64_t* entries) {
+    return guard([&] {
+        if (mode < 0 || mode >= t->t.order) fail(HQ_ERR_RANGE, "mode out of range");
+        export_buckets(t->t, mode, offsets, entries, t->stream);
+    });
+}
+
+int hq_tensor_norm_sq(const hq_tensor* t, double* out) {
+    return guard([&] { *out = t->t.norm_sq; });
+}
+
+namespace {
+
+struct UploadedFactors {
+    DBuf<double> u[kMaxOrder];
+    FactorPtrs f{};
+    int ranks[kMaxOrder] = {0};
+};
+
+void upload_factors(const DeviceTensor& T, const double* const* factors, const uint64_t* ranks, UploadedFactors& uf,
+                    cudaStream_t s) {
+    for (int v = 0; v < T.order; ++v) {
+        if (ranks[v] == 0) fail(HQ_ERR_SHAPE, "factor with zero columns");
+        check_rank_limits((int)ranks[v]);
+        uf.ranks[v] = (int)ranks[v];
+        uf.u[v].alloc(T.dims[v] * ranks[v]);
+        HQ_CUDA(cudaMemcpyAsync(uf.u[v].get(), factors[v], sizeof(double) * T.dims[v] * ranks[v],
+                                cudaMemcpyHostToDevice, s));
+        uf.f.u[v] = uf.u[v].get();
+        uf.f.k[v] = (int)ranks[v];
+    }
+}
+
+struct PassBuffers {
+    DBuf<double> mpart, wpart, maxpart, ypart, core;
+    void ensure(const ModeLayout& L, const ModeShape& sh) {
+        int sl = pass_slots(L, sh);
+        mpart.alloc((size_t)sl * sh.kn * sh.L);
+        wpart.alloc((size_t)sl * sh.kn * sh.kn);
+        maxpart.alloc(sl);
+        ypart.alloc(std::max<size_t>(1, pass_ypart_doubles(L, sh)));
+    }
+};
+
+void core_device(const DeviceTensor& T, const UploadedFactors& uf, double* core_dev, cudaStream_t s) {
+    ModeShape sh = make_mode_shape(T.order, uf.ranks, 0);
+    PassBuffers pb;
+    pb.ensure(T.modes[0], sh);
+    PassOut out{nullptr, pb.mpart.get(), pb.wpart.get(), pb.maxpart.get(), pb.ypart.get()};
+    launch_pass(T, 0, sh, uf.f, kCore, nullptr, out, nullptr, kAlways, s);
+    uint64_t size = (uint64_t)sh.kn * sh.L;
+    launch_reduce_core(pb.mpart.get(), pass_slots(T.modes[0], sh), size, core_dev, nullptr, kAlways, s);
+    HQ_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
+int hq_ttmc_core(const hq_tensor* t, const double* const* factors, const uint64_t* ranks, double* core_out) {
+    return guard([&] {
+        cudaStream_t s = t->stream;
+        UploadedFactors uf;
+        upload_factors(t->t, factors, ranks, uf, s);
+        uint64_t size = 1;
+        for (int v = 0; v < t->t.order; ++v) size *= ranks[v];
+        DBuf<double> core;
+        core.alloc(size);
+        core_device(t->t, uf, core.get(), s);
+        HQ_CUDA(cudaMemcpyAsync(core_out, core.get(), sizeof(double) * size, cudaMemcpyDeviceToHost, s));
+        HQ_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int hq_ttmctc(const hq_tensor* t, const double* const* factors, const uint64_t* ranks, int mode, const double* core,
+              int variant, double* a_out) {
+    (void)variant;
+    return guard([&] {
+        if (mode < 0 || mode >= t->t.order) fail(HQ_ERR_RANGE, "ttmctc: mode out of range");
+        cudaStream_t s = t->stream;
+        const DeviceTensor& T = t->t;
+        UploadedFactors uf;
+        upload_factors(T, factors, ranks, uf, s);
+        uint64_t size = 1;
+        for (int v = 0; v < T.order; ++v) size *= ranks[v];
+        DBuf<double> dcore;
+        dcore.alloc(size);
+        if (core)
+            HQ_CUDA(cudaMemcpyAsync(dcore.get(), core, sizeof(double) * size, cudaMemcpyHostToDevice, s));
+        else
+            core_device(T, uf, dcore.get(), s);
+        ModeShape sh = make_mode_shape(T.order, uf.ranks, mode);
+        DBuf<double> gt, A;
+        gt.alloc((size_t)sh.L * sh.kn);
+        A.alloc(T.dims[mode] * sh.kn);
+        launch_gt(dcore.get(), sh, uf.ranks, gt.get(), nullptr, s);
+        PassBuffers pb;
+        pb.ensure(T.modes[mode], sh);
+        PassOut out{A.get(), pb.mpart.get(), pb.wpart.get(), pb.maxpart.get(), pb.ypart.get()};
+        launch_pass(T, mode, sh, uf.f, kTTMcTC, gt.get(), out, nullptr, kAlways, s);
+        HQ_CUDA(cudaMemcpyAsync(a_out, A.get(), sizeof(double) * T.dims[mode] * sh.kn, cudaMemcpyDeviceToHost, s));
+        HQ_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int hq_qr_orthonormal(uint64_t rows, uint64_t cols, const double* a, double* q_out) {
+    return guard([&] {
+        if (rows < cols) fail(HQ_ERR_SHAPE, "qr_orthonormal: need rows >= cols");
+        if (cols == 0) return;
+        check_rank_limits((int)cols);
+        cudaStream_t s = nullptr;
+        DBuf<double> A, Q;
+        A.alloc(rows * cols);
+        Q.alloc(rows * cols);
+        HQ_CUDA(cudaMemcpyAsync(A.get(), a, sizeof(double) * rows * cols, cudaMemcpyHostToDevice, s));
+        QrWork w;
+        qr_device(A.get(), rows, (int)cols, Q.get(), w, s);
+        HQ_CUDA(cudaMemcpyAsync(q_out, Q.get(), sizeof(double) * rows * cols, cudaMemcpyDeviceToHost, s));
+        HQ_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int hq_subspace_distance(uint64_t rows, uint64_t cols, const double* u, const double* v, double* out) {
+    return guard([&] {
+        if (cols == 0) {
+            *out = 0.0;
+            return;
+        }
+        check_rank_limits((int)cols);
+        cudaStream_t s = nullptr;
+        DBuf<double> U, V, pp, d, obj, fit, fp;
+        DBuf<DevStatus> st;
+        U.alloc(rows * cols);
+        V.alloc(rows * cols);
+        pp.alloc((size_t)dense_slots() * cols * cols);
+        d.alloc(1);
+        obj.alloc(1);
+        fit.alloc(1);
+        fp.alloc(1);
+        st.alloc(1);
+        HQ_CUDA(cudaMemsetAsync(st.get(), 0, sizeof(DevStatus), s));
+        HQ_CUDA(cudaMemcpyAsync(U.get(), u, sizeof(double) * rows * cols, cudaMemcpyHostToDevice, s));
+        HQ_CUDA(cudaMemcpyAsync(V.get(), v, sizeof(double) * rows * cols, cudaMemcpyHostToDevice, s));
+        launch_apply(nullptr, rows, (int)cols, nullptr, U.get(), V.get(), pp.get(), false, nullptr, kAlways, s);
+        SweepTrace tr{obj.get(), fit.get(), d.get(), fp.get()};
+        launch_drift(pp.get(), dense_slots(), (int)cols, nullptr, 0, 0.0, 1, 0, false, 0.0, 1, tr, st.get(), s);
+        HQ_CUDA(cudaMemcpyAsync(out, d.get(), 8, cudaMemcpyDeviceToHost, s));
+        HQ_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int hq_random_factors(int order, const uint64_t* dims, const uint64_t* ranks, uint64_t seed,
+                      double* const* factors_out) {
+    return guard([&] {
+        cudaStream_t s = nullptr;
+        QrWork w;
+        for (int v = 0; v < order; ++v) {
+            if (ranks[v] > dims[v]) fail(HQ_ERR_SHAPE, "qr_orthonormal: need rows >= cols");
+            if (ranks[v] == 0) continue;
+            check_rank_limits((int)ranks[v]);
+            std::vector<double> g(dims[v] * ranks[v]);
+            gaussian_stream(mix_seed(seed, (uint64_t)v), g.size(), g.data());
+            DBuf<double> A, Q;
+            A.alloc(g.size());
+            Q.alloc(g.size());
+            HQ_CUDA(cudaMemcpyAsync(A.get(), g.data(), sizeof(double) * g.size(), cudaMemcpyHostToDevice, s));
+            qr_device(A.get(), dims[v], (int)ranks[v], Q.get(), w, s);
+            HQ_CUDA(cudaMemcpyAsync(factors_out[v], Q.get(), sizeof(double) * g.size(), cudaMemcpyDeviceToHost, s));
+            HQ_CUDA(cudaStreamSynchronize(s));
+        }
+    });
+}
+
+void hq_config_default(hq_config* cfg) {
+    std::memset(cfg, 0, sizeof(*cfg));
+    cfg->max_sweeps = 100;
+    cfg->tol_fit_change = 1e-12;
+}
+
+int hq_solver_create(const hq_tensor* t, const hq_config* cfg, const double* const* init_factors, void* stream,
+                     hq_solver** out) {
+    return guard([&] {
+        auto h = std::make_unique<hq_solver>();
+        h->impl = std::make_unique<Solver>();
+        cudaStream_t s = stream ? as_stream(stream) : t->stream;
+        if (cfg->trace_gradients || cfg->tol_grad > 0.0)
+            fail(HQ_ERR_CAPACITY, "gradient tracing is not implemented on the device engine yet");
+        h->impl->setup(&t->t, cfg, init_factors, s);
+        *out = h.release();
+    });
+}
+
+int hq_solver_destroy(hq_solver* s) {
+    return guard([&] { delete s; });
+}
+
+int hq_solver_run(hq_solver* s, uint64_t sweeps) {
+    return guard([&] { s->impl->run(sweeps); });
+}
+
+int hq_solver_sync(hq_solver* s) {
+    return guard([&] { s->impl->check_status(s->impl->status()); });
+}
+
+int hq_solver_launch_mode_pass(hq_solver* sv, int mode) {
+    return guard([&] {
+        Solver& S = *sv->impl;
+        if (mode < 0 || mode >= S.N) fail(HQ_ERR_RANGE, "mode out of range");
+        FactorPtrs f = S.factors_for_mode(mode, S.host_parity);
+        launch_pass(*S.T, mode, S.sh[mode], f, kTTMcTC, S.gt.get(), S.pass_out(S.A.get()), nullptr, kAlways, S.s);
+    });
+}
+
+int hq_solver_launch_ttmctc(hq_solver* sv, int mode) { return hq_solver_launch_mode_pass(sv, mode); }
+
+int hq_solver_launches_per_sweep(const hq_solver* s, uint64_t* out) {
+    return guard([&] { *out = (uint64_t)s->impl->launches_per_sweep(); });
+}
+
+int hq_solver_download(hq_solver* s, double* const* factors_out, double* core_out, hq_trace* trace) {
+    return guard([&] { s->impl->download(factors_out, core_out, trace); });
+}
+
+int hq_solver_mode_pass_work(const hq_solver* sv, int mode, double* flops, double* bytes) {
+    return guard([&] {
+        const Solver& S = *sv->impl;
+        const ModeShape& m = S.sh[mode];
+        const ModeLayout& L = S.T->modes[mode];
+        double nnz = (double)S.T->nnz, R = (double)L.nonempty_rows;
+        // kron rows (L per nonzero, built as (L/K_last) products + L FMAs),
+        // a_i = Y_i G^T, M += a_i^T Y_i, W += a_i^T a_i
+        *flops = 2.0 * nnz * m.L + 2.0 * R * m.L * m.kn * 2.0 + 2.0 * R * m.kn * m.kn;
+        double fb = 0.0;
+        for (int v = 0; v < S.N; ++v)
+            if (v != mode) fb += 8.0 * (double)S.dims[v] * S.ranks[v];
+        *bytes = nnz * (4.0 * (S.N - 1) + 8.0) + 8.0 * (double)(L.rows + 1) + fb + 8.0 * (double)S.dims[mode] * m.kn;
+    });
+}
+
+int hq_solver_ttmctc_work(const hq_solver* sv, int mode, double* flops, double* bytes) {
+    return guard([&] {
+        const Solver& S = *sv->impl;
+        const ModeShape& m = S.sh[mode];
+        const ModeLayout& L = S.T->modes[mode];
+        double nnz = (double)S.T->nnz, R = (double)L.nonempty_rows;
+        // F = 2 nnz prod_{v!=n} K_v + 2 R_n prod_v K_v
+        *flops = 2.0 * nnz * m.L + 2.0 * R * m.L * m.kn;
+        double fb = 0.0;
+        for (int v = 0; v < S.N; ++v)
+            if (v != mode) fb += 8.0 * (double)S.dims[v] * S.ranks[v];
+        // B = nnz (4N + 8) + 8 sum_{v!=n} I_v K_v + 8 I_n K_n
+        *bytes = nnz * (4.0 * S.N + 8.0) + fb + 8.0 * (double)S.dims[mode] * m.kn;
+    });
+}
+
+int hq_hoqri(const hq_tensor* t, const hq_config* cfg, const double* const* init_factors, double* const* factors_out,
+             double* core_out, hq_trace* trace) {
+    return guard([&] {
+        if (cfg->trace_gradients || cfg->tol_grad > 0.0)
+            fail(HQ_ERR_CAPACITY, "gradient tracing is not implemented on the device engine yet");
+        Solver S;
+        S.setup(&t->t, cfg, init_factors, t->stream);
+        S.solve();
+        S.download(factors_out, core_out, trace);
+    });
+}
+
+int hq_fit_error(double data_norm_sq, uint64_t core_size, const double* core, double* out) {
+    return guard([&] {  // solvers.cpp:225-236
+        double f = 0.0;
+        for (uint64_t i = 0; i < core_size; ++i) f += core[i] * core[i];
+        double r = data_norm_sq - f;
+        double scale = std::max(1.0, data_norm_sq);
+        if (r < -1e-8 * scale)
+            fail(HQ_ERR_CONTRACT,
+                 "fit_error: core energy exceeds the data norm; core is inconsistent with the factors");
+        *out = (std::fabs(r) <= 1e-10 * scale) ? 0.0 : std::max(r, 0.0);
+    });
+}
+
+}  // extern "C"

@@ -257,7 +257,8 @@ def run_engine(args, ws, rank, local):
     c, coords, vals = workload(args.config)
     dims, ranks = list(c["dims"]), list(c["ranks"])
     N = len(dims)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # a real stream: the solver launches (and is timed) on it
+    torch.cuda.set_stream(stream)
     x = hq.SparseTensor(dims, coords, vals)
     nnz = x.nnz()
     u0 = hq.random_factors(dims, ranks, SEED_INIT)

@@ -1,0 +1,3 @@
+#pragma once
+// B200 drop-in: the errors.hpp names live in tucker_b200.hpp
+#include "tucker/tucker_b200.hpp"

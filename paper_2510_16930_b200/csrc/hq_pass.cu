@@ -16,7 +16,9 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
+#include "hq_fast.cuh"
 #include "hq_plan.cuh"
 
 namespace hq {
@@ -337,6 +339,13 @@ int generic_rows_per_tile(const ModeShape& sh) {
 }
 
 int short_grid() { return num_sms() * 2; }
+
+// HQ_FORCE_GENERIC=1 routes every shape through the generic kernels (tests
+// compare both paths on the same inputs).
+bool force_generic() {
+    const char* e = std::getenv("HQ_FORCE_GENERIC");
+    return e && e[0] == '1';
+}
 int long_grid(const ModeLayout& L) { return (int)std::min<uint64_t>(L.long_rows, (uint64_t)num_sms() * 2); }
 
 void set_smem(const void* fn, size_t bytes) {
@@ -387,10 +396,32 @@ void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const Fac
     a.R = generic_rows_per_tile(sh);
     a.ntiles = (int64_t)ceil_div(L.rows, a.R);
     a.slot0 = 0;
-    size_t smem = sizeof(double) * ((size_t)a.R * sh.L + (size_t)a.R * sh.kn);
-    set_smem((const void*)k_pass_tiles_generic, smem);
-    k_pass_tiles_generic<<<short_grid(), kGenericThreads, smem, s>>>(a);
-    HQ_CHECK_LAUNCH();
+    if (fast_supported(sh) && !force_generic()) {
+        FastArgs fa{};
+        fa.rows = L.rows;
+        fa.rowptr = a.rowptr;
+        fa.val = a.val;
+        fa.ia = a.idx[0];
+        fa.ib = a.idx[1];
+        fa.ua = a.uo[0];
+        fa.ub = a.uo[1];
+        fa.un = a.un;
+        fa.gt = gt;
+        fa.A = out.A;
+        fa.mpart = out.mpart;
+        fa.wpart = out.wpart;
+        fa.maxpart = out.maxpart;
+        fa.kind = kind;
+        fa.slot0 = 0;
+        fa.st = st;
+        fa.run_if = run_if;
+        launch_fast(fa, sh, short_grid(), s);
+    } else {
+        size_t smem = sizeof(double) * ((size_t)a.R * sh.L + (size_t)a.R * sh.kn);
+        set_smem((const void*)k_pass_tiles_generic, smem);
+        k_pass_tiles_generic<<<short_grid(), kGenericThreads, smem, s>>>(a);
+        HQ_CHECK_LAUNCH();
+    }
     if (L.long_rows) {
         int segs = (int)std::min<uint64_t>(L.long_segments, (uint64_t)num_sms() * 8);
         k_pass_longseg_generic<<<segs, kGenericThreads, 0, s>>>(a);

@@ -22,6 +22,12 @@ struct QrScratch {
 
 int dense_slots();
 
+// X = A T (T null: identity); out <- X (optional); part[cta] = X^T Y with
+// Y = other (optional) or X; maxpart[cta] = max|A| (optional).  hq_rowgemm.cu
+bool rowgemm_supported(int K);
+void launch_rowgemm(int K, const double* A, uint64_t rows, const double* T, double* out, const double* other,
+                    double* part, double* maxpart, const DevStatus* st, int run_if, cudaStream_t s);
+
 // W = sum of `nslots` partial K*K slots (fixed order) and max over max partials
 void launch_reduce_pass(const double* mpart, int mlen, const double* wpart, int wlen, const double* maxpart,
                         int nslots, double* m_out, double* w_out, double* max_out, const DevStatus* st, int run_if,

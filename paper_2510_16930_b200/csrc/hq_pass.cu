@@ -354,9 +354,13 @@ void set_smem(const void* fn, size_t bytes) {
 
 }  // namespace
 
+int tile_grid(const ModeShape& sh) {
+    if (fast_supported(sh) && !force_generic()) return fast_grid(sh.ko[0], sh.ko[1], sh.kn);
+    return short_grid();
+}
+
 int pass_slots(const ModeLayout& L, const ModeShape& sh) {
-    (void)sh;
-    return short_grid() + (L.long_rows ? long_grid(L) : 0);
+    return tile_grid(sh) + (L.long_rows ? long_grid(L) : 0);
 }
 
 size_t pass_ypart_doubles(const ModeLayout& L, const ModeShape& sh) { return (size_t)L.long_segments * sh.L; }
@@ -415,7 +419,7 @@ void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const Fac
         fa.slot0 = 0;
         fa.st = st;
         fa.run_if = run_if;
-        launch_fast(fa, sh, short_grid(), s);
+        launch_fast(fa, sh, tile_grid(sh), s);
     } else {
         size_t smem = sizeof(double) * ((size_t)a.R * sh.L + (size_t)a.R * sh.kn);
         set_smem((const void*)k_pass_tiles_generic, smem);
@@ -426,7 +430,7 @@ void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const Fac
         int segs = (int)std::min<uint64_t>(L.long_segments, (uint64_t)num_sms() * 8);
         k_pass_longseg_generic<<<segs, kGenericThreads, 0, s>>>(a);
         HQ_CHECK_LAUNCH();
-        a.slot0 = short_grid();
+        a.slot0 = tile_grid(sh);
         size_t smem2 = sizeof(double) * ((size_t)sh.L + sh.kn);
         set_smem((const void*)k_pass_longfix_generic, smem2);
         k_pass_longfix_generic<<<long_grid(L), kGenericThreads, smem2, s>>>(a);

@@ -3,21 +3,30 @@
 //
 // Same contract as the generic tile kernel in hq_pass.cu (per row i of the
 // mode-n unfolding: Y_i, a_i = Y_i G_(n)^T or U_n[i], partials of
-// M = sum a_i^T Y_i, W = sum a_i^T a_i, max|a_i|), mapped onto the B200 FP64
-// datapath, which DFMA and DMMA share (measured: 35.4 / 37.1 TFLOP/s alone,
-// 36.7 mixed — tools/microbench_mix.cu):
+// M = sum a_i^T Y_i, W = sum a_i^T a_i, max|a_i|), mapped onto B200:
 //
-//  * tile = R consecutive short rows; rows are ranked by length inside the
-//    tile and dealt to warps in that order, so the TR lanes of a row and the
-//    rows sharing a warp run loops of near-equal length.
-//  * Kronecker phase (DFMA): lane (row, pb, qb) owns a BP x BQ block of
-//    Y_i = sum_e x_e U_a[j_e, :] (x) U_b[k_e, :]; factor rows are gathered
-//    straight from L2 with 16-byte loads (two 80-byte rows per nonzero is the
-//    whole of this pass's random traffic).
-//  * GEMM phase (DMMA m8n8k4 f64): A_tile = Y_tile G_(n)^T and
-//    M += A_tile^T Y_tile with G^T and Y_tile in shared memory; M's C
-//    fragments live in registers across all tiles of the CTA.
-//  * W += A^T A and max|A| with DFMA on the A tile in shared memory.
+//  * FP64 datapath: DFMA and DMMA share it (35.4 / 37.1 TFLOP/s alone, 36.7
+//    mixed; tools/microbench_mix.cu), so the pass minimises issue slots:
+//    DFMA for the per-nonzero Kronecker rows, DMMA m8n8k4 for the per-row
+//    GEMMs.
+//  * Memory: the only random traffic is two factor rows per nonzero.  A
+//    tile's rows are gathered in bulk with cp.async (every row of the tile in
+//    flight at once, no registers held), factor rows with an L2 evict_last
+//    policy and the nonzero streams with evict_first; small CTAs (128
+//    threads, 3 per SM at K = 10) let one CTA's gathers overlap another's
+//    arithmetic.
+//
+// Per tile of R consecutive short rows (rows with <= kShortMax nonzeros):
+//   1. row lengths, virtual offsets (scan), rows ranked by length and dealt to
+//      lanes in that order (equal loop lengths per warp);
+//   2. records (x, j, k) of the tile -> smem (cp.async), then the two factor
+//      rows of every record -> smem (cp.async 16 B), CAP records per round;
+//   3. Kronecker rows: lane (row, pb, qb) accumulates a BP x BQ block of
+//      Y_i = sum_e x_e U_a[j_e, :] (x) U_b[k_e, :] (DFMA);
+//   4. Y tile -> smem (aliasing the gather buffer); A_tile = Y_tile G_(n)^T
+//      (DMMA, G_(n)^T fragments from L1) or U_n rows; A written; max|A|;
+//   5. M += A_tile^T Y_tile (DMMA, C fragments resident in registers for the
+//      CTA's whole tile range), W += A^T A (DFMA).
 // Deterministic: fixed row->lane assignment per tile, fixed tile->CTA
 // assignment, per-CTA partial slots reduced in fixed order.
 #include <algorithm>
@@ -34,88 +43,120 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                  : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
-
-// Loads B consecutive doubles starting at p (8-byte aligned; 16-byte aligned
-// when `odd` is false) with 16-byte loads and no divergence: always reads the
-// aligned window [p - odd, p - odd + 2*ceil((B+1)/2)) and shifts.
-template <int B>
-__device__ __forceinline__ void load_part(const double* p, bool odd, double (&v)[B]) {
-    constexpr int W = (B + 2) / 2;  // double2 words covering B+1 doubles
-    double w[2 * W];
-    const double* base = p - (odd ? 1 : 0);
-#pragma unroll
-    for (int i = 0; i < W; ++i) {
-        double2 d = ldg2(base + 2 * i);
-        w[2 * i] = d.x;
-        w[2 * i + 1] = d.y;
-    }
-#pragma unroll
-    for (int i = 0; i < B; ++i) v[i] = odd ? w[i + 1] : w[i];
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
 }
 
-// Exact-width loads when every block start is 16-byte aligned.
-template <int B>
-__device__ __forceinline__ void load_part_aligned(const double* p, double (&v)[B]) {
-#pragma unroll
-    for (int i = 0; i < B / 2; ++i) {
-        double2 d = ldg2(p + 2 * i);
-        v[2 * i] = d.x;
-        v[2 * i + 1] = d.y;
-    }
-    if (B & 1) v[B - 1] = __ldg(p + B - 1);
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+__device__ __forceinline__ void cp16(void* dst, const void* src, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
+                 "l"(pol));
+}
+__device__ __forceinline__ void cp8(void* dst, const void* src, uint64_t pol) {
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(smem_addr(dst)), "l"(src),
+                 "l"(pol));
+}
+__device__ __forceinline__ void cp4(void* dst, const void* src, uint64_t pol) {
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(smem_addr(dst)), "l"(src),
+                 "l"(pol));
+}
+__device__ __forceinline__ void cp_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// B consecutive doubles from shared memory at p (8-byte aligned; 16-byte
+// aligned when `odd` is false) with 16-byte loads and no divergence.
+template <int B>
+__device__ __forceinline__ void lds_part(const double* p, bool odd, double (&v)[B]) {
+    if constexpr (B % 2 == 0) {
+#pragma unroll
+        for (int i = 0; i < B / 2; ++i) {
+            const double2 d = *reinterpret_cast<const double2*>(p + 2 * i);
+            v[2 * i] = d.x;
+            v[2 * i + 1] = d.y;
+        }
+    } else {
+        constexpr int W = (B + 2) / 2;
+        double w[2 * W];
+        const double* base = p - (odd ? 1 : 0);
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            const double2 d = *reinterpret_cast<const double2*>(base + 2 * i);
+            w[2 * i] = d.x;
+            w[2 * i + 1] = d.y;
+        }
+#pragma unroll
+        for (int i = 0; i < B; ++i) v[i] = odd ? w[i + 1] : w[i];
+    }
+}
+
+struct Rec {
+    double x;
+    uint32_t j, k;
+};
 
 template <int KA, int KB, int KN>
 struct Cfg {
     static constexpr int L = KA * KB;
     static constexpr int TP = 2;
     static constexpr int TQ = (KB >= 16) ? 4 : 2;
-    static constexpr int TR = TP * TQ;          // lanes per row
+    static constexpr int TR = TP * TQ;           // lanes per row
     static constexpr int BP = KA / TP;
     static constexpr int BQ = KB / TQ;
-    static constexpr int RPW = 32 / TR;         // rows per warp
-    static constexpr int WARPS = 8;
+    static constexpr int WARPS = 4;
     static constexpr int THREADS = 32 * WARPS;
-    static constexpr int R = RPW * WARPS;       // rows per tile
-    static constexpr int LP = (L + 7) / 8 * 8;  // Y columns padded to whole n-tiles
-    static constexpr int LDY = LP + 4;          // Y row stride (doubles)
-    static constexpr int NT = (KN + 7) / 8;     // A n-tiles
-    static constexpr int GLD = NT * 8;          // G^T row stride
-    static constexpr int ALD = NT * 8 + 1;      // A tile row stride
-    static constexpr int MT = NT;               // M m-tiles
-    static constexpr int NLT = LP / 8;          // M n-tiles
-    static constexpr int MB = MT * NLT;         // M blocks
+    static constexpr int R = THREADS / TR;       // rows per tile
+    static constexpr int RPW = 32 / TR;          // rows per warp
+    static constexpr int LP = (L + 7) / 8 * 8;   // Y columns padded to whole n-tiles
+    static constexpr int LDY = LP + 4;           // Y row stride (== 4 mod 8 doubles)
+    static constexpr int NT = (KN + 7) / 8;      // A n-tiles / M m-tiles
+    static constexpr int ALD = NT * 8 + 4;       // A tile row stride
+    static constexpr int NLT = LP / 8;           // M n-tiles
+    static constexpr int MB = NT * NLT;          // M blocks
     static constexpr int MBW = (MB + WARPS - 1) / WARPS;
-    static constexpr int AB = (R / 8) * NT;     // A blocks
+    static constexpr int AB = (R / 8) * NT;      // A blocks
     static constexpr int ABW = (AB + WARPS - 1) / WARPS;
     static constexpr int WQ = (KN * KN + THREADS - 1) / THREADS;
+    static constexpr int FW = KA + KB;           // staged doubles per record (two factor rows)
+    static constexpr int CAP = (KB >= 16) ? 192 : 384;  // records per gather round
+    static constexpr int MINB = (KB >= 16) ? 2 : 3;     // CTAs per SM the register budget targets
     static_assert(KA % TP == 0 && KB % TQ == 0, "rank split");
+    static_assert(KA % 2 == 0 && KB % 2 == 0, "16-byte factor rows");
     static_assert(L % 4 == 0, "k-steps of 4");
     static_assert(R % 8 == 0, "m-tiles of 8 rows");
-    static constexpr size_t smem_doubles = (size_t)L * GLD + (size_t)R * LDY + (size_t)R * ALD;
-    static constexpr size_t smem_bytes = smem_doubles * 8 + 2 * R * sizeof(int);
+    // shared memory: gather buffer (aliased by the Y tile), records, A tile, row info
+    static constexpr size_t GBUF = (size_t)CAP * FW > (size_t)R * LDY ? (size_t)CAP * FW : (size_t)R * LDY;
+    static constexpr size_t smem_bytes =
+        GBUF * 8 + (size_t)CAP * sizeof(Rec) + (size_t)R * ALD * 8 + 4 * R * sizeof(int) + 64;
 };
 
 template <int KA, int KB, int KN>
-__global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS)
+__global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MINB)
     k_pass_fast3(FastArgs a) {
     using C = Cfg<KA, KB, KN>;
     if (skip_kernel(a.st, a.run_if)) return;
-    extern __shared__ double sm[];
-    double* sG = sm;                                  // L x GLD   (G_(n)^T, zero-padded)
-    double* sY = sG + (size_t)C::L * C::GLD;          // R x LDY   (Kronecker rows)
-    double* sA = sY + (size_t)C::R * C::LDY;          // R x ALD   (a_i rows)
+    extern __shared__ __align__(16) double sm[];
+    double* sF = sm;                                        // CAP x FW gathered factor rows
+    double* sY = sm;                                        // R x LDY Kronecker rows (after the gather)
+    Rec* sRec = reinterpret_cast<Rec*>(sm + C::GBUF);       // CAP records
+    double* sA = reinterpret_cast<double*>(sRec + C::CAP);  // R x ALD a_i rows
     int* sLen = reinterpret_cast<int*>(sA + (size_t)C::R * C::ALD);
-    int* sPerm = sLen + C::R;
+    int* sOff = sLen + C::R;   // virtual record offset of each row
+    int* sPerm = sOff + C::R;  // lane slot -> row
+    int* sTot = sPerm + C::R;  // [0] records in the tile
     __shared__ double red[C::WARPS];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int q = tid; q < C::L * C::GLD; q += C::THREADS) {
-        int l = q / C::GLD, r = q - l * C::GLD;
-        sG[q] = (a.kind == kTTMcTC && r < KN) ? a.gt[(size_t)l * KN + r] : 0.0;
-    }
-    for (int q = tid; q < C::R * C::LDY; q += C::THREADS) sY[q] = 0.0;
+    const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
     for (int q = tid; q < C::R * C::ALD; q += C::THREADS) sA[q] = 0.0;
 
     // ---- tile range of this CTA (nnz-balanced, static)
@@ -144,9 +185,7 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS)
 
     const double* __restrict__ Ua = a.ua;
     const double* __restrict__ Ub = a.ub;
-    const double* __restrict__ val = a.val;
-    const uint32_t* __restrict__ ia = a.ia;
-    const uint32_t* __restrict__ ib = a.ib;
+    const double* __restrict__ gt = a.gt;
 
     // lane roles in the Kronecker phase
     const int rslot = warp * C::RPW + lane / C::TR;
@@ -157,67 +196,96 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS)
     for (int64_t t = t0; t < t1; ++t) {
         const uint64_t r0 = (uint64_t)t * C::R;
         const int nr = (int)min((uint64_t)C::R, a.rows - r0);
+        // 1. lengths (-1: long row, handled by the segmented path), offsets, ranking
         if (tid < C::R) {
             int len = 0;
             if (tid < nr) {
-                int64_t l = a.rowptr[r0 + tid + 1] - a.rowptr[r0 + tid];
-                len = (l > kShortMax) ? -1 : (int)l;  // -1: long row (segmented path)
+                const int64_t l = a.rowptr[r0 + tid + 1] - a.rowptr[r0 + tid];
+                len = (l > kShortMax) ? -1 : (int)l;
             }
             sLen[tid] = len;
         }
         __syncthreads();
-        if (tid < C::R) {  // rank rows by length, descending, ties by index
+        if (tid < C::R) {
             const int me = max(sLen[tid], 0);
-            int rank = 0;
+            int rank = 0, off = 0;
             for (int r = 0; r < C::R; ++r) {
-                int o = max(sLen[r], 0);
+                const int o = max(sLen[r], 0);
                 rank += (o > me) || (o == me && r < tid);
+                off += (r < tid) ? o : 0;
             }
             sPerm[rank] = tid;
+            sOff[tid] = off;
+            if (tid == C::R - 1) sTot[0] = off + me;
         }
         __syncthreads();
+        const int total = sTot[0];
+        const int lr = sPerm[rslot];
+        const int len = max(sLen[lr], 0);
+        const int voff = sOff[lr];
 
-        // ---- Kronecker rows (DFMA)
-        {
-            const int lr = sPerm[rslot];
-            const int len = max(sLen[lr], 0);
-            const int64_t zb = len ? a.rowptr[r0 + lr] : 0;
-            double acc[C::BP][C::BQ];
+        double acc[C::BP][C::BQ];
 #pragma unroll
-            for (int p = 0; p < C::BP; ++p)
+        for (int p = 0; p < C::BP; ++p)
 #pragma unroll
-                for (int q = 0; q < C::BQ; ++q) acc[p][q] = 0.0;
-            for (int e = 0; e < len; ++e) {
-                const int64_t z = zb + e;
-                const double x = __ldg(val + z);
-                const uint32_t j = __ldg(ia + z), k = __ldg(ib + z);
+            for (int q = 0; q < C::BQ; ++q) acc[p][q] = 0.0;
+
+        for (int cv = 0; cv < total; cv += C::CAP) {
+            const int cn = min(C::CAP, total - cv);
+            // 2a. records of virtual positions [cv, cv + cn)
+            for (int v = tid; v < cn; v += C::THREADS) {
+                const int vv = cv + v;
+                int lo = 0, hi = C::R - 1;  // last row whose offset is <= vv
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (sOff[mid] <= vv) lo = mid; else hi = mid - 1;
+                }
+                while (sOff[lo] + max(sLen[lo], 0) <= vv) ++lo;  // never needed; defensive
+                const int64_t pz = a.rowptr[r0 + lo] + (vv - sOff[lo]);
+                cp8(&sRec[v].x, a.val + pz, pol_stream);
+                cp4(&sRec[v].j, a.ia + pz, pol_stream);
+                cp4(&sRec[v].k, a.ib + pz, pol_stream);
+            }
+            cp_wait_all();
+            __syncthreads();
+            // 2b. factor rows of every record: FW/2 16-byte pieces each
+            constexpr int PA = KA / 2, PP = (KA + KB) / 2;
+            for (int q = tid; q < cn * PP; q += C::THREADS) {
+                const int e = q / PP, pc = q - e * PP;
+                const Rec& r = sRec[e];
+                const double* src = (pc < PA) ? Ua + (size_t)r.j * KA + 2 * pc : Ub + (size_t)r.k * KB + 2 * (pc - PA);
+                cp16(sF + (size_t)e * C::FW + 2 * pc, src, pol_keep);
+            }
+            cp_wait_all();
+            __syncthreads();
+            // 3. Kronecker rows from shared memory
+            const int e0 = max(voff, cv) - cv, e1 = min(voff + len, cv + cn) - cv;
+            for (int e = e0; e < e1; ++e) {
+                const double x = sRec[e].x;
+                const double* f = sF + (size_t)e * C::FW;
                 double sa[C::BP], vb[C::BQ];
-                if constexpr (C::BP % 2 == 0) {
-                    load_part_aligned<C::BP>(Ua + (size_t)j * KA + p0, sa);
-                } else {
-                    load_part<C::BP>(Ua + (size_t)j * KA + p0, (p0 & 1) != 0, sa);
-                }
-                if constexpr (C::BQ % 2 == 0) {
-                    load_part_aligned<C::BQ>(Ub + (size_t)k * KB + q0, vb);
-                } else {
-                    load_part<C::BQ>(Ub + (size_t)k * KB + q0, (q0 & 1) != 0, vb);
-                }
+                lds_part<C::BP>(f + p0, (p0 & 1) != 0, sa);
+                lds_part<C::BQ>(f + KA + q0, (q0 & 1) != 0, vb);
 #pragma unroll
                 for (int p = 0; p < C::BP; ++p) {
-                    const double s = x * sa[p];
+                    const double sx = x * sa[p];
 #pragma unroll
-                    for (int q = 0; q < C::BQ; ++q) acc[p][q] = fma(s, vb[q], acc[p][q]);
+                    for (int q = 0; q < C::BQ; ++q) acc[p][q] = fma(sx, vb[q], acc[p][q]);
                 }
             }
+            __syncthreads();
+        }
+        // 4. Y tile (aliases the gather buffer)
+        {
             double* y = sY + (size_t)lr * C::LDY;
 #pragma unroll
             for (int p = 0; p < C::BP; ++p)
 #pragma unroll
                 for (int q = 0; q < C::BQ; ++q) y[(p0 + p) * KB + q0 + q] = acc[p][q];
+            if (C::LP > C::L && pb == 0 && qb == 0)
+                for (int l = C::L; l < C::LP; ++l) y[l] = 0.0;
         }
         __syncthreads();
-
-        // ---- a_i rows: A_tile = Y_tile G^T (DMMA) or U_n rows
         if (a.kind == kTTMcTC) {
 #pragma unroll
             for (int bi = 0; bi < C::ABW; ++bi) {
@@ -225,10 +293,15 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS)
                 if (b < C::AB) {
                     const int mt = b / C::NT, nt = b - mt * C::NT;
                     const double* yrow = sY + (size_t)(mt * 8 + (lane >> 2)) * C::LDY + (lane & 3);
-                    const double* gcol = sG + (size_t)(lane & 3) * C::GLD + nt * 8 + (lane >> 2);
+                    const int gcolidx = nt * 8 + (lane >> 2);
+                    const bool gvalid = gcolidx < KN;
+                    const double* gcol = gt + (size_t)(lane & 3) * KN + (gvalid ? gcolidx : 0);
                     double c0 = 0.0, c1 = 0.0;
 #pragma unroll 5
-                    for (int ks = 0; ks < C::L / 4; ++ks) dmma884(c0, c1, yrow[ks * 4], gcol[(size_t)ks * 4 * C::GLD]);
+                    for (int ks = 0; ks < C::L / 4; ++ks) {
+                        const double gv = gvalid ? __ldg(gcol + (size_t)ks * 4 * KN) : 0.0;
+                        dmma884(c0, c1, yrow[ks * 4], gv);
+                    }
                     const int row = mt * 8 + (lane >> 2);
                     const int col = nt * 8 + 2 * (lane & 3);
                     sA[row * C::ALD + col] = c0;
@@ -237,15 +310,14 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS)
             }
         } else {
             for (int q = tid; q < C::R * KN; q += C::THREADS) {
-                int row = q / KN, r = q - row * KN;
+                const int row = q / KN, r = q - row * KN;
                 sA[row * C::ALD + r] = (row < nr && sLen[row] >= 0) ? a.un[(r0 + row) * KN + r] : 0.0;
             }
         }
         __syncthreads();
-        // write A (short rows only), max|A|
         for (int q = tid; q < C::R * KN; q += C::THREADS) {
-            int row = q / KN, r = q - row * KN;
-            double v = sA[row * C::ALD + r];
+            const int row = q / KN, r = q - row * KN;
+            const double v = sA[row * C::ALD + r];
             if (row < nr && sLen[row] >= 0) {
                 if (a.A) a.A[(r0 + row) * KN + r] = v;
                 mx = fmax(mx, fabs(v));
@@ -254,8 +326,7 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS)
             }
         }
         __syncthreads();
-
-        // ---- M += A_tile^T Y_tile (DMMA, C fragments in registers)
+        // 5. M += A_tile^T Y_tile (DMMA), W += A^T A (DFMA)
 #pragma unroll
         for (int bi = 0; bi < C::MBW; ++bi) {
             const int b = warp + bi * C::WARPS;
@@ -263,12 +334,11 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS)
                 const int mt = b / C::NLT, nt = b - mt * C::NLT;
                 const double* acol = sA + (size_t)(lane & 3) * C::ALD + mt * 8 + (lane >> 2);
                 const double* ycol = sY + (size_t)(lane & 3) * C::LDY + nt * 8 + (lane >> 2);
-#pragma unroll 4
+#pragma unroll
                 for (int ks = 0; ks < C::R / 4; ++ks)
                     dmma884(macc[bi][0], macc[bi][1], acol[(size_t)ks * 4 * C::ALD], ycol[(size_t)ks * 4 * C::LDY]);
             }
         }
-        // ---- W += A^T A (DFMA)
 #pragma unroll
         for (int wi = 0; wi < C::WQ; ++wi) {
             const int q = tid + wi * C::THREADS;
@@ -314,7 +384,7 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS)
 }
 
 template <int KA, int KB, int KN>
-bool launch_fast3(const FastArgs& a, int grid, cudaStream_t s) {
+void launch_fast3(const FastArgs& a, int grid, cudaStream_t s) {
     using C = Cfg<KA, KB, KN>;
     auto fn = k_pass_fast3<KA, KB, KN>;
     static bool attr = false;
@@ -324,13 +394,19 @@ bool launch_fast3(const FastArgs& a, int grid, cudaStream_t s) {
     }
     fn<<<grid, C::THREADS, C::smem_bytes, s>>>(a);
     HQ_CHECK_LAUNCH();
-    return true;
+}
+
+template <int KA, int KB, int KN>
+int grid_fast3() {
+    return num_sms() * Cfg<KA, KB, KN>::MINB;
 }
 
 }  // namespace
 
 int fast_grid(int ka, int kb, int kn) {
-    (void)ka; (void)kb; (void)kn;
+    if (ka == 10 && kb == 10 && kn == 10) return grid_fast3<10, 10, 10>();
+    if (ka == 16 && kb == 16 && kn == 16) return grid_fast3<16, 16, 16>();
+    if (ka == 8 && kb == 8 && kn == 8) return grid_fast3<8, 8, 8>();
     return num_sms() * 2;
 }
 

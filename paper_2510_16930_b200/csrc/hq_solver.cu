@@ -145,7 +145,11 @@ struct Solver {
     double initial_objective = 0.0;
 
     DBuf<double> U[kMaxOrder][2];
-    DBuf<double> core, gt, A, mpart, wpart, maxpart, ypart, mred, wred, maxv, r1inv, rinv, w2part, ppart, hh;
+    DBuf<double> core, gt, A, mpart, wpart, maxpart, ypart, mred, wred, maxv, r1inv, rinv, w2part, hh;
+    DBuf<double> ppart[kMaxOrder];  // per-mode drift products (their drift kernels run on the side stream)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork[kMaxOrder] = {nullptr};
+    cudaEvent_t ev_join = nullptr;
     DBuf<double> tr_obj, tr_fit, tr_drift, fit_prev;
     DBuf<DevStatus> st;
     ModeShape sh[kMaxOrder];
@@ -159,6 +163,10 @@ struct Solver {
         for (auto& g : graph)
             if (g) cudaGraphExecDestroy(g);
         for (auto e : ev) cudaEventDestroy(e);
+        for (auto e : ev_fork)
+            if (e) cudaEventDestroy(e);
+        if (ev_join) cudaEventDestroy(ev_join);
+        if (side) cudaStreamDestroy(side);
     }
 
     FactorPtrs factors_for_mode(int n, int p) const {
@@ -219,8 +227,11 @@ struct Solver {
         r1inv.alloc(kmax * kmax);
         rinv.alloc(kmax * kmax);
         w2part.alloc((size_t)dense_slots() * kmax * kmax);
-        ppart.alloc((size_t)dense_slots() * kmax * kmax);
+        for (int v = 0; v < N; ++v) ppart[v].alloc((size_t)dense_slots() * ranks[v] * ranks[v]);
         hh.alloc(2 * maxIK + 8);
+        HQ_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        for (int v = 0; v < N; ++v) HQ_CUDA(cudaEventCreateWithFlags(&ev_fork[v], cudaEventDisableTiming));
+        HQ_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
         tr_obj.alloc(cfg.max_sweeps);
         tr_fit.alloc(cfg.max_sweeps);
         tr_drift.alloc(cfg.max_sweeps * N);
@@ -286,14 +297,25 @@ struct Solver {
         launch_chol2(w2part.get(), dense_slots(), K, r1inv.get(), rinv.get(), mred.get(), &m, core.get(), S, s);
         double* unew = U[n][1 - p].get();
         const double* uold = U[n][p].get();
-        launch_apply(A.get(), rows, K, rinv.get(), unew, uold, ppart.get(), true, S, kOnlyCholQR, s);
+        double* pp = ppart[n].get();
+        launch_apply(A.get(), rows, K, rinv.get(), unew, uold, pp, true, S, kOnlyCholQR, s);
         // Householder branch (device flag)
         launch_householder(A.get(), rows, K, unew, hh.get(), S, kOnlyFallback, s);
-        launch_apply(nullptr, rows, K, nullptr, unew, uold, ppart.get(), false, S, kOnlyFallback, s);
+        launch_apply(nullptr, rows, K, nullptr, unew, uold, pp, false, S, kOnlyFallback, s);
         compute_core(p, kOnlyFallback, n);
         SweepTrace tr{tr_obj.get(), tr_fit.get(), tr_drift.get(), fit_prev.get()};
-        launch_drift(ppart.get(), dense_slots(), K, core.get(), core_size, dns, N, n, n == N - 1,
-                     cfg.tol_fit_change, cfg.max_sweeps, tr, S, s);
+        if (n < N - 1) {
+            // the drift feeds only the trace: run it beside the next mode update
+            HQ_CUDA(cudaEventRecord(ev_fork[n], s));
+            HQ_CUDA(cudaStreamWaitEvent(side, ev_fork[n], 0));
+            launch_drift(pp, dense_slots(), K, core.get(), core_size, dns, N, n, false, cfg.tol_fit_change,
+                         cfg.max_sweeps, tr, S, side);
+        } else {
+            HQ_CUDA(cudaEventRecord(ev_join, side));
+            HQ_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+            launch_drift(pp, dense_slots(), K, core.get(), core_size, dns, N, n, true, cfg.tol_fit_change,
+                         cfg.max_sweeps, tr, S, s);
+        }
     }
 
     void issue_sweep(int p) {

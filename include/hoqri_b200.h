@@ -169,6 +169,27 @@ int hq_solver_download(hq_solver* s, double* const* factors_out, double* core_ou
 int hq_solver_mode_pass_work(const hq_solver* s, int mode, double* flops, double* bytes);
 int hq_solver_ttmctc_work(const hq_solver* s, int mode, double* flops, double* bytes);
 
+/* ------------------------------------------------------------- multi-GPU --
+ * One process per GPU.  Every rank builds the same tensor;
+ * for each mode the unfolding's rows are split into contiguous whole-row
+ * ranges of ~nnz/P nonzeros (the row partition of SPEC.md:247), each rank
+ * runs the pass on its rows, K x K / K x L partials are all-reduced and new
+ * factor rows broadcast from their owners (NCCL, captured in the sweep
+ * graph).  The reference has no multi-GPU path; this is the north_star's. */
+typedef struct hq_comm hq_comm;
+
+/* NCCL unique id (128 bytes) — call on one rank, share with the others */
+int hq_nccl_unique_id(uint8_t* id_out);
+/* communicator on the current CUDA device; world 1 needs no NCCL */
+int hq_comm_create(int world, int rank, const uint8_t* id, hq_comm** out);
+int hq_comm_destroy(hq_comm* c);
+/* host planner: rank r owns rows [bounds[r], bounds[r+1]) given a mode's
+ * bucket offsets (length rows + 1); bounds has world + 1 slots */
+int hq_partition_rows(const uint64_t* offsets, uint64_t rows, int world, uint64_t* bounds);
+/* hq_solver_create on a communicator: the device-resident solve, distributed */
+int hq_solver_create_dist(const hq_tensor* t, const hq_config* cfg, const double* const* init_factors, void* stream,
+                          const hq_comm* comm, hq_solver** out);
+
 #ifdef __cplusplus
 }
 #endif

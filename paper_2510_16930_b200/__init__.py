@@ -115,7 +115,8 @@ EXPORTED_SYMBOLS = [
     "hq_config_default", "hq_hoqri", "hq_fit_error",
     "hq_solver_create", "hq_solver_destroy", "hq_solver_run", "hq_solver_sync", "hq_solver_launch_mode_pass",
     "hq_solver_launch_ttmctc", "hq_solver_launches_per_sweep", "hq_solver_download", "hq_solver_mode_pass_work",
-    "hq_solver_ttmctc_work",
+    "hq_solver_ttmctc_work", "hq_nccl_unique_id", "hq_comm_create", "hq_comm_destroy", "hq_partition_rows",
+    "hq_solver_create_dist",
 ]
 
 _lib = None
@@ -160,6 +161,11 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.hq_solver_download.argtypes = [vp, vp, vp, C.POINTER(HqTrace)]
     L.hq_solver_mode_pass_work.argtypes = [vp, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.hq_solver_ttmctc_work.argtypes = [vp, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.hq_nccl_unique_id.argtypes = [vp]
+    L.hq_comm_create.argtypes = [C.c_int, C.c_int, vp, pp]
+    L.hq_comm_destroy.argtypes = [vp]
+    L.hq_partition_rows.argtypes = [_u64p, C.c_uint64, C.c_int, _u64p]
+    L.hq_solver_create_dist.argtypes = [vp, C.POINTER(HqConfig), vp, vp, vp, pp]
     _lib = L
     return L
 
@@ -539,11 +545,46 @@ def fit_error(x: SparseTensor, model: TuckerModel) -> float:
 
 
 # ---------------------------------------------------- device-resident API --
+def partition_rows(offsets, world: int) -> np.ndarray:
+    """Row partition of one mode (rank r owns rows [b[r], b[r+1])): contiguous
+    whole rows with ~nnz/world nonzeros each.  Host code, no GPU needed."""
+    off = np.ascontiguousarray(np.asarray(offsets, dtype=np.uint64))
+    b = np.zeros(world + 1, np.uint64)
+    _check(load_library().hq_partition_rows(off, off.size - 1, world, b))
+    return b
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(load_library().hq_nccl_unique_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)
+
+
+class Comm:
+    """NCCL communicator of one rank (one process per GPU, current device)."""
+
+    def __init__(self, world: int, rank: int, uid: bytes = b"\0" * 128):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        _check(load_library().hq_comm_create(world, rank, C.cast(buf, C.c_void_p), C.byref(h)))
+        self._h = h
+        self.world, self.rank = world, rank
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                load_library().hq_comm_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
 class Solver:
     """Device-resident solve for benchmarks: every operand stays in HBM; sweeps
-    and single kernels are launched on `stream` (a cudaStream_t as int)."""
+    and single kernels are launched on `stream` (a cudaStream_t as int).  With
+    `comm`, the rows of every mode are partitioned over the ranks."""
 
-    def __init__(self, x: SparseTensor, config: SolverConfig, init_factors=None, stream: int = 0):
+    def __init__(self, x: SparseTensor, config: SolverConfig, init_factors=None, stream: int = 0, comm: "Comm" = None):
         L = load_library()
         self.x = x
         self.n = x.order()
@@ -556,7 +597,11 @@ class Solver:
             arr = _ptr_array(fs0)
             self._keep = fs0
         h = C.c_void_p()
-        _check(L.hq_solver_create(x.handle, C.byref(cfg), arr, stream or None, C.byref(h)))
+        if comm is not None:
+            self._comm = comm
+            _check(L.hq_solver_create_dist(x.handle, C.byref(cfg), arr, stream or None, comm._h, C.byref(h)))
+        else:
+            _check(L.hq_solver_create(x.handle, C.byref(cfg), arr, stream or None, C.byref(h)))
         self._h = h
 
     def __del__(self):

@@ -20,7 +20,7 @@
 
 namespace hq {
 
-int dense_slots() { return num_sms() * 2; }
+int dense_slots() { return num_sms() * 4; }
 
 namespace {
 
@@ -257,8 +257,8 @@ void launch_gram(const double* A, uint64_t rows, int K, double* wpart, double* m
 }
 
 void launch_chol1(const double* w, const double* maxv, int K, double* r1inv, DevStatus* st, int degenerate_mode,
-                  cudaStream_t s) {
-    k_chol1<<<1, 32, 0, s>>>(w, maxv, K, r1inv, st, degenerate_mode);
+                  cudaStream_t s, bool abort_on_fallback) {
+    k_chol1<<<1, 32, 0, s>>>(w, maxv, K, r1inv, st, degenerate_mode, abort_on_fallback ? 1 : 0);
     HQ_CHECK_LAUNCH();
 }
 
@@ -268,9 +268,10 @@ void launch_gram2(const double* A, uint64_t rows, int K, const double* r1inv, do
 }
 
 void launch_chol2(const double* wpart, int nslots, int K, const double* r1inv, double* rinv, const double* m,
-                  const ModeShape* sh, double* core_out, DevStatus* st, cudaStream_t s) {
+                  const ModeShape* sh, double* core_out, DevStatus* st, cudaStream_t s, bool abort_on_fallback) {
     ModeShape z{};
-    k_chol2<<<1, 256, 0, s>>>(wpart, nslots, K, r1inv, rinv, m, sh ? *sh : z, m != nullptr, core_out, st);
+    k_chol2<<<1, 1024, 0, s>>>(wpart, nslots, K, r1inv, rinv, m, sh ? *sh : z, m != nullptr, core_out, st,
+                               abort_on_fallback ? 1 : 0);
     HQ_CHECK_LAUNCH();
 }
 
@@ -285,7 +286,7 @@ void launch_apply(const double* A, uint64_t rows, int K, const double* rinv, dou
 void launch_drift(const double* ppart, int nslots, int K, const double* core, uint64_t core_size, double dns,
                   int order, int mode, bool end_of_sweep, double tol, uint64_t max_sweeps, const SweepTrace& tr,
                   DevStatus* st, cudaStream_t s) {
-    k_drift<<<1, 256, 0, s>>>(ppart, nslots, K, core, core_size, dns, order, mode, end_of_sweep ? 1 : 0, tol,
+    k_drift<<<1, 1024, 0, s>>>(ppart, nslots, K, core, core_size, dns, order, mode, end_of_sweep ? 1 : 0, tol,
                               max_sweeps, tr, st);
     HQ_CHECK_LAUNCH();
 }

@@ -39,14 +39,15 @@ void launch_gram(const double* A, uint64_t rows, int K, double* wpart, double* m
 // degenerate_mode > 0), Cholesky of W, inverse of R1; sets st->fallback when
 // CholeskyQR2 would lose accuracy
 void launch_chol1(const double* w, const double* maxv, int K, double* r1inv, DevStatus* st, int degenerate_mode,
-                  cudaStream_t s);
+                  cudaStream_t s, bool abort_on_fallback = false);
 // W2 partials of (A R1^-1)^T (A R1^-1)
 void launch_gram2(const double* A, uint64_t rows, int K, const double* r1inv, double* wpart, const DevStatus* st,
                   cudaStream_t s);
 // Cholesky of W2 (reduced from partials), Rinv = R1inv R2inv; if m != null,
 // G_(n) = Rinv^T M refolded into the core layout (core_out)
 void launch_chol2(const double* wpart, int nslots, int K, const double* r1inv, double* rinv, const double* m,
-                  const ModeShape* sh, double* core_out, DevStatus* st, cudaStream_t s);
+                  const ModeShape* sh, double* core_out, DevStatus* st, cudaStream_t s,
+                  bool abort_on_fallback = false);
 // U = A Rinv (written to u_out when non-null); P partials of U^T U_old when
 // u_old non-null.  apply=false: U read from u_out (fallback drift).
 void launch_apply(const double* A, uint64_t rows, int K, const double* rinv, double* u_out, const double* u_old,

@@ -6,7 +6,8 @@
 namespace hq {
 
 struct FastArgs {
-    uint64_t rows;
+    uint64_t rbase;  // first row of the processed range
+    uint64_t rows;   // rows in the range
     const int64_t* rowptr;
     const double* val;
     const uint32_t* ia;   // first other mode's index
@@ -23,7 +24,15 @@ struct FastArgs {
     int slot0;
     const DevStatus* st;
     int run_if;
+    // L2 residency: the first gathered factor (ua) is marked persisting for
+    // the launch when l2_bytes > 0 (cudaLaunchAttributeAccessPolicyWindow)
+    size_t l2_bytes;
+    float l2_hit;
 };
+
+// Sets the device's persisting-L2 carve-out to its maximum once and returns
+// it (bytes); 0 when the device has none.
+size_t l2_persist_budget();
 
 bool fast_supported(const ModeShape& sh);
 int fast_grid(int ka, int kb, int kn);

@@ -136,7 +136,8 @@ namespace {
 
 struct PassArgs {
     ModeShape sh;
-    uint64_t rows;
+    uint64_t rbase;  // first row of the processed range
+    uint64_t rows;   // rows in the range
     const int64_t* rowptr;
     const double* val;
     const uint32_t* idx[kMaxOrder - 1];
@@ -174,10 +175,11 @@ __device__ __forceinline__ void col_digits(const ModeShape& sh, int col, int* ki
 
 __device__ int64_t tile_lower(const PassArgs& a, int64_t z) {
     int64_t lo = 0, hi = a.ntiles;
+    const int64_t zb = a.rowptr[a.rbase];
     while (lo < hi) {
         int64_t mid = (lo + hi) >> 1;
-        uint64_t r = min((uint64_t)mid * a.R, a.rows);
-        if (a.rowptr[r] >= z)
+        uint64_t r = a.rbase + min((uint64_t)mid * a.R, a.rows);
+        if (a.rowptr[r] - zb >= z)
             hi = mid;
         else
             lo = mid + 1;
@@ -203,7 +205,7 @@ __global__ void __launch_bounds__(kGenericThreads) k_pass_tiles_generic(PassArgs
     double* Y = sm;
     double* as = sm + (size_t)R * L;
     const int G = gridDim.x, c = blockIdx.x;
-    const int64_t Z = a.rowptr[a.rows];
+    const int64_t Z = a.rowptr[a.rbase + a.rows] - a.rowptr[a.rbase];
     const int64_t t0 = tile_lower(a, (Z * c) / G);
     const int64_t t1 = (c == G - 1) ? a.ntiles : tile_lower(a, (Z * (c + 1)) / G);
     const int slot = a.slot0 + c;
@@ -213,8 +215,8 @@ __global__ void __launch_bounds__(kGenericThreads) k_pass_tiles_generic(PassArgs
     for (int q = threadIdx.x; q < Kn * Kn; q += blockDim.x) wp[q] = 0.0;
     double mx = 0.0;
     for (int64_t t = t0; t < t1; ++t) {
-        const uint64_t r0 = (uint64_t)t * R;
-        const int nr = (int)min((uint64_t)R, a.rows - r0);
+        const uint64_t r0 = a.rbase + (uint64_t)t * R;
+        const int nr = (int)min((uint64_t)R, a.rbase + a.rows - r0);
         for (int q = threadIdx.x; q < nr * L; q += blockDim.x) {
             int lr = q / L, col = q - lr * L;
             uint64_t i = r0 + lr;
@@ -271,6 +273,7 @@ __global__ void __launch_bounds__(kGenericThreads) k_pass_longseg_generic(PassAr
     for (uint64_t sg = blockIdx.x; sg < a.nseg; sg += gridDim.x) {
         int64_t sb = a.seg_begin[sg];
         uint32_t row = a.long_ids[a.seg_row[sg]];
+        if (row < a.rbase || row >= a.rbase + a.rows) continue;
         int64_t se = min(sb + kSegLen, a.rowptr[row + 1]);
         for (int col = threadIdx.x; col < L; col += blockDim.x) {
             int kidx[kMaxOrder - 1];
@@ -300,6 +303,7 @@ __global__ void __launch_bounds__(kGenericThreads) k_pass_longfix_generic(PassAr
     double mx = 0.0;
     for (uint64_t lr = lb; lr < le; ++lr) {
         const uint32_t row = a.long_ids[lr];
+        if (row < a.rbase || row >= a.rbase + a.rows) continue;
         const int64_t s0 = a.long_segptr[lr], s1 = a.long_segptr[lr + 1];
         for (int col = threadIdx.x; col < L; col += blockDim.x) {
             double y = 0.0;
@@ -342,6 +346,11 @@ int short_grid() { return num_sms() * 2; }
 
 // HQ_FORCE_GENERIC=1 routes every shape through the generic kernels (tests
 // compare both paths on the same inputs).
+bool l2_window_enabled() {
+    const char* e = std::getenv("HQ_NO_L2_WINDOW");
+    return !(e && e[0] == '1');
+}
+
 bool force_generic() {
     const char* e = std::getenv("HQ_FORCE_GENERIC");
     return e && e[0] == '1';
@@ -371,13 +380,17 @@ int pass_launch_count(const ModeLayout& L, const ModeShape& sh) {
 }
 
 void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const FactorPtrs& f, PassKind kind,
-                 const double* gt, const PassOut& out, const DevStatus* st, int run_if, cudaStream_t s) {
+                 const double* gt, const PassOut& out, const DevStatus* st, int run_if, cudaStream_t s,
+                 uint64_t row_begin, uint64_t row_end) {
     const ModeLayout& L = T.modes[mode];
+    row_end = std::min<uint64_t>(row_end, L.rows);
+    row_begin = std::min(row_begin, row_end);
     if ((size_t)sh.L * 8 > 200 * 1024)
         fail(HQ_ERR_CAPACITY, "Kronecker row of " + std::to_string(sh.L) + " entries exceeds the device kernel limit");
     PassArgs a{};
     a.sh = sh;
-    a.rows = L.rows;
+    a.rbase = row_begin;
+    a.rows = row_end - row_begin;
     a.rowptr = L.rowptr.get();
     a.val = L.val.get();
     for (int j = 0; j < sh.nothers; ++j) {
@@ -398,11 +411,12 @@ void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const Fac
     a.nseg = L.long_segments;
 
     a.R = generic_rows_per_tile(sh);
-    a.ntiles = (int64_t)ceil_div(L.rows, a.R);
+    a.ntiles = (int64_t)ceil_div(a.rows, a.R);
     a.slot0 = 0;
     if (fast_supported(sh) && !force_generic()) {
         FastArgs fa{};
-        fa.rows = L.rows;
+        fa.rbase = a.rbase;
+        fa.rows = a.rows;
         fa.rowptr = a.rowptr;
         fa.val = a.val;
         fa.ia = a.idx[0];
@@ -419,6 +433,10 @@ void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const Fac
         fa.slot0 = 0;
         fa.st = st;
         fa.run_if = run_if;
+        const size_t fbytes = (size_t)T.dims[L.others[0]] * sh.ko[0] * sizeof(double);
+        const size_t budget = l2_window_enabled() ? l2_persist_budget() : 0;
+        fa.l2_bytes = budget ? fbytes : 0;
+        fa.l2_hit = budget ? (float)std::min(1.0, (double)budget / (double)fbytes) : 0.f;
         launch_fast(fa, sh, tile_grid(sh), s);
     } else {
         size_t smem = sizeof(double) * ((size_t)a.R * sh.L + (size_t)a.R * sh.kn);

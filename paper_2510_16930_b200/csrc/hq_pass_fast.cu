@@ -48,6 +48,11 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -73,30 +78,29 @@ __device__ __forceinline__ void cp_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
-// B consecutive doubles from shared memory at p (8-byte aligned; 16-byte
-// aligned when `odd` is false) with 16-byte loads and no divergence.
+// Loads the B doubles of a lane's block starting at element `st` of a staged
+// factor row with 16-byte shared loads and no selects: for odd B the element
+// that breaks 16-byte alignment is loaded last and the lane keeps its own
+// local->global index map (blk_index) for the write-back.
 template <int B>
-__device__ __forceinline__ void lds_part(const double* p, bool odd, double (&v)[B]) {
-    if constexpr (B % 2 == 0) {
+__device__ __forceinline__ void lds_block(const double* f, int st, double (&v)[B]) {
+    const int odd = st & 1;
+    const double* pr = f + st + odd;
 #pragma unroll
-        for (int i = 0; i < B / 2; ++i) {
-            const double2 d = *reinterpret_cast<const double2*>(p + 2 * i);
-            v[2 * i] = d.x;
-            v[2 * i + 1] = d.y;
-        }
-    } else {
-        constexpr int W = (B + 2) / 2;
-        double w[2 * W];
-        const double* base = p - (odd ? 1 : 0);
-#pragma unroll
-        for (int i = 0; i < W; ++i) {
-            const double2 d = *reinterpret_cast<const double2*>(base + 2 * i);
-            w[2 * i] = d.x;
-            w[2 * i + 1] = d.y;
-        }
-#pragma unroll
-        for (int i = 0; i < B; ++i) v[i] = odd ? w[i + 1] : w[i];
+    for (int i = 0; i < B / 2; ++i) {
+        const double2 d = *reinterpret_cast<const double2*>(pr + 2 * i);
+        v[2 * i] = d.x;
+        v[2 * i + 1] = d.y;
     }
+    if constexpr (B & 1) v[B - 1] = f[odd ? st : st + B - 1];
+}
+template <int B>
+__device__ __forceinline__ int blk_index(int st, int i) {
+    const int odd = st & 1;
+    if constexpr (B & 1) {
+        if (i == B - 1) return odd ? st : st + B - 1;
+    }
+    return st + odd + i;
 }
 
 struct Rec {
@@ -156,19 +160,25 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
     __shared__ double red[C::WARPS];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
+    const uint64_t pol_stream = policy_evict_first();
+    // with a persisting window on U_a its gathers carry no explicit hint and
+    // U_b streams; without one both factors are asked to stay (evict_last)
+    const uint64_t pol_a = a.l2_bytes ? policy_evict_normal() : policy_evict_last();
+    const uint64_t pol_b = a.l2_bytes ? pol_stream : policy_evict_last();
     for (int q = tid; q < C::R * C::ALD; q += C::THREADS) sA[q] = 0.0;
 
     // ---- tile range of this CTA (nnz-balanced, static)
     const int G = gridDim.x, c = blockIdx.x;
     const int64_t ntiles = (int64_t)((a.rows + C::R - 1) / C::R);
-    const int64_t Z = a.rowptr[a.rows];
+    const uint64_t rend = a.rbase + a.rows;
+    const int64_t zb = a.rowptr[a.rbase];
+    const int64_t Z = a.rowptr[rend] - zb;
     auto lower = [&](int64_t z) {
         int64_t lo = 0, hi = ntiles;
         while (lo < hi) {
             int64_t mid = (lo + hi) >> 1;
-            uint64_t r = min((uint64_t)mid * C::R, a.rows);
-            if (a.rowptr[r] >= z) hi = mid; else lo = mid + 1;
+            uint64_t r = a.rbase + min((uint64_t)mid * C::R, a.rows);
+            if (a.rowptr[r] - zb >= z) hi = mid; else lo = mid + 1;
         }
         return lo;
     };
@@ -191,11 +201,12 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
     const int rslot = warp * C::RPW + lane / C::TR;
     const int pb = (lane % C::TR) / C::TQ, qb = lane % C::TQ;
     const int p0 = pb * C::BP, q0 = qb * C::BQ;
+    const int sub = lane % C::TR;
 
     __syncthreads();
     for (int64_t t = t0; t < t1; ++t) {
-        const uint64_t r0 = (uint64_t)t * C::R;
-        const int nr = (int)min((uint64_t)C::R, a.rows - r0);
+        const uint64_t r0 = a.rbase + (uint64_t)t * C::R;
+        const int nr = (int)min((uint64_t)C::R, rend - r0);
         // 1. lengths (-1: long row, handled by the segmented path), offsets, ranking
         if (tid < C::R) {
             int len = 0;
@@ -223,6 +234,7 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
         const int lr = sPerm[rslot];
         const int len = max(sLen[lr], 0);
         const int voff = sOff[lr];
+        const int64_t rbase = (len ? a.rowptr[r0 + lr] : 0) - voff;  // physical position = rbase + virtual
 
         double acc[C::BP][C::BQ];
 #pragma unroll
@@ -232,29 +244,28 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
 
         for (int cv = 0; cv < total; cv += C::CAP) {
             const int cn = min(C::CAP, total - cv);
-            // 2a. records of virtual positions [cv, cv + cn)
-            for (int v = tid; v < cn; v += C::THREADS) {
-                const int vv = cv + v;
-                int lo = 0, hi = C::R - 1;  // last row whose offset is <= vv
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (sOff[mid] <= vv) lo = mid; else hi = mid - 1;
+            // 2a. records of virtual positions [cv, cv + cn): each row's lanes copy their row
+            {
+                const int lo = max(voff, cv), hi = min(voff + len, cv + cn);
+                for (int v = lo + sub; v < hi; v += C::TR) {
+                    const int64_t pz = rbase + v;
+                    cp8(&sRec[v - cv].x, a.val + pz, pol_stream);
+                    cp4(&sRec[v - cv].j, a.ia + pz, pol_stream);
+                    cp4(&sRec[v - cv].k, a.ib + pz, pol_stream);
                 }
-                while (sOff[lo] + max(sLen[lo], 0) <= vv) ++lo;  // never needed; defensive
-                const int64_t pz = a.rowptr[r0 + lo] + (vv - sOff[lo]);
-                cp8(&sRec[v].x, a.val + pz, pol_stream);
-                cp4(&sRec[v].j, a.ia + pz, pol_stream);
-                cp4(&sRec[v].k, a.ib + pz, pol_stream);
             }
             cp_wait_all();
             __syncthreads();
-            // 2b. factor rows of every record: FW/2 16-byte pieces each
-            constexpr int PA = KA / 2, PP = (KA + KB) / 2;
-            for (int q = tid; q < cn * PP; q += C::THREADS) {
-                const int e = q / PP, pc = q - e * PP;
-                const Rec& r = sRec[e];
-                const double* src = (pc < PA) ? Ua + (size_t)r.j * KA + 2 * pc : Ub + (size_t)r.k * KB + 2 * (pc - PA);
-                cp16(sF + (size_t)e * C::FW + 2 * pc, src, pol_keep);
+            // 2b. both factor rows of every record (16-byte pieces)
+            for (int e = tid; e < cn; e += C::THREADS) {
+                const Rec r = sRec[e];
+                const double* ua = Ua + (size_t)r.j * KA;
+                const double* ub = Ub + (size_t)r.k * KB;
+                double* dst = sF + (size_t)e * C::FW;
+#pragma unroll
+                for (int pc = 0; pc < KA / 2; ++pc) cp16(dst + 2 * pc, ua + 2 * pc, pol_a);
+#pragma unroll
+                for (int pc = 0; pc < KB / 2; ++pc) cp16(dst + KA + 2 * pc, ub + 2 * pc, pol_b);
             }
             cp_wait_all();
             __syncthreads();
@@ -264,8 +275,8 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
                 const double x = sRec[e].x;
                 const double* f = sF + (size_t)e * C::FW;
                 double sa[C::BP], vb[C::BQ];
-                lds_part<C::BP>(f + p0, (p0 & 1) != 0, sa);
-                lds_part<C::BQ>(f + KA + q0, (q0 & 1) != 0, vb);
+                lds_block<C::BP>(f, p0, sa);
+                lds_block<C::BQ>(f + KA, q0, vb);
 #pragma unroll
                 for (int p = 0; p < C::BP; ++p) {
                     const double sx = x * sa[p];
@@ -281,31 +292,46 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
 #pragma unroll
             for (int p = 0; p < C::BP; ++p)
 #pragma unroll
-                for (int q = 0; q < C::BQ; ++q) y[(p0 + p) * KB + q0 + q] = acc[p][q];
+                for (int q = 0; q < C::BQ; ++q) y[blk_index<C::BP>(p0, p) * KB + blk_index<C::BQ>(q0, q)] = acc[p][q];
             if (C::LP > C::L && pb == 0 && qb == 0)
                 for (int l = C::L; l < C::LP; ++l) y[l] = 0.0;
         }
         __syncthreads();
         if (a.kind == kTTMcTC) {
+            // all of this warp's A blocks share one n-tile (b = warp + WARPS*bi, WARPS % NT == 0):
+            // interleave the blocks and split the k-chain in two for ILP
+            static_assert(C::WARPS % C::NT == 0, "warp -> n-tile mapping");
+            const int nt = warp % C::NT;
+            const int gcolidx = nt * 8 + (lane >> 2);
+            const bool gvalid = gcolidx < KN;
+            const double* gcol = gt + (size_t)(lane & 3) * KN + (gvalid ? gcolidx : 0);
+            constexpr int KSN = C::L / 4;
+            double g[KSN];
+#pragma unroll
+            for (int ks = 0; ks < KSN; ++ks) g[ks] = gvalid ? __ldg(gcol + (size_t)ks * 4 * KN) : 0.0;
+            double c[C::ABW][2][2];
+#pragma unroll
+            for (int bi = 0; bi < C::ABW; ++bi) c[bi][0][0] = c[bi][0][1] = c[bi][1][0] = c[bi][1][1] = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < KSN; ++ks)
+#pragma unroll
+                for (int bi = 0; bi < C::ABW; ++bi) {
+                    const int b = warp + bi * C::WARPS;
+                    if (b < C::AB) {
+                        const int mt = b / C::NT;
+                        const double yv = sY[(size_t)(mt * 8 + (lane >> 2)) * C::LDY + (lane & 3) + ks * 4];
+                        dmma884(c[bi][ks & 1][0], c[bi][ks & 1][1], yv, g[ks]);
+                    }
+                }
 #pragma unroll
             for (int bi = 0; bi < C::ABW; ++bi) {
                 const int b = warp + bi * C::WARPS;
                 if (b < C::AB) {
-                    const int mt = b / C::NT, nt = b - mt * C::NT;
-                    const double* yrow = sY + (size_t)(mt * 8 + (lane >> 2)) * C::LDY + (lane & 3);
-                    const int gcolidx = nt * 8 + (lane >> 2);
-                    const bool gvalid = gcolidx < KN;
-                    const double* gcol = gt + (size_t)(lane & 3) * KN + (gvalid ? gcolidx : 0);
-                    double c0 = 0.0, c1 = 0.0;
-#pragma unroll 5
-                    for (int ks = 0; ks < C::L / 4; ++ks) {
-                        const double gv = gvalid ? __ldg(gcol + (size_t)ks * 4 * KN) : 0.0;
-                        dmma884(c0, c1, yrow[ks * 4], gv);
-                    }
+                    const int mt = b / C::NT;
                     const int row = mt * 8 + (lane >> 2);
                     const int col = nt * 8 + 2 * (lane & 3);
-                    sA[row * C::ALD + col] = c0;
-                    sA[row * C::ALD + col + 1] = c1;
+                    sA[row * C::ALD + col] = c[bi][0][0] + c[bi][1][0];
+                    sA[row * C::ALD + col + 1] = c[bi][0][1] + c[bi][1][1];
                 }
             }
         } else {
@@ -328,17 +354,17 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
         __syncthreads();
         // 5. M += A_tile^T Y_tile (DMMA), W += A^T A (DFMA)
 #pragma unroll
-        for (int bi = 0; bi < C::MBW; ++bi) {
-            const int b = warp + bi * C::WARPS;
-            if (b < C::MB) {
-                const int mt = b / C::NLT, nt = b - mt * C::NLT;
-                const double* acol = sA + (size_t)(lane & 3) * C::ALD + mt * 8 + (lane >> 2);
-                const double* ycol = sY + (size_t)(lane & 3) * C::LDY + nt * 8 + (lane >> 2);
+        for (int ks = 0; ks < C::R / 4; ++ks)
 #pragma unroll
-                for (int ks = 0; ks < C::R / 4; ++ks)
-                    dmma884(macc[bi][0], macc[bi][1], acol[(size_t)ks * 4 * C::ALD], ycol[(size_t)ks * 4 * C::LDY]);
+            for (int bi = 0; bi < C::MBW; ++bi) {
+                const int b = warp + bi * C::WARPS;
+                if (b < C::MB) {
+                    const int mt = b / C::NLT, nt = b - mt * C::NLT;
+                    const double av = sA[(size_t)(ks * 4 + (lane & 3)) * C::ALD + mt * 8 + (lane >> 2)];
+                    const double yv = sY[(size_t)(ks * 4 + (lane & 3)) * C::LDY + nt * 8 + (lane >> 2)];
+                    dmma884(macc[bi][0], macc[bi][1], av, yv);
+                }
             }
-        }
 #pragma unroll
         for (int wi = 0; wi < C::WQ; ++wi) {
             const int q = tid + wi * C::THREADS;
@@ -392,8 +418,23 @@ void launch_fast3(const FastArgs& a, int grid, cudaStream_t s) {
         HQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes));
         attr = true;
     }
-    fn<<<grid, C::THREADS, C::smem_bytes, s>>>(a);
-    HQ_CHECK_LAUNCH();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(C::THREADS);
+    cfg.dynamicSmemBytes = C::smem_bytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr_l2[1];
+    if (a.l2_bytes) {
+        attr_l2[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr_l2[0].val.accessPolicyWindow.base_ptr = const_cast<double*>(a.ua);
+        attr_l2[0].val.accessPolicyWindow.num_bytes = a.l2_bytes;
+        attr_l2[0].val.accessPolicyWindow.hitRatio = a.l2_hit;
+        attr_l2[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr_l2[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.attrs = attr_l2;
+        cfg.numAttrs = 1;
+    }
+    HQ_CUDA(cudaLaunchKernelEx(&cfg, fn, a));
 }
 
 template <int KA, int KB, int KN>
@@ -402,6 +443,20 @@ int grid_fast3() {
 }
 
 }  // namespace
+
+size_t l2_persist_budget() {
+    static size_t budget = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess || v <= 0) return (size_t)0;
+        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)v) != cudaSuccess) {
+            cudaGetLastError();
+            return (size_t)0;
+        }
+        return (size_t)v;
+    }();
+    return budget;
+}
 
 int fast_grid(int ka, int kb, int kn) {
     if (ka == 10 && kb == 10 && kn == 10) return grid_fast3<10, 10, 10>();

@@ -64,8 +64,11 @@ size_t pass_ypart_doubles(const ModeLayout& L, const ModeShape& sh);
 
 // Launches the pass kernels (no host synchronisation; graph-capturable).
 // gt = G_(n)^T as L x K_n (kTTMcTC only).
+// Only rows [row_begin, row_end) of the mode-n unfolding are processed (the
+// rank's share in a multi-GPU solve; the whole mode by default).
 void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const FactorPtrs& f, PassKind kind,
-                 const double* gt, const PassOut& out, const DevStatus* st, int run_if, cudaStream_t s);
+                 const double* gt, const PassOut& out, const DevStatus* st, int run_if, cudaStream_t s,
+                 uint64_t row_begin = 0, uint64_t row_end = ~0ull);
 // number of kernels launch_pass issues
 int pass_launch_count(const ModeLayout& L, const ModeShape& sh);
 

@@ -77,16 +77,38 @@ __global__ void __launch_bounds__(kRgWarps * 32)
     double mx = 0.0;
     double* sx = sX[warp];
     double* sy = sY[warp];
-    for (uint64_t g = gb; g < ge; ++g) {
+    constexpr int OQ = (8 * K + 31) / 32;  // elements of an 8-row group of `other` per lane
+    double an[C::KS], on[OQ];  // next group's operands (one group of 8 rows in flight ahead)
+    auto load_a = [&](uint64_t g, double (&dst)[C::KS], double (&od)[OQ]) {
         const uint64_t row = g * 8 + gid;
-        const bool rv = row < rows;
-        double a[C::KS];
+        const bool rv = g < ge && row < rows;
 #pragma unroll
         for (int ks = 0; ks < C::KS; ++ks) {
             const int k = 4 * ks + tig;
-            a[ks] = (rv && k < K) ? A[row * K + k] : 0.0;
+            dst[ks] = (rv && k < K) ? A[row * K + k] : 0.0;
+        }
+        if (other) {
+#pragma unroll
+            for (int i = 0; i < OQ; ++i) {
+                const int q = lane + 32 * i;
+                const uint64_t e = g * 8 * K + q;
+                od[i] = (g < ge && q < 8 * K && e < rows * K) ? other[e] : 0.0;
+            }
+        }
+    };
+    load_a(gb, an, on);
+    for (uint64_t g = gb; g < ge; ++g) {
+        const uint64_t row = g * 8 + gid;
+        const bool rv = row < rows;
+        double a[C::KS], o[OQ];
+#pragma unroll
+        for (int ks = 0; ks < C::KS; ++ks) {
+            a[ks] = an[ks];
             mx = fmax(mx, fabs(a[ks]));
         }
+#pragma unroll
+        for (int i = 0; i < OQ; ++i) o[i] = on[i];
+        load_a(g + 1, an, on);
         // X = A T (C fragment: row gid, cols 8nt + 2 tig + {0,1})
 #pragma unroll
         for (int nt = 0; nt < C::NT; ++nt) {
@@ -102,10 +124,13 @@ __global__ void __launch_bounds__(kRgWarps * 32)
             }
         }
         if (other) {
-            for (int q = lane; q < 8 * K; q += 32) {
-                const int r = q / K, cc = q - r * K;
-                const uint64_t rr = g * 8 + r;
-                sy[r * C::LD + cc] = (rr < rows) ? other[rr * K + cc] : 0.0;
+#pragma unroll
+            for (int i = 0; i < OQ; ++i) {
+                const int q = lane + 32 * i;
+                if (q < 8 * K) {
+                    const int r = q / K, cc = q - r * K;
+                    sy[r * C::LD + cc] = o[i];
+                }
             }
         }
         __syncwarp();
@@ -153,7 +178,7 @@ __global__ void __launch_bounds__(kRgWarps * 32)
 template <int K>
 void launch_rg(const double* A, uint64_t rows, const double* T, double* out, const double* other, double* part,
                double* maxpart, const DevStatus* st, int run_if, cudaStream_t s) {
-    k_rowgemm<K><<<dense_slots(), kRgWarps * 32, 0, s>>>(A, rows, T, out, other, part, maxpart, st, run_if);
+    k_rowgemm<K><<<dense_slots(), kRgWarps * 32, 0, s>>>(A, rows, T, out, other, part, maxpart, st, run_if);  // dense_slots() = 4 CTAs/SM
     HQ_CHECK_LAUNCH();
 }
 

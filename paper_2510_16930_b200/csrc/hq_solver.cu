@@ -28,6 +28,7 @@
 #include <random>
 #include <thread>
 
+#include "hq_comm.cuh"
 #include "hq_dense.cuh"
 
 namespace hq {
@@ -151,6 +152,12 @@ struct Solver {
     cudaEvent_t ev_fork[kMaxOrder] = {nullptr};
     cudaEvent_t ev_join = nullptr;
     DBuf<double> tr_obj, tr_fit, tr_drift, fit_prev;
+    // multi-GPU: this rank owns rows [bnd[n][rank], bnd[n][rank+1]) of every mode n
+    const Comm* comm = nullptr;
+    std::vector<uint64_t> bnd[kMaxOrder];
+    DBuf<double> w2red, pred;  // all-reduced K x K Gram / drift product (distributed path)
+    uint64_t rb(int n) const { return comm ? bnd[n][comm->rank] : 0; }
+    uint64_t re(int n) const { return comm ? bnd[n][comm->rank + 1] : dims[n]; }
     DBuf<DevStatus> st;
     ModeShape sh[kMaxOrder];
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
@@ -182,8 +189,10 @@ struct Solver {
         return PassOut{a, mpart.get(), wpart.get(), maxpart.get(), ypart.get()};
     }
 
-    void setup(const DeviceTensor* t, const hq_config* c, const double* const* init, cudaStream_t stream) {
+    void setup(const DeviceTensor* t, const hq_config* c, const double* const* init, cudaStream_t stream,
+               const Comm* cm = nullptr) {
         T = t;
+        comm = (cm && cm->world > 1) ? cm : nullptr;
         s = stream;
         cfg = *c;
         N = t->order;
@@ -229,6 +238,19 @@ struct Solver {
         w2part.alloc((size_t)dense_slots() * kmax * kmax);
         for (int v = 0; v < N; ++v) ppart[v].alloc((size_t)dense_slots() * ranks[v] * ranks[v]);
         hh.alloc(2 * maxIK + 8);
+        w2red.alloc(kmax * kmax);
+        pred.alloc(kmax * kmax);
+        if (comm) {
+            for (int v = 0; v < N; ++v) {
+                std::vector<int64_t> off(dims[v] + 1);
+                HQ_CUDA(cudaMemcpyAsync(off.data(), t->modes[v].rowptr.get(), sizeof(int64_t) * off.size(),
+                                        cudaMemcpyDeviceToHost, s));
+                HQ_CUDA(cudaStreamSynchronize(s));
+                std::vector<uint64_t> uo(off.begin(), off.end());
+                bnd[v].assign(comm->world + 1, 0);
+                partition_rows(uo.data(), dims[v], comm->world, bnd[v].data());
+            }
+        }
         HQ_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
         for (int v = 0; v < N; ++v) HQ_CUDA(cudaEventCreateWithFlags(&ev_fork[v], cudaEventDisableTiming));
         HQ_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
@@ -277,44 +299,69 @@ struct Solver {
             f.u[v] = U[v][q].get();
             f.k[v] = ranks[v];
         }
-        launch_pass(*T, 0, sh[0], f, kCore, nullptr, pass_out(nullptr), st.get(), run_if, s);
+        launch_pass(*T, 0, sh[0], f, kCore, nullptr, pass_out(nullptr), st.get(), run_if, s, rb(0), re(0));
         launch_reduce_core(mpart.get(), pass_slots(T->modes[0], sh[0]), core_size, core.get(), st.get(), run_if, s);
+        if (comm && run_if != kOnlyFallback) comm->allreduce_sum(core.get(), core_size, s);
     }
 
     void mode_update(int n, int p) {
         const ModeShape& m = sh[n];
         const int K = ranks[n];
-        const uint64_t rows = dims[n];
+        const uint64_t r0 = rb(n), r1 = re(n), lrows = r1 - r0;
         FactorPtrs f = factors_for_mode(n, p);
         DevStatus* S = st.get();
         launch_gt(core.get(), m, ranks, gt.get(), S, s);
-        launch_pass(*T, n, m, f, kTTMcTC, gt.get(), pass_out(A.get()), S, kAlways, s);
+        launch_pass(*T, n, m, f, kTTMcTC, gt.get(), pass_out(A.get()), S, kAlways, s, r0, r1);
         const int slots = pass_slots(T->modes[n], m);
         launch_reduce_pass(mpart.get(), m.kn * m.L, wpart.get(), K * K, maxpart.get(), slots, mred.get(), wred.get(),
                            maxv.get(), S, kAlways, s);
-        launch_chol1(wred.get(), maxv.get(), K, r1inv.get(), S, n + 1, s);
-        launch_gram2(A.get(), rows, K, r1inv.get(), w2part.get(), S, s);
-        launch_chol2(w2part.get(), dense_slots(), K, r1inv.get(), rinv.get(), mred.get(), &m, core.get(), S, s);
+        if (comm) {  // M, W, max|A| over all ranks' rows
+            comm->allreduce_sum(mred.get(), (size_t)m.kn * m.L, s);
+            comm->allreduce_sum(wred.get(), (size_t)K * K, s);
+            comm->allreduce_max(maxv.get(), 1, s);
+        }
+        launch_chol1(wred.get(), maxv.get(), K, r1inv.get(), S, n + 1, s, comm != nullptr);
+        const double* a_loc = A.get() + r0 * K;
         double* unew = U[n][1 - p].get();
         const double* uold = U[n][p].get();
         double* pp = ppart[n].get();
-        launch_apply(A.get(), rows, K, rinv.get(), unew, uold, pp, true, S, kOnlyCholQR, s);
-        // Householder branch (device flag)
-        launch_householder(A.get(), rows, K, unew, hh.get(), S, kOnlyFallback, s);
-        launch_apply(nullptr, rows, K, nullptr, unew, uold, pp, false, S, kOnlyFallback, s);
-        compute_core(p, kOnlyFallback, n);
+        int pslots = dense_slots();
+        if (!comm) {
+            launch_gram2(a_loc, lrows, K, r1inv.get(), w2part.get(), S, s);
+            launch_chol2(w2part.get(), dense_slots(), K, r1inv.get(), rinv.get(), mred.get(), &m, core.get(), S, s);
+            launch_apply(a_loc, lrows, K, rinv.get(), unew, uold, pp, true, S, kOnlyCholQR, s);
+            // Householder branch (device flag)
+            launch_householder(A.get(), dims[n], K, unew, hh.get(), S, kOnlyFallback, s);
+            launch_apply(nullptr, dims[n], K, nullptr, unew, uold, pp, false, S, kOnlyFallback, s);
+            compute_core(p, kOnlyFallback, n);
+        } else {
+            launch_gram2(a_loc, lrows, K, r1inv.get(), w2part.get(), S, s);
+            launch_reduce_pass(nullptr, 0, w2part.get(), K * K, nullptr, dense_slots(), nullptr, w2red.get(), nullptr, S,
+                               kOnlyCholQR, s);
+            comm->allreduce_sum(w2red.get(), (size_t)K * K, s);
+            launch_chol2(w2red.get(), 1, K, r1inv.get(), rinv.get(), mred.get(), &m, core.get(), S, s, true);
+            launch_apply(a_loc, lrows, K, rinv.get(), unew + r0 * K, uold + r0 * K, pp, true, S, kOnlyCholQR, s);
+            launch_reduce_pass(nullptr, 0, pp, K * K, nullptr, dense_slots(), nullptr, pred.get(), nullptr, S, kAlways,
+                               s);
+            comm->allreduce_sum(pred.get(), (size_t)K * K, s);
+            comm->allgather_rows(unew, bnd[n].data(), (size_t)K, s);
+            // per-mode copy point: the side-stream drift of mode n reads pred_m[n]
+            HQ_CUDA(cudaMemcpyAsync(ppart[n].get(), pred.get(), sizeof(double) * K * K, cudaMemcpyDeviceToDevice, s));
+            pp = ppart[n].get();
+            pslots = 1;
+        }
         SweepTrace tr{tr_obj.get(), tr_fit.get(), tr_drift.get(), fit_prev.get()};
         if (n < N - 1) {
             // the drift feeds only the trace: run it beside the next mode update
             HQ_CUDA(cudaEventRecord(ev_fork[n], s));
             HQ_CUDA(cudaStreamWaitEvent(side, ev_fork[n], 0));
-            launch_drift(pp, dense_slots(), K, core.get(), core_size, dns, N, n, false, cfg.tol_fit_change,
-                         cfg.max_sweeps, tr, S, side);
+            launch_drift(pp, pslots, K, core.get(), core_size, dns, N, n, false, cfg.tol_fit_change, cfg.max_sweeps,
+                         tr, S, side);
         } else {
             HQ_CUDA(cudaEventRecord(ev_join, side));
             HQ_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
-            launch_drift(pp, dense_slots(), K, core.get(), core_size, dns, N, n, true, cfg.tol_fit_change,
-                         cfg.max_sweeps, tr, S, s);
+            launch_drift(pp, pslots, K, core.get(), core_size, dns, N, n, true, cfg.tol_fit_change, cfg.max_sweeps,
+                         tr, S, s);
         }
     }
 
@@ -377,6 +424,9 @@ struct Solver {
     }
 
     void check_status(const DevStatus& h) {
+        if (h.abort == 3)
+            fail(HQ_ERR_DIAGNOSTIC, "rank-deficient TTMcTC output in a multi-GPU solve (CholeskyQR2 breakdown); the "
+                                    "Householder fallback runs on one GPU: rerun with a single rank");
         if (h.abort == 1)
             fail(HQ_ERR_DEGENERATE,
                  "degenerate state: TTMcTC output is identically zero for mode " + std::to_string(h.degenerate_mode),
@@ -713,6 +763,42 @@ int hq_solver_create(const hq_tensor* t, const hq_config* cfg, const double* con
         if (cfg->trace_gradients || cfg->tol_grad > 0.0)
             fail(HQ_ERR_CAPACITY, "gradient tracing is not implemented on the device engine yet");
         h->impl->setup(&t->t, cfg, init_factors, s);
+        *out = h.release();
+    });
+}
+
+int hq_nccl_unique_id(uint8_t* id_out) {
+    return guard([&] { nccl_unique_id(id_out); });
+}
+
+int hq_comm_create(int world, int rank, const uint8_t* id, hq_comm** out) {
+    return guard([&] {
+        auto c = std::make_unique<hq_comm>();
+        c->impl = comm_create(world, rank, id);
+        *out = c.release();
+    });
+}
+
+int hq_comm_destroy(hq_comm* c) {
+    return guard([&] { delete c; });
+}
+
+int hq_partition_rows(const uint64_t* offsets, uint64_t rows, int world, uint64_t* bounds) {
+    return guard([&] {
+        if (world < 1) fail(HQ_ERR_SHAPE, "world size must be positive");
+        partition_rows(offsets, rows, world, bounds);
+    });
+}
+
+int hq_solver_create_dist(const hq_tensor* t, const hq_config* cfg, const double* const* init_factors, void* stream,
+                          const hq_comm* comm, hq_solver** out) {
+    return guard([&] {
+        auto h = std::make_unique<hq_solver>();
+        h->impl = std::make_unique<Solver>();
+        cudaStream_t s = stream ? as_stream(stream) : t->stream;
+        if (cfg->trace_gradients || cfg->tol_grad > 0.0)
+            fail(HQ_ERR_CAPACITY, "gradient tracing is not implemented on the device engine yet");
+        h->impl->setup(&t->t, cfg, init_factors, s, comm ? comm->impl : nullptr);
         *out = h.release();
     });
 }

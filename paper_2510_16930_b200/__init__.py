@@ -122,11 +122,13 @@ EXPORTED_SYMBOLS = [
 _lib = None
 
 
-def load_library(path: str = LIB_PATH) -> C.CDLL:
-    """Loads lib/libhoqri_b200.so (builds it in-tree first if it is missing)."""
+def load_library(path: str = None) -> C.CDLL:
+    """Loads lib/libhoqri_b200.so (builds it in-tree first if it is missing).
+    HQ_LIB overrides the path (kernel-variant experiments)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("HQ_LIB") or LIB_PATH
     if not os.path.exists(path):
         from . import build
         build.build_engine()

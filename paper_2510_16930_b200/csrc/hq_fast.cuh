@@ -33,6 +33,7 @@ struct FastArgs {
 // Sets the device's persisting-L2 carve-out to its maximum once and returns
 // it (bytes); 0 when the device has none.
 size_t l2_persist_budget();
+void debug_phase_cycles(unsigned long long* out, int reset);
 
 bool fast_supported(const ModeShape& sh);
 int fast_grid(int ka, int kb, int kn);

@@ -33,6 +33,36 @@
 
 #include "hq_fast.cuh"
 
+// Debug instrumentation: -DHQ_PHASE_TIMING accumulates per-phase cycles of
+// thread 0 of every CTA into hq_phase_cycles[] (read back with
+// hq_debug_phase_cycles); compiled out otherwise.
+#ifdef HQ_PHASE_TIMING
+__device__ unsigned long long hq_phase_cycles[16];
+#define HQ_PHASE(i)                                                   \
+    do {                                                              \
+        if (threadIdx.x == 0) {                                       \
+            long long _now = clock64();                               \
+            atomicAdd(&hq_phase_cycles[i], (unsigned long long)(_now - _ph_t)); \
+            _ph_t = _now;                                             \
+        }                                                             \
+    } while (0)
+#else
+#define HQ_PHASE(i) do { } while (0)
+#endif
+
+#ifndef HQ_CAP
+#define HQ_CAP 384
+#endif
+#ifndef HQ_MINB
+#define HQ_MINB 2
+#endif
+#ifndef HQ_CAP16
+#define HQ_CAP16 192
+#endif
+#ifndef HQ_MINB16
+#define HQ_MINB16 2
+#endif
+
 namespace hq {
 
 namespace {
@@ -61,6 +91,13 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ double2 ldg2(const double* p, uint64_t pol) {
+    double2 d;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                 : "=d"(d.x), "=d"(d.y)
+                 : "l"(p), "l"(pol));
+    return d;
 }
 __device__ __forceinline__ void cp16(void* dst, const void* src, uint64_t pol) {
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
@@ -130,17 +167,18 @@ struct Cfg {
     static constexpr int AB = (R / 8) * NT;      // A blocks
     static constexpr int ABW = (AB + WARPS - 1) / WARPS;
     static constexpr int WQ = (KN * KN + THREADS - 1) / THREADS;
-    static constexpr int FW = KA + KB;           // staged doubles per record (two factor rows)
-    static constexpr int CAP = (KB >= 16) ? 192 : 384;  // records per gather round
-    static constexpr int MINB = (KB >= 16) ? 2 : 3;     // CTAs per SM the register budget targets
+    static constexpr int FW = KA + KB + ((KA + KB) % 8 == 4 ? 2 : ((KA + KB) % 8 == 0 ? 4 : 0));  // staged doubles per
+    // record: the two factor rows, padded so consecutive records start 8 banks apart (conflict-free 16 B loads)
+    static constexpr int CAP = (KB >= 16) ? HQ_CAP16 : HQ_CAP;  // records per gather round
+    static constexpr int MINB = (KB >= 16) ? HQ_MINB16 : HQ_MINB;  // CTAs per SM the register budget targets
     static_assert(KA % TP == 0 && KB % TQ == 0, "rank split");
     static_assert(KA % 2 == 0 && KB % 2 == 0, "16-byte factor rows");
     static_assert(L % 4 == 0, "k-steps of 4");
     static_assert(R % 8 == 0, "m-tiles of 8 rows");
-    // shared memory: gather buffer (aliased by the Y tile), records, A tile, row info
-    static constexpr size_t GBUF = (size_t)CAP * FW > (size_t)R * LDY ? (size_t)CAP * FW : (size_t)R * LDY;
-    static constexpr size_t smem_bytes =
-        GBUF * 8 + (size_t)CAP * sizeof(Rec) + (size_t)R * ALD * 8 + 4 * R * sizeof(int) + 64;
+    // shared memory: gather buffer, Y tile, two record buffers, A tile, three row-meta slots
+    static constexpr size_t META = (size_t)R * (8 + 4 + 4 + 4) + 16;  // start, len, off, perm, total
+    static constexpr size_t smem_bytes = (size_t)CAP * FW * 8 + (size_t)R * LDY * 8 + 2 * (size_t)CAP * sizeof(Rec) +
+                                         (size_t)R * ALD * 8 + 3 * META + 64;
 };
 
 template <int KA, int KB, int KN>
@@ -148,18 +186,25 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
     k_pass_fast3(FastArgs a) {
     using C = Cfg<KA, KB, KN>;
     if (skip_kernel(a.st, a.run_if)) return;
+#ifdef HQ_PHASE_TIMING
+    long long _ph_t = clock64();
+#endif
     extern __shared__ __align__(16) double sm[];
-    double* sF = sm;                                        // CAP x FW gathered factor rows
-    double* sY = sm;                                        // R x LDY Kronecker rows (after the gather)
-    Rec* sRec = reinterpret_cast<Rec*>(sm + C::GBUF);       // CAP records
-    double* sA = reinterpret_cast<double*>(sRec + C::CAP);  // R x ALD a_i rows
-    int* sLen = reinterpret_cast<int*>(sA + (size_t)C::R * C::ALD);
-    int* sOff = sLen + C::R;   // virtual record offset of each row
-    int* sPerm = sOff + C::R;  // lane slot -> row
-    int* sTot = sPerm + C::R;  // [0] records in the tile
+    double* sF = sm;                                          // CAP x FW gathered factor rows
+    double* sY = sF + (size_t)C::CAP * C::FW;                 // R x LDY Kronecker rows
+    Rec* sRecB = reinterpret_cast<Rec*>(sY + (size_t)C::R * C::LDY);  // 2 x CAP records
+    double* sA = reinterpret_cast<double*>(sRecB + 2 * C::CAP);       // R x ALD a_i rows
+    char* sMetaB = reinterpret_cast<char*>(sA + (size_t)C::R * C::ALD);
+    // row meta of a tile: start position, length (-1: long row), virtual offset, lane slot -> row, total
+    auto m_start = [&](int mb) { return reinterpret_cast<int64_t*>(sMetaB + mb * C::META); };
+    auto m_len = [&](int mb) { return reinterpret_cast<int*>(sMetaB + mb * C::META + 8 * C::R); };
+    auto m_off = [&](int mb) { return m_len(mb) + C::R; };
+    auto m_perm = [&](int mb) { return m_len(mb) + 2 * C::R; };
+    auto m_tot = [&](int mb) { return m_len(mb) + 3 * C::R; };
     __shared__ double red[C::WARPS];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
     const uint64_t pol_stream = policy_evict_first();
     // with a persisting window on U_a its gathers carry no explicit hint and
     // U_b streams; without one both factors are asked to stay (evict_last)
@@ -197,82 +242,142 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
     const double* __restrict__ Ub = a.ub;
     const double* __restrict__ gt = a.gt;
 
+    // G_(n)^T fragments of this warp's n-tile, resident for the whole kernel (L1 is nearly all smem here)
+    static_assert(C::WARPS % C::NT == 0, "warp -> n-tile mapping");
+    constexpr bool kGReg = C::L / 4 <= 32;  // K = 10, 8: fragments fit in registers; K = 16: reloaded per tile
+    double gfr[kGReg ? C::L / 4 : 1];
+    const int gcolidx = (warp % C::NT) * 8 + (lane >> 2);
+    const bool gvalid = a.kind == kTTMcTC && gcolidx < KN;
+    if constexpr (kGReg) {
+#pragma unroll
+        for (int ks = 0; ks < C::L / 4; ++ks)
+            gfr[ks] = gvalid ? __ldg(gt + (size_t)(ks * 4 + (lane & 3)) * KN + gcolidx) : 0.0;
+    }
     // lane roles in the Kronecker phase
     const int rslot = warp * C::RPW + lane / C::TR;
     const int pb = (lane % C::TR) / C::TQ, qb = lane % C::TQ;
     const int p0 = pb * C::BP, q0 = qb * C::BQ;
     const int sub = lane % C::TR;
 
-    __syncthreads();
-    for (int64_t t = t0; t < t1; ++t) {
+    // ---- pipeline helpers (all collective over the CTA unless noted)
+    // row meta of tile t from its rowptr slice (st[0..R] already loaded by threads <= R)
+    auto meta_from = [&](int64_t t, int mb, int64_t st_lo, int64_t st_hi) {
         const uint64_t r0 = a.rbase + (uint64_t)t * C::R;
         const int nr = (int)min((uint64_t)C::R, rend - r0);
-        // 1. lengths (-1: long row, handled by the segmented path), offsets, ranking
         if (tid < C::R) {
             int len = 0;
             if (tid < nr) {
-                const int64_t l = a.rowptr[r0 + tid + 1] - a.rowptr[r0 + tid];
+                const int64_t l = st_hi - st_lo;
                 len = (l > kShortMax) ? -1 : (int)l;
             }
-            sLen[tid] = len;
+            m_len(mb)[tid] = len;
+            m_start(mb)[tid] = st_lo;
         }
         __syncthreads();
         if (tid < C::R) {
-            const int me = max(sLen[tid], 0);
+            const int* ln = m_len(mb);
+            const int me = max(ln[tid], 0);
             int rank = 0, off = 0;
             for (int r = 0; r < C::R; ++r) {
-                const int o = max(sLen[r], 0);
+                const int o = max(ln[r], 0);
                 rank += (o > me) || (o == me && r < tid);
                 off += (r < tid) ? o : 0;
             }
-            sPerm[rank] = tid;
-            sOff[tid] = off;
-            if (tid == C::R - 1) sTot[0] = off + me;
+            m_perm(mb)[rank] = tid;
+            m_off(mb)[tid] = off;
+            if (tid == C::R - 1) m_tot(mb)[0] = off + me;
         }
         __syncthreads();
-        const int total = sTot[0];
-        const int lr = sPerm[rslot];
-        const int len = max(sLen[lr], 0);
-        const int voff = sOff[lr];
-        const int64_t rbase = (len ? a.rowptr[r0 + lr] : 0) - voff;  // physical position = rbase + virtual
+    };
+    auto load_starts = [&](int64_t t, int64_t& lo, int64_t& hi) {  // per thread, tid < R
+        lo = hi = 0;
+        if (t < t1 && tid < C::R) {
+            const uint64_t r = a.rbase + (uint64_t)t * C::R + tid;
+            if (r < rend) {
+                lo = a.rowptr[r];
+                hi = a.rowptr[r + 1];
+            }
+        }
+    };
+    // records of virtual positions [cv, cv + CAP) of tile (meta mb) -> record buffer rb (per row lanes)
+    auto records_issue = [&](int mb, int rb, int cv) {
+        const int lr = m_perm(mb)[rslot];
+        const int len = max(m_len(mb)[lr], 0);
+        const int voff = m_off(mb)[lr];
+        const int64_t pbase = m_start(mb)[lr] - voff;
+        Rec* rec = sRecB + rb * C::CAP;
+        const int lo = max(voff, cv), hi = min(voff + len, cv + C::CAP);
+        for (int v = lo + sub; v < hi; v += C::TR) {
+            const int64_t pz = pbase + v;
+            cp8(&rec[v - cv].x, a.val + pz, pol_stream);
+            cp4(&rec[v - cv].j, a.ia + pz, pol_stream);
+            cp4(&rec[v - cv].k, a.ib + pz, pol_stream);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    // both factor rows of records [0, cn) -> sF with cp.async, piece-major: consecutive lanes copy
+    // consecutive 16-byte pieces of one row.  (Register-staged LDG.128 would double the gather rate but
+    // needs ~100 registers per thread for a whole tile: measured, spills.)
+    constexpr int PA = KA / 2, PP = (KA + KB) / 2;
+    constexpr int ESTEP = C::THREADS / PP, PSTEP = C::THREADS % PP;
+    auto gathers_issue = [&](int rb, int cn) {
+        const Rec* rec = sRecB + rb * C::CAP;
+        int e = tid / PP, pc = tid % PP;
+        for (; e < cn;) {
+            const Rec& r = rec[e];
+            const double* src = (pc < PA) ? Ua + (size_t)r.j * KA + 2 * pc : Ub + (size_t)r.k * KB + 2 * (pc - PA);
+            double* dst = sF + (size_t)e * C::FW + ((pc < PA) ? 2 * pc : KA + 2 * (pc - PA));
+            cp16(dst, src, (pc < PA) ? pol_a : pol_b);
+            e += ESTEP;
+            pc += PSTEP;
+            if (pc >= PP) {
+                pc -= PP;
+                ++e;
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+
+    __syncthreads();
+    if (t0 < t1) {  // prologue: tile t0 gathered, tile t0+1 records in flight
+        int64_t lo, hi;
+        load_starts(t0, lo, hi);
+        meta_from(t0, 0, lo, hi);
+        records_issue(0, 0, 0);
+        cp_wait_all();
+        __syncthreads();
+        gathers_issue(0, min(C::CAP, m_tot(0)[0]));
+        if (t0 + 1 < t1) {
+            load_starts(t0 + 1, lo, hi);
+            meta_from(t0 + 1, 1, lo, hi);
+            records_issue(1, 1, 0);
+        }
+    }
+    for (int64_t t = t0; t < t1; ++t) {
+        const int it = (int)(t - t0);
+        const int mb = it % 3, rb = it & 1;
+        const uint64_t r0 = a.rbase + (uint64_t)t * C::R;
+        const int nr = (int)min((uint64_t)C::R, rend - r0);
+        int64_t pf_lo, pf_hi;  // tile t+2's rowptr slice, prefetched into registers
+        load_starts(t + 2, pf_lo, pf_hi);
+        cp_wait_all();  // gathers(t), records(t+1)
+        __syncthreads();
+        HQ_PHASE(0);
+        const int total = m_tot(mb)[0];
+        const int lr = m_perm(mb)[rslot];
+        const int len = max(m_len(mb)[lr], 0);
+        const int voff = m_off(mb)[lr];
+        const Rec* rec = sRecB + rb * C::CAP;
 
         double acc[C::BP][C::BQ];
 #pragma unroll
         for (int p = 0; p < C::BP; ++p)
 #pragma unroll
             for (int q = 0; q < C::BQ; ++q) acc[p][q] = 0.0;
-
-        for (int cv = 0; cv < total; cv += C::CAP) {
-            const int cn = min(C::CAP, total - cv);
-            // 2a. records of virtual positions [cv, cv + cn): each row's lanes copy their row
-            {
-                const int lo = max(voff, cv), hi = min(voff + len, cv + cn);
-                for (int v = lo + sub; v < hi; v += C::TR) {
-                    const int64_t pz = rbase + v;
-                    cp8(&sRec[v - cv].x, a.val + pz, pol_stream);
-                    cp4(&sRec[v - cv].j, a.ia + pz, pol_stream);
-                    cp4(&sRec[v - cv].k, a.ib + pz, pol_stream);
-                }
-            }
-            cp_wait_all();
-            __syncthreads();
-            // 2b. both factor rows of every record (16-byte pieces)
-            for (int e = tid; e < cn; e += C::THREADS) {
-                const Rec r = sRec[e];
-                const double* ua = Ua + (size_t)r.j * KA;
-                const double* ub = Ub + (size_t)r.k * KB;
-                double* dst = sF + (size_t)e * C::FW;
-#pragma unroll
-                for (int pc = 0; pc < KA / 2; ++pc) cp16(dst + 2 * pc, ua + 2 * pc, pol_a);
-#pragma unroll
-                for (int pc = 0; pc < KB / 2; ++pc) cp16(dst + KA + 2 * pc, ub + 2 * pc, pol_b);
-            }
-            cp_wait_all();
-            __syncthreads();
-            // 3. Kronecker rows from shared memory
-            const int e0 = max(voff, cv) - cv, e1 = min(voff + len, cv + cn) - cv;
+        auto kron = [&](int e0, int e1) {
+#pragma unroll 2
             for (int e = e0; e < e1; ++e) {
-                const double x = sRec[e].x;
+                const double x = rec[e].x;
                 const double* f = sF + (size_t)e * C::FW;
                 double sa[C::BP], vb[C::BQ];
                 lds_block<C::BP>(f, p0, sa);
@@ -284,9 +389,20 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
                     for (int q = 0; q < C::BQ; ++q) acc[p][q] = fma(sx, vb[q], acc[p][q]);
                 }
             }
+        };
+        kron(min(voff, C::CAP), min(voff + len, C::CAP));
+        for (int cv = C::CAP; cv < total; cv += C::CAP) {  // tiles above CAP records: extra synchronous rounds
             __syncthreads();
+            records_issue(mb, rb, cv);
+            cp_wait_all();
+            __syncthreads();
+            gathers_issue(rb, min(C::CAP, total - cv));
+            cp_wait_all();
+            __syncthreads();
+            kron(max(voff, cv) - cv, min(voff + len, cv + C::CAP) - cv);
         }
-        // 4. Y tile (aliases the gather buffer)
+        HQ_PHASE(1);
+        // Y tile
         {
             double* y = sY + (size_t)lr * C::LDY;
 #pragma unroll
@@ -296,19 +412,16 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
             if (C::LP > C::L && pb == 0 && qb == 0)
                 for (int l = C::L; l < C::LP; ++l) y[l] = 0.0;
         }
-        __syncthreads();
+        __syncthreads();  // sF and this tile's record buffer are free
+        HQ_PHASE(2);
+        if (t + 1 < t1) gathers_issue(rb ^ 1, min(C::CAP, m_tot((mb + 1) % 3)[0]));
+        HQ_PHASE(3);
+        const int* ln = m_len(mb);
         if (a.kind == kTTMcTC) {
             // all of this warp's A blocks share one n-tile (b = warp + WARPS*bi, WARPS % NT == 0):
-            // interleave the blocks and split the k-chain in two for ILP
-            static_assert(C::WARPS % C::NT == 0, "warp -> n-tile mapping");
+            // interleave the blocks and split the k-chain in two for ILP; G^T fragments are in gfr[]
             const int nt = warp % C::NT;
-            const int gcolidx = nt * 8 + (lane >> 2);
-            const bool gvalid = gcolidx < KN;
-            const double* gcol = gt + (size_t)(lane & 3) * KN + (gvalid ? gcolidx : 0);
             constexpr int KSN = C::L / 4;
-            double g[KSN];
-#pragma unroll
-            for (int ks = 0; ks < KSN; ++ks) g[ks] = gvalid ? __ldg(gcol + (size_t)ks * 4 * KN) : 0.0;
             double c[C::ABW][2][2];
 #pragma unroll
             for (int bi = 0; bi < C::ABW; ++bi) c[bi][0][0] = c[bi][0][1] = c[bi][1][0] = c[bi][1][1] = 0.0;
@@ -320,7 +433,12 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
                     if (b < C::AB) {
                         const int mt = b / C::NT;
                         const double yv = sY[(size_t)(mt * 8 + (lane >> 2)) * C::LDY + (lane & 3) + ks * 4];
-                        dmma884(c[bi][ks & 1][0], c[bi][ks & 1][1], yv, g[ks]);
+                        double gv;
+                        if constexpr (kGReg)
+                            gv = gfr[ks];
+                        else
+                            gv = gvalid ? __ldg(gt + (size_t)(ks * 4 + (lane & 3)) * KN + gcolidx) : 0.0;
+                        dmma884(c[bi][ks & 1][0], c[bi][ks & 1][1], yv, gv);
                     }
                 }
 #pragma unroll
@@ -337,14 +455,15 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
         } else {
             for (int q = tid; q < C::R * KN; q += C::THREADS) {
                 const int row = q / KN, r = q - row * KN;
-                sA[row * C::ALD + r] = (row < nr && sLen[row] >= 0) ? a.un[(r0 + row) * KN + r] : 0.0;
+                sA[row * C::ALD + r] = (row < nr && ln[row] >= 0) ? a.un[(r0 + row) * KN + r] : 0.0;
             }
         }
         __syncthreads();
+        HQ_PHASE(4);
         for (int q = tid; q < C::R * KN; q += C::THREADS) {
             const int row = q / KN, r = q - row * KN;
             const double v = sA[row * C::ALD + r];
-            if (row < nr && sLen[row] >= 0) {
+            if (row < nr && ln[row] >= 0) {
                 if (a.A) a.A[(r0 + row) * KN + r] = v;
                 mx = fmax(mx, fabs(v));
             } else {
@@ -352,7 +471,8 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
             }
         }
         __syncthreads();
-        // 5. M += A_tile^T Y_tile (DMMA), W += A^T A (DFMA)
+        HQ_PHASE(5);
+        // M += A_tile^T Y_tile (DMMA), W += A^T A (DFMA)
 #pragma unroll
         for (int ks = 0; ks < C::R / 4; ++ks)
 #pragma unroll
@@ -376,6 +496,12 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
             }
         }
         __syncthreads();
+        HQ_PHASE(6);
+        if (t + 2 < t1) {  // tile t+2: meta from the prefetched slice, records into this tile's buffer
+            meta_from(t + 2, (mb + 2) % 3, pf_lo, pf_hi);
+            records_issue((mb + 2) % 3, rb, 0);
+        }
+        HQ_PHASE(7);
     }
 
     // ---- partial slots
@@ -443,6 +569,20 @@ int grid_fast3() {
 }
 
 }  // namespace
+
+#ifdef HQ_PHASE_TIMING
+void debug_phase_cycles(unsigned long long* out, int reset) {
+    HQ_CUDA(cudaMemcpyFromSymbol(out, hq_phase_cycles, sizeof(unsigned long long) * 16));
+    if (reset) {
+        unsigned long long z[16] = {0};
+        HQ_CUDA(cudaMemcpyToSymbol(hq_phase_cycles, z, sizeof(z)));
+    }
+}
+#else
+void debug_phase_cycles(unsigned long long* out, int) {
+    for (int i = 0; i < 16; ++i) out[i] = 0;
+}
+#endif
 
 size_t l2_persist_budget() {
     static size_t budget = [] {

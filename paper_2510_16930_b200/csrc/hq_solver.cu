@@ -30,6 +30,7 @@
 
 #include "hq_comm.cuh"
 #include "hq_dense.cuh"
+#include "hq_fast.cuh"
 
 namespace hq {
 
@@ -765,6 +766,12 @@ int hq_solver_create(const hq_tensor* t, const hq_config* cfg, const double* con
         h->impl->setup(&t->t, cfg, init_factors, s);
         *out = h.release();
     });
+}
+
+// debug: per-phase cycle counters of the specialised pass (zeros unless built
+// with -DHQ_PHASE_TIMING); not part of the public header
+int hq_debug_phase_cycles(unsigned long long* out16, int reset) {
+    return guard([&] { debug_phase_cycles(out16, reset); });
 }
 
 int hq_nccl_unique_id(uint8_t* id_out) {

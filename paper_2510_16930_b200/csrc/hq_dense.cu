@@ -291,6 +291,26 @@ void launch_drift(const double* ppart, int nslots, int K, const double* core, ui
     HQ_CHECK_LAUNCH();
 }
 
+void launch_store_p(const double* ppart, int nslots, int K, int order, int mode, int kmax, uint64_t max_sweeps,
+                    double* trp, const DevStatus* st, cudaStream_t s) {
+    const int blocks = std::max(1, (K * K + 7) / 8);
+    k_store_p<<<blocks, 256, 0, s>>>(ppart, nslots, K, order, mode, kmax, max_sweeps, trp, st);
+    HQ_CHECK_LAUNCH();
+}
+
+void launch_sweep_end(const double* core, uint64_t core_size, double dns, double tol, uint64_t max_sweeps,
+                      const SweepTrace& tr, DevStatus* st, cudaStream_t s) {
+    k_sweep_end<<<1, 1024, 0, s>>>(core, core_size, dns, tol, max_sweeps, tr, st);
+    HQ_CHECK_LAUNCH();
+}
+
+void launch_drift_batch(const double* trp, int pairs, int order, const int* ranks_dev, int kmax, double* drift,
+                        cudaStream_t s) {
+    if (pairs <= 0) return;
+    k_drift_batch<<<pairs, 32, 0, s>>>(trp, pairs, order, ranks_dev, kmax, drift);
+    HQ_CHECK_LAUNCH();
+}
+
 void launch_householder(const double* A, uint64_t rows, int K, double* q_out, double* work, const DevStatus* st,
                         int run_if, cudaStream_t s) {
     k_householder<<<1, kHhThreads, 0, s>>>(A, rows, K, q_out, work, st, run_if);

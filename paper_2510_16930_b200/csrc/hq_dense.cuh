@@ -64,6 +64,15 @@ struct SweepTrace {
 void launch_drift(const double* ppart, int nslots, int K, const double* core, uint64_t core_size, double dns,
                   int order, int mode, bool end_of_sweep, double tol, uint64_t max_sweeps, const SweepTrace& tr,
                   DevStatus* st, cudaStream_t s);
+// P (reduced) -> trace slot of the current sweep (trp[sweep][mode][kmax^2])
+void launch_store_p(const double* ppart, int nslots, int K, int order, int mode, int kmax, uint64_t max_sweeps,
+                    double* trp, const DevStatus* st, cudaStream_t s);
+// objective / fit / stop rule at the end of a sweep
+void launch_sweep_end(const double* core, uint64_t core_size, double dns, double tol, uint64_t max_sweeps,
+                      const SweepTrace& tr, DevStatus* st, cudaStream_t s);
+// drifts of `pairs` (sweep, mode) trace slots; ranks: device array of the N ranks
+void launch_drift_batch(const double* trp, int pairs, int order, const int* ranks_dev, int kmax, double* drift,
+                        cudaStream_t s);
 // Householder QR following dense_core.cpp:127-198 exactly (single CTA), with
 // the seeded rank-deficiency fill generated on the device (MT19937-64 +
 // Box-Muller, rng.hpp:13-35, seed 0x48514F5251).

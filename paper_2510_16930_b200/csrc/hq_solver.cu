@@ -22,6 +22,9 @@
 // runs instead of gram2..apply only when chol1/chol2 flag it on the device.
 // A whole sweep is captured once per factor-buffer parity as a CUDA graph.
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <map>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -153,6 +156,9 @@ struct Solver {
     cudaEvent_t ev_fork[kMaxOrder] = {nullptr};
     cudaEvent_t ev_join = nullptr;
     DBuf<double> tr_obj, tr_fit, tr_drift, fit_prev;
+    DBuf<double> tr_p;      // P = U_new^T U_old per (sweep, mode): drifts evaluated at download
+    DBuf<int> dranks;
+    int kmax_ = 1;
     // multi-GPU: this rank owns rows [bnd[n][rank], bnd[n][rank+1]) of every mode n
     const Comm* comm = nullptr;
     std::vector<uint64_t> bnd[kMaxOrder];
@@ -166,6 +172,16 @@ struct Solver {
     uint64_t launched = 0;
     std::vector<cudaEvent_t> ev;  // ev[0] start, ev[i] after sweep i
     QrWork qw;
+    // opt-in step profiler (HQ_PROFILE_SWEEP=1): events after every launch of one eager sweep
+    bool prof = false;
+    std::vector<std::pair<std::string, cudaEvent_t>> prof_ev;
+    void mark(const char* what) {
+        if (!prof) return;
+        cudaEvent_t e;
+        HQ_CUDA(cudaEventCreate(&e));
+        HQ_CUDA(cudaEventRecord(e, s));
+        prof_ev.emplace_back(what, e);
+    }
 
     ~Solver() {
         for (auto& g : graph)
@@ -258,6 +274,10 @@ struct Solver {
         tr_obj.alloc(cfg.max_sweeps);
         tr_fit.alloc(cfg.max_sweeps);
         tr_drift.alloc(cfg.max_sweeps * N);
+        kmax_ = kmax;
+        tr_p.alloc((size_t)cfg.max_sweeps * N * kmax * kmax);
+        dranks.alloc(N);
+        HQ_CUDA(cudaMemcpyAsync(dranks.get(), ranks, sizeof(int) * N, cudaMemcpyHostToDevice, s));
         fit_prev.alloc(1);
         st.alloc(1);
         HQ_CUDA(cudaMemsetAsync(st.get(), 0, sizeof(DevStatus), s));
@@ -312,16 +332,20 @@ struct Solver {
         FactorPtrs f = factors_for_mode(n, p);
         DevStatus* S = st.get();
         launch_gt(core.get(), m, ranks, gt.get(), S, s);
+        mark("gt");
         launch_pass(*T, n, m, f, kTTMcTC, gt.get(), pass_out(A.get()), S, kAlways, s, r0, r1);
+        mark("pass");
         const int slots = pass_slots(T->modes[n], m);
         launch_reduce_pass(mpart.get(), m.kn * m.L, wpart.get(), K * K, maxpart.get(), slots, mred.get(), wred.get(),
                            maxv.get(), S, kAlways, s);
+        mark("reduce");
         if (comm) {  // M, W, max|A| over all ranks' rows
             comm->allreduce_sum(mred.get(), (size_t)m.kn * m.L, s);
             comm->allreduce_sum(wred.get(), (size_t)K * K, s);
             comm->allreduce_max(maxv.get(), 1, s);
         }
         launch_chol1(wred.get(), maxv.get(), K, r1inv.get(), S, n + 1, s, comm != nullptr);
+        mark("chol1");
         const double* a_loc = A.get() + r0 * K;
         double* unew = U[n][1 - p].get();
         const double* uold = U[n][p].get();
@@ -329,12 +353,16 @@ struct Solver {
         int pslots = dense_slots();
         if (!comm) {
             launch_gram2(a_loc, lrows, K, r1inv.get(), w2part.get(), S, s);
+            mark("gram2");
             launch_chol2(w2part.get(), dense_slots(), K, r1inv.get(), rinv.get(), mred.get(), &m, core.get(), S, s);
+            mark("chol2");
             launch_apply(a_loc, lrows, K, rinv.get(), unew, uold, pp, true, S, kOnlyCholQR, s);
+            mark("apply");
             // Householder branch (device flag)
             launch_householder(A.get(), dims[n], K, unew, hh.get(), S, kOnlyFallback, s);
             launch_apply(nullptr, dims[n], K, nullptr, unew, uold, pp, false, S, kOnlyFallback, s);
             compute_core(p, kOnlyFallback, n);
+            mark("fallback(no-op)");
         } else {
             launch_gram2(a_loc, lrows, K, r1inv.get(), w2part.get(), S, s);
             launch_reduce_pass(nullptr, 0, w2part.get(), K * K, nullptr, dense_slots(), nullptr, w2red.get(), nullptr, S,
@@ -351,18 +379,17 @@ struct Solver {
             pp = ppart[n].get();
             pslots = 1;
         }
-        SweepTrace tr{tr_obj.get(), tr_fit.get(), tr_drift.get(), fit_prev.get()};
-        if (n < N - 1) {
-            // the drift feeds only the trace: run it beside the next mode update
-            HQ_CUDA(cudaEventRecord(ev_fork[n], s));
-            HQ_CUDA(cudaStreamWaitEvent(side, ev_fork[n], 0));
-            launch_drift(pp, pslots, K, core.get(), core_size, dns, N, n, false, cfg.tol_fit_change, cfg.max_sweeps,
-                         tr, S, side);
-        } else {
+        // the drift feeds only the trace: P is stored beside the next mode update (side stream) and the
+        // drifts are evaluated in one batch at download
+        HQ_CUDA(cudaEventRecord(ev_fork[n], s));
+        HQ_CUDA(cudaStreamWaitEvent(side, ev_fork[n], 0));
+        launch_store_p(pp, pslots, K, N, n, kmax_, cfg.max_sweeps, tr_p.get(), S, side);
+        if (n == N - 1) {
             HQ_CUDA(cudaEventRecord(ev_join, side));
             HQ_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
-            launch_drift(pp, pslots, K, core.get(), core_size, dns, N, n, true, cfg.tol_fit_change, cfg.max_sweeps,
-                         tr, S, s);
+            SweepTrace tr{tr_obj.get(), tr_fit.get(), tr_drift.get(), fit_prev.get()};
+            launch_sweep_end(core.get(), core_size, dns, cfg.tol_fit_change, cfg.max_sweeps, tr, S, s);
+            mark("sweep_end");
         }
     }
 
@@ -389,7 +416,34 @@ struct Solver {
         }
     }
 
+    void profile_one_sweep() {
+        prof = true;
+        mark("start");
+        issue_sweep(host_parity);
+        host_parity ^= 1;
+        ++launched;
+        HQ_CUDA(cudaStreamSynchronize(s));
+        prof = false;
+        std::map<std::string, double> tot;
+        for (size_t i = 1; i < prof_ev.size(); ++i) {
+            float ms = 0.f;
+            HQ_CUDA(cudaEventElapsedTime(&ms, prof_ev[i - 1].second, prof_ev[i].second));
+            tot[prof_ev[i].first] += ms * 1e3;
+        }
+        double all = 0.0;
+        for (auto& kv : tot) all += kv.second;
+        std::fprintf(stderr, "[hq] sweep profile (us, warm, eager):");
+        for (auto& kv : tot) std::fprintf(stderr, " %s=%.1f", kv.first.c_str(), kv.second);
+        std::fprintf(stderr, " total=%.1f\n", all);
+        for (auto& pe : prof_ev) cudaEventDestroy(pe.second);
+        prof_ev.clear();
+    }
+
     void run(uint64_t sweeps) {
+        if (!graph[0] && std::getenv("HQ_PROFILE_SWEEP") && sweeps > 1) {
+            profile_one_sweep();
+            --sweeps;
+        }
         if (!graph[0]) {
             // first sweep eagerly (sets kernel attributes), then capture
             ensure_events();
@@ -468,8 +522,10 @@ struct Solver {
                 if (tr->objective)
                     HQ_CUDA(cudaMemcpyAsync(tr->objective, tr_obj.get(), 8 * h.sweep, cudaMemcpyDeviceToHost, s));
                 if (tr->fit) HQ_CUDA(cudaMemcpyAsync(tr->fit, tr_fit.get(), 8 * h.sweep, cudaMemcpyDeviceToHost, s));
-                if (tr->drift)
+                if (tr->drift) {
+                    launch_drift_batch(tr_p.get(), h.sweep * N, N, dranks.get(), kmax_, tr_drift.get(), s);
                     HQ_CUDA(cudaMemcpyAsync(tr->drift, tr_drift.get(), 8 * h.sweep * N, cudaMemcpyDeviceToHost, s));
+                }
             }
             HQ_CUDA(cudaStreamSynchronize(s));
             if (tr->elapsed_s && !ev.empty()) {

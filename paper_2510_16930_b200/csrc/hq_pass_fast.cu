@@ -30,6 +30,7 @@
 // Deterministic: fixed row->lane assignment per tile, fixed tile->CTA
 // assignment, per-CTA partial slots reduced in fixed order.
 #include <algorithm>
+#include <cstdlib>
 
 #include "hq_fast.cuh"
 
@@ -535,19 +536,385 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
     }
 }
 
+
+// ============================================================================
+// Warp-specialised variant: one producer warp (row meta, records, factor-row
+// gathers with cp.async) and four consumer warps (Kronecker rows, GEMMs).  The
+// single gather buffer is handed over with named barriers: FULL (producer ->
+// consumers: a round of gathered rows is in shared memory) and FREE
+// (consumers -> producer: the Kronecker phase is done with it).  The producer
+// therefore fills tile t+1 while the consumers run tile t's GEMMs, and the
+// LSU-bound gather issue never stalls the arithmetic warps.
+__device__ __forceinline__ void bar_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_arrive_n(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void mbar_init_cta(uint64_t* mbar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(mbar)), "r"(count) : "memory");
+}
+// arrives on mbar once all of this thread's earlier cp.async have landed
+__device__ __forceinline__ void cp_async_arrive(uint64_t* mbar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(mbar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* mbar, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(mbar)),
+        "r"(parity)
+        : "memory");
+}
+
+template <int KA, int KB, int KN>
+struct WsCfg {
+    using C = Cfg<KA, KB, KN>;
+    static constexpr int CTHREADS = C::THREADS;         // consumers
+    static constexpr int THREADS = C::THREADS + 32;      // + producer warp
+    static constexpr int XOFF = KA + KB;                 // x is staged after the two factor rows
+    static_assert(C::FW >= KA + KB + 1, "room for x in the gather slot");
+    static constexpr int BAR_FULL = 1, BAR_FREE = 2, BAR_C = 3;
+    static constexpr size_t smem_bytes = (size_t)C::CAP * C::FW * 8 + (size_t)C::R * C::LDY * 8 +
+                                         (size_t)C::CAP * 8 + (size_t)C::R * C::ALD * 8 + 3 * C::META + 64;
+};
+
+template <int KA, int KB, int KN>
+__global__ void __launch_bounds__(WsCfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MINB)
+    k_pass_ws3(FastArgs a) {
+    using C = Cfg<KA, KB, KN>;
+    using W = WsCfg<KA, KB, KN>;
+    if (skip_kernel(a.st, a.run_if)) return;
+    extern __shared__ __align__(16) double sm[];
+    double* sF = sm;                                                    // CAP x FW: rows + x
+    double* sY = sF + (size_t)C::CAP * C::FW;                           // R x LDY
+    uint2* sJK = reinterpret_cast<uint2*>(sY + (size_t)C::R * C::LDY);  // CAP (j, k)
+    double* sA = reinterpret_cast<double*>(sJK + C::CAP);               // R x ALD
+    char* sMetaB = reinterpret_cast<char*>(sA + (size_t)C::R * C::ALD);
+    auto m_start = [&](int mb) { return reinterpret_cast<int64_t*>(sMetaB + mb * C::META); };
+    auto m_len = [&](int mb) { return reinterpret_cast<int*>(sMetaB + mb * C::META + 8 * C::R); };
+    auto m_off = [&](int mb) { return m_len(mb) + C::R; };
+    auto m_perm = [&](int mb) { return m_len(mb) + 2 * C::R; };
+    auto m_tot = [&](int mb) { return m_len(mb) + 3 * C::R; };
+    __shared__ double red[C::WARPS];
+    __shared__ __align__(8) uint64_t full_mbar;  // "a round of gathered rows has landed"
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool producer = warp == C::WARPS;
+    if (tid == 0) mbar_init_cta(&full_mbar, 32);  // one cp.async arrival per producer lane
+    __syncthreads();
+
+    // ---- tile range of this CTA (nnz-balanced, static)
+    const int G = gridDim.x, c = blockIdx.x;
+    const int64_t ntiles = (int64_t)((a.rows + C::R - 1) / C::R);
+    const uint64_t rend = a.rbase + a.rows;
+    const int64_t zb = a.rowptr[a.rbase];
+    const int64_t Z = a.rowptr[rend] - zb;
+    auto lower = [&](int64_t z) {
+        int64_t lo = 0, hi = ntiles;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            uint64_t r = a.rbase + min((uint64_t)mid * C::R, a.rows);
+            if (a.rowptr[r] - zb >= z) hi = mid; else lo = mid + 1;
+        }
+        return lo;
+    };
+    const int64_t t0 = lower((Z * c) / G);
+    const int64_t t1 = (c == G - 1) ? ntiles : lower((Z * (c + 1)) / G);
+    auto rounds_of = [&](int total) { return total > 0 ? (total + C::CAP - 1) / C::CAP : 1; };
+
+    if (producer) {
+        // ================================ producer warp
+        const uint64_t pol_stream = policy_evict_first();
+        const uint64_t pol_f = policy_evict_last();
+        constexpr int PA = KA / 2, PP = (KA + KB) / 2;
+        // row meta of tile t (lane r owns row r of the tile), warp-synchronous
+        auto meta = [&](int64_t t, int mb) {
+            const uint64_t r0 = a.rbase + (uint64_t)t * C::R;
+            const int nr = (int)min((uint64_t)C::R, rend - r0);
+            for (int r = lane; r < C::R; r += 32) {
+                int len = 0;
+                int64_t st = 0;
+                if (r < nr) {
+                    st = a.rowptr[r0 + r];
+                    const int64_t l = a.rowptr[r0 + r + 1] - st;
+                    len = (l > kShortMax) ? -1 : (int)l;
+                }
+                m_len(mb)[r] = len;
+                m_start(mb)[r] = st;
+            }
+            __syncwarp();
+            const int* ln = m_len(mb);
+            for (int r = lane; r < C::R; r += 32) {
+                const int me = max(ln[r], 0);
+                int rank = 0, off = 0;
+                for (int q = 0; q < C::R; ++q) {
+                    const int o = max(ln[q], 0);
+                    rank += (o > me) || (o == me && q < r);
+                    off += (q < r) ? o : 0;
+                }
+                m_perm(mb)[rank] = r;
+                m_off(mb)[r] = off;
+                if (r == C::R - 1) m_tot(mb)[0] = off + me;
+            }
+            __syncwarp();
+        };
+        // (j, k) of virtual records [cv, cv + CAP) of a tile -> sJK (lane per row)
+        auto records = [&](int mb, int cv) {
+            for (int r = lane; r < C::R; r += 32) {
+                const int len = max(m_len(mb)[r], 0), off = m_off(mb)[r];
+                const int64_t pbase = m_start(mb)[r] - off;
+                const int lo = max(off, cv), hi = min(off + len, cv + C::CAP);
+                for (int v = lo; v < hi; ++v) {
+                    cp4(&sJK[v - cv].x, a.ia + pbase + v, pol_stream);
+                    cp4(&sJK[v - cv].y, a.ib + pbase + v, pol_stream);
+                }
+            }
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+        };
+        // factor rows + x of virtual records [cv, cv + cn) -> sF; completion arrives on full_mbar
+        auto gathers = [&](int mb, int cv, int cn) {
+            cp_wait_all();  // (j, k) staged (earlier gathers landed long ago: the consumers freed sF)
+            __syncwarp();
+            for (int q = lane; q < cn * PP; q += 32) {
+                const int e = q / PP, pc = q - e * PP;
+                const uint2 jk = sJK[e];
+                const double* src = (pc < PA) ? a.ua + (size_t)jk.x * KA + 2 * pc : a.ub + (size_t)jk.y * KB + 2 * (pc - PA);
+                cp16(sF + (size_t)e * C::FW + ((pc < PA) ? 2 * pc : KA + 2 * (pc - PA)), src, pol_f);
+            }
+            for (int r = lane; r < C::R; r += 32) {  // x, straight from the value stream
+                const int len = max(m_len(mb)[r], 0), off = m_off(mb)[r];
+                const int64_t pbase = m_start(mb)[r] - off;
+                const int lo = max(off, cv), hi = min(off + len, cv + cn);
+                for (int v = lo; v < hi; ++v) cp8(sF + (size_t)(v - cv) * C::FW + W::XOFF, a.val + pbase + v, pol_stream);
+            }
+            cp_async_arrive(&full_mbar);
+        };
+        if (t0 < t1) {
+            meta(t0, 0);
+            records(0, 0);
+        }
+        bool first = true;
+        for (int64_t t = t0; t < t1; ++t) {
+            const int mb = (int)((t - t0) % 3);
+            const int total = m_tot(mb)[0];
+            const int rounds = rounds_of(total);
+            for (int rd = 0; rd < rounds; ++rd) {
+                const int cv = rd * C::CAP, cn = max(0, min(C::CAP, total - cv));
+                if (!first) bar_sync_n(W::BAR_FREE, W::THREADS);
+                first = false;
+                if (rd > 0) records(mb, cv);
+                gathers(mb, cv, cn);
+                if (rd == rounds - 1 && t + 1 < t1) {  // next tile's meta and records while the consumers work
+                    meta(t + 1, (mb + 1) % 3);
+                    records((mb + 1) % 3, 0);
+                }
+            }
+        }
+        if (!first) bar_sync_n(W::BAR_FREE, W::THREADS);  // the consumers' last FREE
+        return;
+    }
+
+    // ================================ consumer warps (C::THREADS threads)
+    for (int q = tid; q < C::R * C::ALD; q += C::THREADS) sA[q] = 0.0;
+    double macc[C::MBW][2];
+#pragma unroll
+    for (int b = 0; b < C::MBW; ++b) macc[b][0] = macc[b][1] = 0.0;
+    double wacc[C::WQ];
+#pragma unroll
+    for (int b = 0; b < C::WQ; ++b) wacc[b] = 0.0;
+    double mx = 0.0;
+    const double* __restrict__ gt = a.gt;
+    static_assert(C::WARPS % C::NT == 0, "warp -> n-tile mapping");
+    constexpr bool kGReg = C::L / 4 <= 32;
+    double gfr[kGReg ? C::L / 4 : 1];
+    const int gcolidx = (warp % C::NT) * 8 + (lane >> 2);
+    const bool gvalid = a.kind == kTTMcTC && gcolidx < KN;
+    if constexpr (kGReg) {
+#pragma unroll
+        for (int ks = 0; ks < C::L / 4; ++ks)
+            gfr[ks] = gvalid ? __ldg(gt + (size_t)(ks * 4 + (lane & 3)) * KN + gcolidx) : 0.0;
+    }
+    const int rslot = warp * C::RPW + lane / C::TR;
+    const int pb = (lane % C::TR) / C::TQ, qb = lane % C::TQ;
+    const int p0 = pb * C::BP, q0 = qb * C::BQ;
+    uint32_t full_phase = 0;
+
+    for (int64_t t = t0; t < t1; ++t) {
+        const int mb = (int)((t - t0) % 3);
+        const uint64_t r0 = a.rbase + (uint64_t)t * C::R;
+        const int nr = (int)min((uint64_t)C::R, rend - r0);
+        double acc[C::BP][C::BQ];
+#pragma unroll
+        for (int p = 0; p < C::BP; ++p)
+#pragma unroll
+            for (int q = 0; q < C::BQ; ++q) acc[p][q] = 0.0;
+        int total = 0, lr = 0, len = 0, voff = 0;
+        for (int rd = 0;; ++rd) {
+            mbar_wait_parity(&full_mbar, full_phase);
+            full_phase ^= 1;
+            if (rd == 0) {
+                total = m_tot(mb)[0];
+                lr = m_perm(mb)[rslot];
+                len = max(m_len(mb)[lr], 0);
+                voff = m_off(mb)[lr];
+            }
+            const int cv = rd * C::CAP;
+            const int e0 = max(voff, cv) - cv, e1 = min(voff + len, cv + C::CAP) - cv;
+#pragma unroll 2
+            for (int e = e0; e < e1; ++e) {
+                const double* f = sF + (size_t)e * C::FW;
+                const double x = f[W::XOFF];
+                double sa[C::BP], vb[C::BQ];
+                lds_block<C::BP>(f, p0, sa);
+                lds_block<C::BQ>(f + KA, q0, vb);
+#pragma unroll
+                for (int p = 0; p < C::BP; ++p) {
+                    const double sx = x * sa[p];
+#pragma unroll
+                    for (int q = 0; q < C::BQ; ++q) acc[p][q] = fma(sx, vb[q], acc[p][q]);
+                }
+            }
+            bar_arrive_n(W::BAR_FREE, W::THREADS);
+            if (rd + 1 >= rounds_of(total)) break;
+        }
+        {
+            double* y = sY + (size_t)lr * C::LDY;
+#pragma unroll
+            for (int p = 0; p < C::BP; ++p)
+#pragma unroll
+                for (int q = 0; q < C::BQ; ++q) y[blk_index<C::BP>(p0, p) * KB + blk_index<C::BQ>(q0, q)] = acc[p][q];
+            if (C::LP > C::L && pb == 0 && qb == 0)
+                for (int l = C::L; l < C::LP; ++l) y[l] = 0.0;
+        }
+        bar_sync_n(W::BAR_C, W::CTHREADS);
+        const int* ln = m_len(mb);
+        if (a.kind == kTTMcTC) {
+            const int nt = warp % C::NT;
+            constexpr int KSN = C::L / 4;
+            double cc[C::ABW][2][2];
+#pragma unroll
+            for (int bi = 0; bi < C::ABW; ++bi) cc[bi][0][0] = cc[bi][0][1] = cc[bi][1][0] = cc[bi][1][1] = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < KSN; ++ks)
+#pragma unroll
+                for (int bi = 0; bi < C::ABW; ++bi) {
+                    const int b = warp + bi * C::WARPS;
+                    if (b < C::AB) {
+                        const int mt = b / C::NT;
+                        const double yv = sY[(size_t)(mt * 8 + (lane >> 2)) * C::LDY + (lane & 3) + ks * 4];
+                        double gv;
+                        if constexpr (kGReg)
+                            gv = gfr[ks];
+                        else
+                            gv = gvalid ? __ldg(gt + (size_t)(ks * 4 + (lane & 3)) * KN + gcolidx) : 0.0;
+                        dmma884(cc[bi][ks & 1][0], cc[bi][ks & 1][1], yv, gv);
+                    }
+                }
+#pragma unroll
+            for (int bi = 0; bi < C::ABW; ++bi) {
+                const int b = warp + bi * C::WARPS;
+                if (b < C::AB) {
+                    const int mt = b / C::NT;
+                    const int row = mt * 8 + (lane >> 2);
+                    const int col = nt * 8 + 2 * (lane & 3);
+                    sA[row * C::ALD + col] = cc[bi][0][0] + cc[bi][1][0];
+                    sA[row * C::ALD + col + 1] = cc[bi][0][1] + cc[bi][1][1];
+                }
+            }
+        } else {
+            for (int q = tid; q < C::R * KN; q += C::THREADS) {
+                const int row = q / KN, r = q - row * KN;
+                sA[row * C::ALD + r] = (row < nr && ln[row] >= 0) ? a.un[(r0 + row) * KN + r] : 0.0;
+            }
+        }
+        bar_sync_n(W::BAR_C, W::CTHREADS);
+        for (int q = tid; q < C::R * KN; q += C::THREADS) {
+            const int row = q / KN, r = q - row * KN;
+            const double v = sA[row * C::ALD + r];
+            if (row < nr && ln[row] >= 0) {
+                if (a.A) a.A[(r0 + row) * KN + r] = v;
+                mx = fmax(mx, fabs(v));
+            } else {
+                sA[row * C::ALD + r] = 0.0;
+            }
+        }
+        bar_sync_n(W::BAR_C, W::CTHREADS);
+#pragma unroll
+        for (int ks = 0; ks < C::R / 4; ++ks)
+#pragma unroll
+            for (int bi = 0; bi < C::MBW; ++bi) {
+                const int b = warp + bi * C::WARPS;
+                if (b < C::MB) {
+                    const int mt = b / C::NLT, nt = b - mt * C::NLT;
+                    const double av = sA[(size_t)(ks * 4 + (lane & 3)) * C::ALD + mt * 8 + (lane >> 2)];
+                    const double yv = sY[(size_t)(ks * 4 + (lane & 3)) * C::LDY + nt * 8 + (lane >> 2)];
+                    dmma884(macc[bi][0], macc[bi][1], av, yv);
+                }
+            }
+#pragma unroll
+        for (int wi = 0; wi < C::WQ; ++wi) {
+            const int q = tid + wi * C::THREADS;
+            if (q < KN * KN) {
+                const int r1 = q / KN, r2 = q - r1 * KN;
+                double sacc = wacc[wi];
+                for (int row = 0; row < C::R; ++row) sacc = fma(sA[row * C::ALD + r1], sA[row * C::ALD + r2], sacc);
+                wacc[wi] = sacc;
+            }
+        }
+        bar_sync_n(W::BAR_C, W::CTHREADS);
+    }
+
+    const int slot = a.slot0 + c;
+    double* mp = a.mpart + (size_t)slot * KN * C::L;
+#pragma unroll
+    for (int bi = 0; bi < C::MBW; ++bi) {
+        const int b = warp + bi * C::WARPS;
+        if (b < C::MB) {
+            const int mt = b / C::NLT, nt = b - mt * C::NLT;
+            const int r = mt * 8 + (lane >> 2);
+            const int l = nt * 8 + 2 * (lane & 3);
+            if (r < KN) {
+                if (l < C::L) mp[(size_t)r * C::L + l] = macc[bi][0];
+                if (l + 1 < C::L) mp[(size_t)r * C::L + l + 1] = macc[bi][1];
+            }
+        }
+    }
+#pragma unroll
+    for (int wi = 0; wi < C::WQ; ++wi) {
+        const int q = tid + wi * C::THREADS;
+        if (q < KN * KN) a.wpart[(size_t)slot * KN * KN + q] = wacc[wi];
+    }
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+    if (lane == 0) red[warp] = mx;
+    bar_sync_n(W::BAR_C, W::CTHREADS);
+    if (tid == 0) {
+        double m = 0.0;
+        for (int w = 0; w < C::WARPS; ++w) m = fmax(m, red[w]);
+        a.maxpart[slot] = m;
+    }
+}
+
 template <int KA, int KB, int KN>
 void launch_fast3(const FastArgs& a, int grid, cudaStream_t s) {
     using C = Cfg<KA, KB, KN>;
-    auto fn = k_pass_fast3<KA, KB, KN>;
+    using W = WsCfg<KA, KB, KN>;
+    // default: the software-pipelined kernel; HQ_PASS_WS=1 selects the warp-specialised variant
+    // (producer warp + 4 consumer warps; measured slower on B200 so far: 1.01 vs 0.84 ms per config-2 pass)
+    static const bool v3 = [] {
+        const char* e = std::getenv("HQ_PASS_WS");
+        return !(e && e[0] == '1');
+    }();
+    auto fn = v3 ? k_pass_fast3<KA, KB, KN> : k_pass_ws3<KA, KB, KN>;
+    const size_t smem = v3 ? C::smem_bytes : W::smem_bytes;
     static bool attr = false;
     if (!attr) {
-        HQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes));
+        HQ_CUDA(cudaFuncSetAttribute(k_pass_fast3<KA, KB, KN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)C::smem_bytes));
+        HQ_CUDA(cudaFuncSetAttribute(k_pass_ws3<KA, KB, KN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)W::smem_bytes));
         attr = true;
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(C::THREADS);
-    cfg.dynamicSmemBytes = C::smem_bytes;
+    cfg.blockDim = dim3(v3 ? C::THREADS : W::THREADS);
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr_l2[1];
     if (a.l2_bytes) {

@@ -35,7 +35,7 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 CONFIG_ID = 2
 SEED_INIT = 20251016
-METRIC = "HOQRI iter/s (FP64) — BASELINE config 2"
+METRIC = "HOQRI iter/s (FP64) — BASELINE config {cfg}"
 
 
 def parse():
@@ -208,7 +208,7 @@ def run_reference(args, ws, rank):
     sweep_s = statistics.median(r["sweep_s"] for r in res)
     value = 1.0 / sweep_s
     model, ncpu = host_desc()
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": ws,
+    line = {"impl": "reference", "metric": METRIC.format(cfg=args.config), "value": value, "unit": "iter/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": sweep_s * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (BASELINE config %d, seeded PCG64)" % args.config,
@@ -321,7 +321,7 @@ def run_engine(args, ws, rank, local):
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tr_path):
         try:
-            traffic = json.load(open(tr_path)).get("mode_pass_dram_bytes")
+            traffic = json.load(open(tr_path)).get("configs", {}).get(str(args.config), {}).get("mode_pass_dram_bytes")
         except Exception:
             traffic = None
 
@@ -374,7 +374,7 @@ def run_engine(args, ws, rank, local):
         return
     model, ncpu = host_desc()
     line = {
-        "metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": ws, "steps": K, "warmup": W,
+        "metric": METRIC.format(cfg=args.config), "value": value, "unit": "iter/s", "n_gpus": ws, "steps": K, "warmup": W,
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (BASELINE config %d: uniform int32 coords, U(0,1) values, seeded PCG64; duplicates "
                 "merged on device)" % args.config,
@@ -387,7 +387,7 @@ def run_engine(args, ws, rank, local):
                    "note": "fused mode pass (TTMcTC + Gram + core projection) per launch, mean over modes"},
         "roofline": {"bound": "tensor", "achieved": tflops, "peak": peak64, "unit": "TFLOP/s",
                      "frac": tflops / peak64, "traffic": traffic,
-                     "kernel": "fused sparse mode pass (hq_pass: k_pass_tiles*)",
+                     "kernel": "fused sparse mode pass (hq_pass: short-row tiles + long-row segment/fix-up kernels)",
                      "flops_per_launch": avg_flops, "bytes_per_launch": avg_bytes, "launch_ms": avg_pass_ms,
                      "per_mode_ms": pass_ms,
                      "hbm": {"achieved_gbs": avg_bytes / (avg_pass_ms * 1e-3) / 1e9, "peak_gbs": peaks.get("hbm_gbs"),

@@ -19,6 +19,7 @@
 #include <cstdlib>
 
 #include "hq_fast.cuh"
+#include "hq_long.cuh"
 #include "hq_plan.cuh"
 
 namespace hq {
@@ -444,7 +445,37 @@ void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const Fac
         k_pass_tiles_generic<<<short_grid(), kGenericThreads, smem, s>>>(a);
         HQ_CHECK_LAUNCH();
     }
-    if (L.long_rows) {
+    if (L.long_rows && long_fast_supported(sh) && !force_generic()) {
+        LongArgs la{};
+        la.rbase = a.rbase;
+        la.rows = a.rows;
+        la.rowptr = a.rowptr;
+        la.val = a.val;
+        la.i0 = a.idx[0];
+        la.i1 = a.idx[1];
+        la.i2 = sh.nothers > 2 ? a.idx[2] : nullptr;
+        la.u0 = a.uo[0];
+        la.u1 = a.uo[1];
+        la.u2 = sh.nothers > 2 ? a.uo[2] : nullptr;
+        la.un = a.un;
+        la.gt = gt;
+        la.long_ids = a.long_ids;
+        la.long_segptr = a.long_segptr;
+        la.seg_begin = a.seg_begin;
+        la.seg_row = a.seg_row;
+        la.nlong = a.nlong;
+        la.nseg = a.nseg;
+        la.ypart = out.ypart;
+        la.A = out.A;
+        la.mpart = out.mpart;
+        la.wpart = out.wpart;
+        la.maxpart = out.maxpart;
+        la.kind = kind;
+        la.slot0 = tile_grid(sh);
+        la.st = st;
+        la.run_if = run_if;
+        launch_long_fast(la, sh, long_grid(L), s);
+    } else if (L.long_rows) {
         int segs = (int)std::min<uint64_t>(L.long_segments, (uint64_t)num_sms() * 8);
         k_pass_longseg_generic<<<segs, kGenericThreads, 0, s>>>(a);
         HQ_CHECK_LAUNCH();

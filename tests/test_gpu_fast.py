@@ -67,3 +67,56 @@ def test_fast_and_generic_agree(k, request):
     assert rel <= 1e-10
     np.testing.assert_allclose([s.objective for s in rf.trace.sweeps], [s.objective for s in rg.trace.sweeps],
                                rtol=1e-10)
+
+
+def _long_case(order, k, seed):
+    """Every row of mode 0 long, lengths straddling kShortMax (256), the
+    128-nonzero staging chunk and kSegLen (4096) boundaries; at order 4 all
+    modes are long (config 5's regime)."""
+    rng = np.random.default_rng(seed)
+    if order == 3:
+        dims = [24, 1800, 1500]
+        lens = [257, 300, 383, 384, 385, 511, 4095, 4096, 4097, 4224, 8192, 8193, 9000, 1000, 600, 700,
+                257, 2000, 3000, 129, 128, 5, 0, 12000]
+    else:
+        dims = [20, 160, 140, 120]
+        lens = [4097, 3000, 5000, 4096, 257, 9000, 2500, 2600, 2700, 2800, 3100, 3200, 3300, 3400, 3500,
+                3600, 3700, 3800, 3900, 4000]
+    rows = np.repeat(np.arange(len(lens), dtype=np.uint32), lens)
+    coords = np.empty((rows.size, order), np.uint32)
+    coords[:, 0] = rows
+    for m in range(1, order):
+        coords[:, m] = rng.integers(0, dims[m], rows.size, dtype=np.uint32)
+    vals = rng.standard_normal(rows.size)
+    x = hq.SparseTensor(dims, coords, vals)
+    u = hq.random_factors(dims, [k] * order, seed + 1)
+    return dims, x, u
+
+
+@pytest.mark.parametrize("order,k", [(3, 10), (3, 16), (3, 8), (4, 8)])
+def test_long_rows_fast_matches_oracle_and_generic(order, k):
+    from oracle_bind import Oracle
+    o = Oracle()
+    dims, x, u = _long_case(order, k, 71 + k + order)
+    ranks = [k] * order
+    core = hq.ttmc_core(x, u)
+    oc = o.ttmc_core(dims, ranks, x.coords(), x.values(), u.factors).reshape(-1)
+    assert np.abs(core.data - oc).max() <= 1e-11 * max(1.0, np.abs(oc).max())
+    fast = []
+    for m in range(order):
+        a = hq.ttmctc_elementwise(x, u, m, core)
+        ao = o.ttmctc(dims, ranks, x.coords(), x.values(), u.factors, m, core.data)
+        assert np.abs(a - ao).max() <= 1e-11 * max(1.0, np.abs(ao).max()), (order, k, m)
+        assert (a == hq.ttmctc_elementwise(x, u, m, core)).all()  # bitwise repeatable
+        fast.append(a)
+    cfg = hq.SolverConfig(ranks=ranks, max_sweeps=3, tol_fit_change=0.0)
+    rf = hq.hoqri(x, cfg, init_factors=u.factors)
+    ref = o.hoqri(dims, ranks, x.coords(), x.values(), u.factors, 3)
+    np.testing.assert_allclose([s.objective for s in rf.trace.sweeps], ref["objective"], rtol=1e-9)
+    os.environ["HQ_FORCE_GENERIC"] = "1"
+    try:
+        gen = [hq.ttmctc_elementwise(x, u, m, core) for m in range(order)]
+    finally:
+        os.environ.pop("HQ_FORCE_GENERIC", None)
+    for a, b in zip(fast, gen):
+        assert np.abs(a - b).max() <= 1e-12 * np.abs(b).max()

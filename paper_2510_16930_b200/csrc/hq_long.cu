@@ -45,6 +45,7 @@ __device__ __forceinline__ void cpa_wait() {
 // shape of the Kronecker row: other-mode ranks K0, K1, (K2 = 0 at order 3)
 template <int K0, int K1, int K2>
 struct LS_ {
+    static constexpr int NO = K2 ? 3 : 2;           // other modes
     static constexpr int LS = K2 ? K0 * K1 : K0;  // S width
     static constexpr int KL = K2 ? K2 : K1;       // V width (last other mode)
     static constexpr int L = LS * KL;
@@ -53,119 +54,176 @@ struct LS_ {
     // + x; row stride = 4 mod 8 doubles: the 4 nonzeros of a k-step land on disjoint banks
     static constexpr int FW = (RW + 4) / 8 * 8 + 4;
     static constexpr int CH = 128;                  // nonzeros per chunk
-    static constexpr int WARPS = 4, THREADS = 128;
-    static constexpr size_t smem = 2 * (size_t)CH * FW * 8 + (size_t)WARPS * MT * NTL * 64 * 8;
+    static constexpr int WARPS = 8, THREADS = 256;
+    static constexpr int PP = RW / 2;               // 16-byte pieces per nonzero
+    static constexpr size_t row_doubles = (size_t)CH * FW;           // one gathered-row buffer
+    static constexpr size_t red_doubles = (size_t)WARPS * MT * NTL * 64;
+    static constexpr size_t rec_words = (size_t)NO * CH;             // one index-record buffer
+    static constexpr size_t smem = (2 * row_doubles + red_doubles) * 8 + 3 * rec_words * 4;
     static_assert(K0 % 2 == 0 && K1 % 2 == 0 && K2 % 2 == 0, "16-byte factor rows");
 };
 
+// Walks a CTA's chunks: segments [sg, se) of the rank's rows, each cut into
+// CH-nonzero chunks (a chunk never straddles two segments).
+struct ChunkCursor {
+    uint64_t sg, se;
+    int64_t z0, zend;
+    __device__ bool valid() const { return sg < se; }
+    __device__ void seek(const LongArgs& a, uint64_t rend) {  // first in-range segment at or after sg
+        for (; sg < se; ++sg) {
+            const uint32_t row = a.long_ids[a.seg_row[sg]];
+            if (row < a.rbase || row >= rend) continue;  // another rank's row
+            z0 = a.seg_begin[sg];
+            zend = min(z0 + (int64_t)kSegLen, a.rowptr[row + 1]);
+            return;
+        }
+    }
+    __device__ int n(int ch) const { return (int)min((int64_t)ch, zend - z0); }
+    __device__ bool last(int ch) const { return z0 + ch >= zend; }
+    __device__ void advance(const LongArgs& a, uint64_t rend, int ch) {
+        z0 += ch;
+        if (z0 >= zend) {
+            ++sg;
+            seek(a, rend);
+        }
+    }
+};
+
+// Three-stage pipeline per CTA over a flat chunk sequence:
+//   iteration c: index records of chunk c+2 (coalesced 4-byte cp.async),
+//                factor-row gathers of chunk c+1 (16-byte cp.async pieces,
+//                row indices read from the staged records), DMMA on chunk c.
+// Warps split a chunk's k-steps; at a segment's last chunk the eight warps'
+// fragments are summed in warp order into ypart[segment].
 template <int K0, int K1, int K2>
-__global__ void __launch_bounds__(128) k_longseg_mma(LongArgs a) {
+__global__ void __launch_bounds__(256) k_longseg_mma(LongArgs a) {
     using S = LS_<K0, K1, K2>;
     if (skip_kernel(a.st, a.run_if)) return;
     extern __shared__ __align__(16) double sm[];
-    double* red = sm + 2 * (size_t)S::CH * S::FW;
+    double* rowbuf = sm;                                   // [2][CH][FW]
+    double* red = sm + 2 * S::row_doubles;                 // [WARPS][MT*NTL][64]
+    uint32_t* rec = reinterpret_cast<uint32_t*>(red + S::red_doubles);  // [3][NO][CH]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gid = lane >> 2, tig = lane & 3;
     const uint64_t G = gridDim.x, c = blockIdx.x;
-    const uint64_t sb = a.nseg * c / G, se = a.nseg * (c + 1) / G;
     const uint64_t rend = a.rbase + a.rows;
-    constexpr int P0 = K0 / 2, P1 = K1 / 2, P2 = K2 / 2, PP = P0 + P1 + P2;
+    constexpr int P0 = K0 / 2, P1 = K1 / 2;
+    const uint32_t* idx[3] = {a.i0, a.i1, a.i2};
 
-    // stage nonzeros [z0, z0 + n) into buffer b: factor rows piece-major, then x
-    auto stage = [&](int b, int64_t z0, int n) {
-        double* dst = sm + (size_t)b * S::CH * S::FW;
-        for (int q = tid; q < n * PP; q += S::THREADS) {
-            const int e = q / PP, pc = q - e * PP;
-            const int64_t z = z0 + e;
-            const double* src;
-            int off;
-            if (pc < P0) {
-                src = a.u0 + (size_t)a.i0[z] * K0 + 2 * pc;
-                off = 2 * pc;
-            } else if (pc < P0 + P1) {
-                src = a.u1 + (size_t)a.i1[z] * K1 + 2 * (pc - P0);
-                off = K0 + 2 * (pc - P0);
-            } else {
-                src = a.u2 + (size_t)a.i2[z] * K2 + 2 * (pc - P0 - P1);
-                off = K0 + K1 + 2 * (pc - P0 - P1);
-            }
-            cpa16(dst + (size_t)e * S::FW + off, src);
+    ChunkCursor cr{a.nseg * c / G, a.nseg * (c + 1) / G, 0, 0};
+    cr.seek(a, rend);
+    ChunkCursor cg = cr, cc = cr;  // gathers / compute cursors trail the records cursor
+
+    auto issue_records = [&](int slot) {
+        if (cr.valid()) {
+            const int n = cr.n(S::CH);
+            uint32_t* r = rec + (size_t)slot * S::rec_words;
+#pragma unroll
+            for (int m = 0; m < S::NO; ++m)
+                for (int e = tid; e < n; e += S::THREADS) {
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr(r + m * S::CH + e)),
+                                 "l"(idx[m] + cr.z0 + e));
+                }
+            cr.advance(a, rend, S::CH);
         }
-        for (int e = tid; e < n; e += S::THREADS) cpa8(dst + (size_t)e * S::FW + S::RW, a.val + z0 + e);
+        cpa_commit();
+    };
+    auto issue_gathers = [&](int rslot, int bslot) {
+        if (cg.valid()) {
+            const int n = cg.n(S::CH);
+            const uint32_t* r = rec + (size_t)rslot * S::rec_words;
+            double* dst = rowbuf + (size_t)bslot * S::row_doubles;
+            for (int q = tid; q < n * S::PP; q += S::THREADS) {
+                const int e = q / S::PP, pc = q - e * S::PP;
+                const double* src;
+                int off;
+                if (pc < P0) {
+                    src = a.u0 + (size_t)r[e] * K0 + 2 * pc;
+                    off = 2 * pc;
+                } else if (pc < P0 + P1) {
+                    src = a.u1 + (size_t)r[S::CH + e] * K1 + 2 * (pc - P0);
+                    off = K0 + 2 * (pc - P0);
+                } else {
+                    src = a.u2 + (size_t)r[2 * S::CH + e] * K2 + 2 * (pc - P0 - P1);
+                    off = K0 + K1 + 2 * (pc - P0 - P1);
+                }
+                cpa16(dst + (size_t)e * S::FW + off, src);
+            }
+            for (int e = tid; e < n; e += S::THREADS) cpa8(dst + (size_t)e * S::FW + S::RW, a.val + cg.z0 + e);
+            cg.advance(a, rend, S::CH);
+        }
         cpa_commit();
     };
 
-    for (uint64_t sg = sb; sg < se; ++sg) {
-        const uint32_t row = a.long_ids[a.seg_row[sg]];
-        if (row < a.rbase || row >= rend) continue;  // another rank's row
-        const int64_t zs = a.seg_begin[sg];
-        const int64_t ze = min(zs + (int64_t)kSegLen, a.rowptr[row + 1]);
-        const int nch = (int)((ze - zs + S::CH - 1) / S::CH);
-        double acc[S::MT][S::NTL][2];
+    double acc[S::MT][S::NTL][2];
 #pragma unroll
-        for (int i = 0; i < S::MT; ++i)
+    for (int i = 0; i < S::MT; ++i)
 #pragma unroll
-            for (int j = 0; j < S::NTL; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-        __syncthreads();  // buffers free (previous segment done)
-        stage(0, zs, (int)min((int64_t)S::CH, ze - zs));
-        for (int ch = 0; ch < nch; ++ch) {
-            const int64_t z0 = zs + (int64_t)ch * S::CH;
-            const int n = (int)min((int64_t)S::CH, ze - z0);
-            if (ch + 1 < nch) {
-                stage((ch + 1) & 1, z0 + S::CH, (int)min((int64_t)S::CH, ze - z0 - S::CH));
-                cpa_wait<1>();
-            } else {
-                cpa_wait<0>();
-            }
-            __syncthreads();
-            const double* f = sm + (size_t)(ch & 1) * S::CH * S::FW;
-            const int ks_n = (n + 3) / 4;
-            for (int ks = warp; ks < ks_n; ks += S::WARPS) {
-                const int e = ks * 4 + tig;
-                const bool ev = e < n;
-                const double* fe = f + (size_t)e * S::FW;
-                const double x = ev ? fe[S::RW] : 0.0;
-                double bv[S::NTL];
-#pragma unroll
-                for (int nt = 0; nt < S::NTL; ++nt) {
-                    const int col = nt * 8 + gid;
-                    bv[nt] = (ev && col < S::KL) ? fe[(K2 ? K0 + K1 : K0) + col] : 0.0;
-                }
-#pragma unroll
-                for (int mt = 0; mt < S::MT; ++mt) {
-                    const int col = mt * 8 + gid;
-                    double av = 0.0;
-                    if (ev && col < S::LS) {
-                        if constexpr (K2 != 0)
-                            av = x * fe[col / K1] * fe[K0 + col % K1];
-                        else
-                            av = x * fe[col];
-                    }
-#pragma unroll
-                    for (int nt = 0; nt < S::NTL; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], av, bv[nt]);
-                }
-            }
-            __syncthreads();  // buffer ch&1 is refilled at ch+2
-        }
-        // fixed-order sum of the four warps' fragments -> ypart[sg]
-        double* rw = red + (size_t)warp * S::MT * S::NTL * 64;
-#pragma unroll
-        for (int mt = 0; mt < S::MT; ++mt)
+        for (int j = 0; j < S::NTL; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    issue_records(0);
+    issue_records(1);
+    cpa_wait<1>();
+    __syncthreads();
+    issue_gathers(0, 0);
+    for (int ch = 0; cc.valid(); ++ch) {
+        issue_records((ch + 2) % 3);
+        cpa_wait<1>();  // gathers of chunk ch and records of chunk ch+1 have landed
+        __syncthreads();
+        issue_gathers((ch + 1) % 3, (ch + 1) & 1);
+        const int n = cc.n(S::CH);
+        const double* f = rowbuf + (size_t)(ch & 1) * S::row_doubles;
+        const int ks_n = (n + 3) / 4;
+        for (int ks = warp; ks < ks_n; ks += S::WARPS) {
+            const int e = ks * 4 + tig;
+            const bool ev = e < n;
+            const double* fe = f + (size_t)e * S::FW;
+            const double x = ev ? fe[S::RW] : 0.0;
+            double bv[S::NTL];
 #pragma unroll
             for (int nt = 0; nt < S::NTL; ++nt) {
-                rw[(mt * S::NTL + nt) * 64 + gid * 8 + 2 * tig] = acc[mt][nt][0];
-                rw[(mt * S::NTL + nt) * 64 + gid * 8 + 2 * tig + 1] = acc[mt][nt][1];
+                const int col = nt * 8 + gid;
+                bv[nt] = (ev && col < S::KL) ? fe[(K2 ? K0 + K1 : K0) + col] : 0.0;
             }
-        __syncthreads();
-        for (int q = tid; q < S::L; q += S::THREADS) {
-            const int sidx = q / S::KL, t = q - sidx * S::KL;  // Kronecker column q = s * KL + t
-            const int mt = sidx / 8, nt = t / 8, o = (sidx % 8) * 8 + (t % 8);
-            double v = 0.0;
 #pragma unroll
-            for (int w = 0; w < S::WARPS; ++w) v += red[(size_t)w * S::MT * S::NTL * 64 + (mt * S::NTL + nt) * 64 + o];
-            a.ypart[sg * S::L + q] = v;
+            for (int mt = 0; mt < S::MT; ++mt) {
+                const int col = mt * 8 + gid;
+                double av = 0.0;
+                if (ev && col < S::LS) {
+                    if constexpr (K2 != 0)
+                        av = x * fe[col / K1] * fe[K0 + col % K1];
+                    else
+                        av = x * fe[col];
+                }
+#pragma unroll
+                for (int nt = 0; nt < S::NTL; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], av, bv[nt]);
+            }
         }
+        if (cc.last(S::CH)) {
+            // fixed-order sum of the warps' fragments -> ypart[segment]
+            double* rw = red + (size_t)warp * S::MT * S::NTL * 64;
+#pragma unroll
+            for (int mt = 0; mt < S::MT; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < S::NTL; ++nt) {
+                    rw[(mt * S::NTL + nt) * 64 + gid * 8 + 2 * tig] = acc[mt][nt][0];
+                    rw[(mt * S::NTL + nt) * 64 + gid * 8 + 2 * tig + 1] = acc[mt][nt][1];
+                    acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+                }
+            __syncthreads();
+            const uint64_t sg = cc.sg;
+            for (int q = tid; q < S::L; q += S::THREADS) {
+                const int sidx = q / S::KL, t = q - sidx * S::KL;  // Kronecker column q = s * KL + t
+                const int o = ((sidx / 8) * S::NTL + t / 8) * 64 + (sidx % 8) * 8 + (t % 8);
+                double v = 0.0;
+#pragma unroll
+                for (int w = 0; w < S::WARPS; ++w) v += red[(size_t)w * S::MT * S::NTL * 64 + o];
+                a.ypart[sg * S::L + q] = v;
+            }
+        }
+        cc.advance(a, rend, S::CH);
     }
+    cpa_wait<0>();
 }
 
 // ---------------------------------------------------------------- fix-up --

@@ -89,6 +89,70 @@ struct ChunkCursor {
     }
 };
 
+// One k-step (4 nonzeros) of Y_seg += S^T V on the DMMA pipe.  Lane (gid, tig)
+// supplies S[e][8 mt + gid] and V[e][8 nt + gid] for nonzero e = 4 ks + tig.
+template <int K0, int K1, int K2, class S, bool FULL>
+__device__ __forceinline__ void kstep(const double* f, int ks, int n, int gid, int tig,
+                                      double (&acc)[S::MT][S::NTL][2]) {
+    const int e = ks * 4 + tig;
+    const bool ev = FULL || e < n;
+    const double* fe = f + (size_t)e * S::FW;
+    const double x = ev ? fe[S::RW] : 0.0;
+    double bv[S::NTL];
+#pragma unroll
+    for (int nt = 0; nt < S::NTL; ++nt) {
+        const int col = nt * 8 + gid;
+        bv[nt] = (ev && col < S::KL) ? fe[(K2 ? K0 + K1 : K0) + col] : 0.0;
+    }
+    if constexpr (K2 != 0) {
+        static_assert(K1 == 8 && K0 % 2 == 0, "order-4 layout: column = 8 * (U_a index) + U_b index");
+        // S[e][8 mt + gid] = x U_a[mt] U_b[gid]: one product per lane, then U_a pairs (16-byte loads)
+        const double xb = ev ? x * fe[K0 + gid] : 0.0;
+#pragma unroll
+        for (int mp = 0; mp < S::MT / 2; ++mp) {
+            const double2 ap = *reinterpret_cast<const double2*>(fe + 2 * mp);
+            const double a0 = ap.x * xb, a1 = ap.y * xb;
+#pragma unroll
+            for (int nt = 0; nt < S::NTL; ++nt) {
+                dmma(acc[2 * mp][nt][0], acc[2 * mp][nt][1], a0, bv[nt]);
+                dmma(acc[2 * mp + 1][nt][0], acc[2 * mp + 1][nt][1], a1, bv[nt]);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int mt = 0; mt < S::MT; ++mt) {
+            const int col = mt * 8 + gid;
+            const double av = (ev && col < S::LS) ? x * fe[col] : 0.0;
+#pragma unroll
+            for (int nt = 0; nt < S::NTL; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], av, bv[nt]);
+        }
+    }
+}
+
+// 16-byte pieces of one factor's rows for n staged nonzeros: four (K/2)
+// consecutive lanes copy one row; full chunks run a fixed-trip loop.
+template <int KM, int OFF, class S>
+__device__ __forceinline__ void gather_mode(const double* __restrict__ u, const uint32_t* r, double* dst, int n,
+                                            int tid) {
+    constexpr int PM = KM / 2;
+    if (n == S::CH) {
+        constexpr int TOT = S::CH * PM, IT = (TOT + S::THREADS - 1) / S::THREADS;
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int q = tid + it * S::THREADS;
+            if (TOT % S::THREADS == 0 || q < TOT) {
+                const int e = q / PM, p = q - e * PM;
+                cpa16(dst + (size_t)e * S::FW + OFF + 2 * p, u + (size_t)r[e] * KM + 2 * p);
+            }
+        }
+    } else {
+        for (int q = tid; q < n * PM; q += S::THREADS) {
+            const int e = q / PM, p = q - e * PM;
+            cpa16(dst + (size_t)e * S::FW + OFF + 2 * p, u + (size_t)r[e] * KM + 2 * p);
+        }
+    }
+}
+
 // Three-stage pipeline per CTA over a flat chunk sequence:
 //   iteration c: index records of chunk c+2 (coalesced 4-byte cp.async),
 //                factor-row gathers of chunk c+1 (16-byte cp.async pieces,
@@ -133,23 +197,10 @@ __global__ void __launch_bounds__(256) k_longseg_mma(LongArgs a) {
             const int n = cg.n(S::CH);
             const uint32_t* r = rec + (size_t)rslot * S::rec_words;
             double* dst = rowbuf + (size_t)bslot * S::row_doubles;
-            for (int q = tid; q < n * S::PP; q += S::THREADS) {
-                const int e = q / S::PP, pc = q - e * S::PP;
-                const double* src;
-                int off;
-                if (pc < P0) {
-                    src = a.u0 + (size_t)r[e] * K0 + 2 * pc;
-                    off = 2 * pc;
-                } else if (pc < P0 + P1) {
-                    src = a.u1 + (size_t)r[S::CH + e] * K1 + 2 * (pc - P0);
-                    off = K0 + 2 * (pc - P0);
-                } else {
-                    src = a.u2 + (size_t)r[2 * S::CH + e] * K2 + 2 * (pc - P0 - P1);
-                    off = K0 + K1 + 2 * (pc - P0 - P1);
-                }
-                cpa16(dst + (size_t)e * S::FW + off, src);
-            }
-            for (int e = tid; e < n; e += S::THREADS) cpa8(dst + (size_t)e * S::FW + S::RW, a.val + cg.z0 + e);
+            gather_mode<K0, 0, S>(a.u0, r, dst, n, tid);
+            gather_mode<K1, K0, S>(a.u1, r + S::CH, dst, n, tid);
+            if constexpr (K2 != 0) gather_mode<K2, K0 + K1, S>(a.u2, r + 2 * S::CH, dst, n, tid);
+            if (tid < n) cpa8(dst + (size_t)tid * S::FW + S::RW, a.val + cg.z0 + tid);
             cg.advance(a, rend, S::CH);
         }
         cpa_commit();
@@ -173,31 +224,11 @@ __global__ void __launch_bounds__(256) k_longseg_mma(LongArgs a) {
         issue_gathers((ch + 1) % 3, (ch + 1) & 1);
         const int n = cc.n(S::CH);
         const double* f = rowbuf + (size_t)(ch & 1) * S::row_doubles;
-        const int ks_n = (n + 3) / 4;
-        for (int ks = warp; ks < ks_n; ks += S::WARPS) {
-            const int e = ks * 4 + tig;
-            const bool ev = e < n;
-            const double* fe = f + (size_t)e * S::FW;
-            const double x = ev ? fe[S::RW] : 0.0;
-            double bv[S::NTL];
-#pragma unroll
-            for (int nt = 0; nt < S::NTL; ++nt) {
-                const int col = nt * 8 + gid;
-                bv[nt] = (ev && col < S::KL) ? fe[(K2 ? K0 + K1 : K0) + col] : 0.0;
-            }
-#pragma unroll
-            for (int mt = 0; mt < S::MT; ++mt) {
-                const int col = mt * 8 + gid;
-                double av = 0.0;
-                if (ev && col < S::LS) {
-                    if constexpr (K2 != 0)
-                        av = x * fe[col / K1] * fe[K0 + col % K1];
-                    else
-                        av = x * fe[col];
-                }
-#pragma unroll
-                for (int nt = 0; nt < S::NTL; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], av, bv[nt]);
-            }
+        if (n == S::CH) {
+#pragma unroll 2
+            for (int ks = warp; ks < S::CH / 4; ks += S::WARPS) kstep<K0, K1, K2, S, true>(f, ks, n, gid, tig, acc);
+        } else {
+            for (int ks = warp; ks < (n + 3) / 4; ks += S::WARPS) kstep<K0, K1, K2, S, false>(f, ks, n, gid, tig, acc);
         }
         if (cc.last(S::CH)) {
             // fixed-order sum of the warps' fragments -> ypart[segment]
@@ -236,20 +267,24 @@ struct LF_ {
     static constexpr int AB = (RT / 8) * NT, ABW = (AB + WARPS - 1) / WARPS;
     static constexpr int NLT = LP / 8, MB = NT * NLT, MBW = (MB + WARPS - 1) / WARPS;
     static constexpr int WQ = (KN * KN + THREADS - 1) / THREADS;
-    static constexpr size_t smem = (size_t)RT * LDY * 8 + (size_t)RT * ALD * 8 + 64;
+    static constexpr int KSPLIT = AB >= WARPS ? 1 : WARPS / AB;  // A-GEMM k split over idle warps
+    static constexpr int L2 = L / 2, YU = 4;                     // Y loads: double2, 4 in flight
+    static constexpr size_t smem = (size_t)RT * LDY * 8 + (size_t)(KSPLIT + 1) * RT * ALD * 8 + 64;
+    static_assert(L % 2 == 0 && LDY % 2 == 0, "16-byte Y loads");
     static_assert(L % 4 == 0, "k-steps");
 };
 
 template <int L, int KN>
-__global__ void __launch_bounds__(128) k_longfix_mma(LongArgs a) {
+__global__ void __launch_bounds__(128, 1) k_longfix_mma(LongArgs a) {
     using F = LF_<L, KN>;
     if (skip_kernel(a.st, a.run_if)) return;
     extern __shared__ __align__(16) double sm[];
     double* sY = sm;
     double* sA = sm + (size_t)F::RT * F::LDY;
+    double* sAp = sA + (size_t)F::RT * F::ALD;  // [KSPLIT][RT][ALD] A-GEMM partials
     __shared__ double red[F::WARPS];
     __shared__ uint32_t srow[F::RT];
-    __shared__ int sval[F::RT];
+    __shared__ int64_t ss0[F::RT], ss1[F::RT];  // segment range; empty when not this rank's row
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gid = lane >> 2, tig = lane & 3;
     const uint64_t G = gridDim.x, c = blockIdx.x;
@@ -269,65 +304,90 @@ __global__ void __launch_bounds__(128) k_longfix_mma(LongArgs a) {
         const int nr = (int)min((uint64_t)F::RT, le - t0);
         if (tid < F::RT) {
             uint32_t row = 0;
-            int v = 0;
+            int64_t s0 = 0, s1 = 0;
             if (tid < nr) {
                 row = a.long_ids[t0 + tid];
-                v = (row >= a.rbase && row < rend);
+                if (row >= a.rbase && row < rend) {
+                    s0 = a.long_segptr[t0 + tid];
+                    s1 = a.long_segptr[t0 + tid + 1];
+                }
             }
             srow[tid] = row;
-            sval[tid] = v;
+            ss0[tid] = s0;
+            ss1[tid] = s1;
         }
         __syncthreads();
-        // Y rows: segment partials summed in segment order
-        for (int q = tid; q < F::RT * L; q += F::THREADS) {
-            const int r = q / L, l = q - r * L;
-            double y = 0.0;
-            if (r < nr && sval[r]) {
-                const int64_t s0 = a.long_segptr[t0 + r], s1 = a.long_segptr[t0 + r + 1];
-                for (int64_t sg = s0; sg < s1; ++sg) y += a.ypart[sg * L + l];
+        // Y rows: segment partials summed in segment order; first segments of
+        // YU elements loaded together, further segments (rows > kSegLen) after
+        for (int q0 = tid; q0 < F::RT * F::L2; q0 += F::THREADS * F::YU) {
+            double2 v[F::YU];
+#pragma unroll
+            for (int u = 0; u < F::YU; ++u) {
+                const int q = q0 + u * F::THREADS;
+                v[u] = make_double2(0.0, 0.0);
+                if (q < F::RT * F::L2) {
+                    const int r = q / F::L2, l = 2 * (q - r * F::L2);
+                    if (ss1[r] > ss0[r]) v[u] = *reinterpret_cast<const double2*>(a.ypart + ss0[r] * L + l);
+                }
             }
-            sY[(size_t)r * F::LDY + l] = y;
+#pragma unroll
+            for (int u = 0; u < F::YU; ++u) {
+                const int q = q0 + u * F::THREADS;
+                if (q < F::RT * F::L2) {
+                    const int r = q / F::L2, l = 2 * (q - r * F::L2);
+                    for (int64_t sg = ss0[r] + 1; sg < ss1[r]; ++sg) {
+                        const double2 w = *reinterpret_cast<const double2*>(a.ypart + sg * L + l);
+                        v[u].x += w.x;
+                        v[u].y += w.y;
+                    }
+                    *reinterpret_cast<double2*>(sY + (size_t)r * F::LDY + l) = v[u];
+                }
+            }
         }
         __syncthreads();
         if (a.kind == kTTMcTC) {
+            constexpr int KS = L / 4;
 #pragma unroll
             for (int bi = 0; bi < F::ABW; ++bi) {
-                const int b = warp + bi * F::WARPS;
+                const int b = (warp % (F::WARPS / F::KSPLIT)) + bi * (F::WARPS / F::KSPLIT);
+                const int kp = warp / (F::WARPS / F::KSPLIT);
                 if (b < F::AB) {
                     const int mt = b / F::NT, nt = b - mt * F::NT;
                     const int gcol = nt * 8 + gid;
                     double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
-                    for (int ks = 0; ks < L / 4; ks += 2) {
+                    const int k0 = kp * KS / F::KSPLIT, k1 = (kp + 1) * KS / F::KSPLIT;
+                    for (int ks = k0; ks < k1; ks += 2) {
                         const double y0 = sY[(size_t)(mt * 8 + gid) * F::LDY + ks * 4 + tig];
                         const double g0 = gcol < KN ? __ldg(a.gt + (size_t)(ks * 4 + tig) * KN + gcol) : 0.0;
                         dmma(c0, c1, y0, g0);
-                        if (ks + 1 < L / 4) {
+                        if (ks + 1 < k1) {
                             const double y1 = sY[(size_t)(mt * 8 + gid) * F::LDY + (ks + 1) * 4 + tig];
                             const double g1 = gcol < KN ? __ldg(a.gt + (size_t)((ks + 1) * 4 + tig) * KN + gcol) : 0.0;
                             dmma(d0, d1, y1, g1);
                         }
                     }
                     const int row = mt * 8 + gid, col = nt * 8 + 2 * tig;
-                    sA[row * F::ALD + col] = c0 + d0;
-                    sA[row * F::ALD + col + 1] = c1 + d1;
+                    double* dst = sAp + (size_t)kp * F::RT * F::ALD;
+                    dst[row * F::ALD + col] = c0 + d0;
+                    dst[row * F::ALD + col + 1] = c1 + d1;
                 }
-            }
-        } else {
-            for (int q = tid; q < F::RT * KN; q += F::THREADS) {
-                const int r = q / KN, k = q - r * KN;
-                sA[r * F::ALD + k] = (r < nr && sval[r]) ? a.un[(size_t)srow[r] * KN + k] : 0.0;
             }
         }
         __syncthreads();
         for (int q = tid; q < F::RT * KN; q += F::THREADS) {
             const int r = q / KN, k = q - r * KN;
-            if (r < nr && sval[r]) {
-                const double v = sA[r * F::ALD + k];
+            double v = 0.0;
+            if (ss1[r] > ss0[r]) {
+                if (a.kind == kTTMcTC) {
+#pragma unroll
+                    for (int kp = 0; kp < F::KSPLIT; ++kp) v += sAp[(size_t)kp * F::RT * F::ALD + r * F::ALD + k];
+                } else {
+                    v = a.un[(size_t)srow[r] * KN + k];
+                }
                 if (a.A) a.A[(size_t)srow[r] * KN + k] = v;
                 mx = fmax(mx, fabs(v));
-            } else {
-                sA[r * F::ALD + k] = 0.0;
             }
+            sA[r * F::ALD + k] = v;
         }
         __syncthreads();
 #pragma unroll

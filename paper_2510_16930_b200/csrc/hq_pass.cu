@@ -369,15 +369,19 @@ int tile_grid(const ModeShape& sh) {
     return short_grid();
 }
 
+// short-row tile kernels run (and own partial slots) only when the mode has short rows
+int short_slots(const ModeLayout& L, const ModeShape& sh) {
+    return (L.long_rows == 0 || L.nonempty_rows > L.long_rows) ? tile_grid(sh) : 0;
+}
+
 int pass_slots(const ModeLayout& L, const ModeShape& sh) {
-    return tile_grid(sh) + (L.long_rows ? long_grid(L) : 0);
+    return short_slots(L, sh) + (L.long_rows ? long_grid(L) : 0);
 }
 
 size_t pass_ypart_doubles(const ModeLayout& L, const ModeShape& sh) { return (size_t)L.long_segments * sh.L; }
 
 int pass_launch_count(const ModeLayout& L, const ModeShape& sh) {
-    (void)sh;
-    return 1 + (L.long_rows ? 2 : 0);
+    return (short_slots(L, sh) ? 1 : 0) + (L.long_rows ? 2 : 0);
 }
 
 void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const FactorPtrs& f, PassKind kind,
@@ -414,7 +418,9 @@ void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const Fac
     a.R = generic_rows_per_tile(sh);
     a.ntiles = (int64_t)ceil_div(a.rows, a.R);
     a.slot0 = 0;
-    if (fast_supported(sh) && !force_generic()) {
+    if (!short_slots(L, sh)) {
+        // every nonempty row is long: no tile kernel
+    } else if (fast_supported(sh) && !force_generic()) {
         FastArgs fa{};
         fa.rbase = a.rbase;
         fa.rows = a.rows;
@@ -471,7 +477,7 @@ void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const Fac
         la.wpart = out.wpart;
         la.maxpart = out.maxpart;
         la.kind = kind;
-        la.slot0 = tile_grid(sh);
+        la.slot0 = short_slots(L, sh);
         la.st = st;
         la.run_if = run_if;
         launch_long_fast(la, sh, long_grid(L), s);
@@ -479,7 +485,7 @@ void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const Fac
         int segs = (int)std::min<uint64_t>(L.long_segments, (uint64_t)num_sms() * 8);
         k_pass_longseg_generic<<<segs, kGenericThreads, 0, s>>>(a);
         HQ_CHECK_LAUNCH();
-        a.slot0 = tile_grid(sh);
+        a.slot0 = short_slots(L, sh);
         size_t smem2 = sizeof(double) * ((size_t)sh.L + sh.kn);
         set_smem((const void*)k_pass_longfix_generic, smem2);
         k_pass_longfix_generic<<<long_grid(L), kGenericThreads, smem2, s>>>(a);

@@ -281,6 +281,7 @@ def run_engine(args, ws, rank, local):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     solver.run(K)
+    # (status read after the timed region)
     e1.record(stream)
     torch.cuda.synchronize()
     if ws > 1:
@@ -288,6 +289,7 @@ def run_engine(args, ws, rank, local):
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     solver.sync()
+    dev_status = solver.status()
     if ws > 1:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -396,6 +398,7 @@ def run_engine(args, ws, rank, local):
                                     "FP64 entry); HBM: MEASURED_PEAKS.json",
                      "ttmctc_canonical": {"flops": ttm_f, "bytes": ttm_b,
                                           "frac_of_fp64_peak": ttm_f / (avg_pass_ms * 1e-3) / 1e12 / peak64}},
+        "solver_status": dev_status,
         "gpu_launches": solver.launches_per_sweep() * K,
         "clocks": clk,
     }

@@ -113,7 +113,7 @@ EXPORTED_SYMBOLS = [
     "hq_tensor_buckets", "hq_tensor_norm_sq",
     "hq_ttmc_core", "hq_ttmctc", "hq_qr_orthonormal", "hq_subspace_distance", "hq_random_factors",
     "hq_config_default", "hq_hoqri", "hq_fit_error",
-    "hq_solver_create", "hq_solver_destroy", "hq_solver_run", "hq_solver_sync", "hq_solver_launch_mode_pass",
+    "hq_solver_create", "hq_solver_destroy", "hq_solver_run", "hq_solver_sync", "hq_solver_status", "hq_solver_launch_mode_pass",
     "hq_solver_launch_ttmctc", "hq_solver_launches_per_sweep", "hq_solver_download", "hq_solver_mode_pass_work",
     "hq_solver_ttmctc_work", "hq_nccl_unique_id", "hq_comm_create", "hq_comm_destroy", "hq_partition_rows",
     "hq_solver_create_dist",
@@ -157,6 +157,7 @@ def load_library(path: str = None) -> C.CDLL:
     L.hq_solver_destroy.argtypes = [vp]
     L.hq_solver_run.argtypes = [vp, C.c_uint64]
     L.hq_solver_sync.argtypes = [vp]
+    L.hq_solver_status.argtypes = [vp, C.POINTER(C.c_int64)]
     L.hq_solver_launch_mode_pass.argtypes = [vp, C.c_int]
     L.hq_solver_launch_ttmctc.argtypes = [vp, C.c_int]
     L.hq_solver_launches_per_sweep.argtypes = [vp, C.POINTER(C.c_uint64)]
@@ -619,6 +620,13 @@ class Solver:
 
     def sync(self):
         _check(load_library().hq_solver_sync(self._h))
+
+    def status(self):
+        """Device status word: sweeps done, Householder fallbacks, abort code, degenerate mode, shifted CholeskyQR3 updates."""
+        out = (C.c_int64 * 5)()
+        _check(load_library().hq_solver_status(self._h, out))
+        return {"sweeps": out[0], "fallbacks": out[1], "abort": out[2], "degenerate_mode": out[3],
+                "shifted": out[4]}
 
     def launch_mode_pass(self, mode):
         _check(load_library().hq_solver_launch_mode_pass(self._h, mode))

@@ -91,88 +91,284 @@ __device__ double rng_normal(DevRng* r) {
     return rad * cos(theta);
 }
 
-constexpr int kHhThreads = 1024;
+// Multi-CTA Householder QR (one CTA per SM, co-resident: cooperative launch)
+// with the reference's exact step sequence (dense_core.cpp:127-198): for each
+// column k, normx over rows >= k, the rank-deficiency fill when
+// normx <= 1e-12 ||A||_F, alpha = -sign(x0) normx, v = x - alpha e_k,
+// beta = 2 / v^T v, and the reflector applied to columns > k; then Q formed by
+// backward accumulation and its columns' signs flipped where alpha < 0
+// (R_kk >= 0).  CTA c owns rows [m c / G, m (c + 1) / G); each column needs
+// one pass over the rows and one grid barrier: the pass that applies
+// reflector k also accumulates, per CTA, T_j = sum_{i > k+1} w_{i,k+1} w_ij for
+// the next column, and every CTA reduces the G partials in the same fixed
+// order, so all CTAs derive identical alpha / beta / dots.  The fill takes
+// its normals from the precomputed stream (fill_table) when one is given,
+// else CTA 0 draws them with the device MT19937-64.
+constexpr int kHhThreads = 256;
+constexpr int kHhSlot = 36;  // partial-slot stride (K <= 32 sums + ||A||^2)
 
-__global__ void __launch_bounds__(kHhThreads) k_householder(const double* __restrict__ A, uint64_t m, int n,
-                                                            double* __restrict__ q, double* __restrict__ work,
-                                                            const DevStatus* st, int run_if) {
-    if (skip_kernel(st, run_if)) return;
-    __shared__ DevRng rng;
-    __shared__ double red[33];
-    __shared__ double betas[kMaxRank];
-    __shared__ int flip[kMaxRank];
-    double* w = work;                       // m x n
-    double* refl = work + m * (uint64_t)n;  // n reflectors of length m
-    const uint64_t tid = threadIdx.x, nt = blockDim.x;
-    double part = 0.0;
-    for (uint64_t i = tid; i < m * (uint64_t)n; i += nt) {
-        double v = A[i];
-        w[i] = v;
-        part += v * v;
-    }
-    const double anorm = sqrt(block_sum(part, red));
-    const double pivot_tol = 1e-12 * anorm;
-    if (tid == 0) rng_seed(&rng, 0x48514F5251ull);
+struct HhCtl {
+    unsigned int bar_count;
+    unsigned int bar_gen;
+    unsigned int rng_seeded;
+    unsigned int pad;
+    DevRng rng;
+};
+
+__host__ __device__ inline size_t hh_part_doubles(int G) { return (size_t)2 * G * kHhSlot; }
+constexpr size_t kHhCtlDoubles = (sizeof(HhCtl) + 15) / 16 * 2;
+
+__device__ __forceinline__ void hh_grid_sync(HhCtl* ctl, unsigned int& gen) {
     __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned int arrived = atomicAdd(&ctl->bar_count, 1u);
+        if (arrived == gridDim.x - 1) {
+            ctl->bar_count = 0;
+            __threadfence();
+            atomicExch(&ctl->bar_gen, gen + 1);
+        } else {
+            while (atomicAdd(&ctl->bar_gen, 0u) == gen) __nanosleep(64);
+        }
+        __threadfence();
+        gen = gen + 1;
+    }
+    __syncthreads();
+}
+
+// per-CTA sums of acc[0..cnt) (deterministic: warp tree, then warps in order)
+template <int KM>
+__device__ __forceinline__ void hh_cta_partials(const double (&acc)[KM + 1], int cnt, double* red_w, double* out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int j = 0; j <= KM; ++j) {
+        double v = acc[j];
+        for (int o = 16; o; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if (lane == 0) red_w[warp * (KM + 1) + j] = v;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+        double t = 0.0;
+        for (int w = 0; w < nw; ++w) t += red_w[w * (KM + 1) + j];
+        out[j] = t;
+    }
+}
+
+// every CTA: T[j] = sum over CTAs (in order) of part[c][j], j < cnt
+__device__ __forceinline__ void hh_reduce_all(const double* part, int cnt, double* T) {
+    for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+        double t = 0.0;
+        for (unsigned c = 0; c < gridDim.x; ++c) t += part[(size_t)c * kHhSlot + j];
+        T[j] = t;
+    }
+    __syncthreads();
+}
+
+template <int KM>
+__device__ __forceinline__ double pick(const double (&row)[KM], int k) {
+    double v = 0.0;
+#pragma unroll
+    for (int j = 0; j < KM; ++j)
+        if (j == k) v = row[j];
+    return v;
+}
+
+template <int KM>
+__global__ void __launch_bounds__(kHhThreads) k_householder_mc(const double* __restrict__ A, uint64_t m, int n,
+                                                               double* __restrict__ q, double* __restrict__ work,
+                                                               const double* __restrict__ table, uint64_t table_len,
+                                                               const DevStatus* st, int run_if) {
+    if (skip_kernel(st, run_if)) return;
+    __shared__ double red_w[(kHhThreads / 32) * (KM + 1)];
+    __shared__ double T[KM + 1];
+    __shared__ double dots[KM];
+    __shared__ double betas[KM];
+    __shared__ int flip[KM];
+    __shared__ double sc[4];  // normx, pivot_tol, x0 - alpha
+    const unsigned G = gridDim.x, c = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+    // work: control block | partials [2][G][kHhSlot] | w (m x n) | reflectors (n x m);
+    // fixed offsets, so every (m, n) shares one barrier
+    HhCtl* ctl = reinterpret_cast<HhCtl*>(work);
+    double* part = work + kHhCtlDoubles;
+    double* w = part + hh_part_doubles((int)G);
+    double* refl = w + m * (uint64_t)n;  // rows >= k of reflector k used
+    const uint64_t r0 = m * c / G, r1 = m * (c + 1) / G;
+    unsigned int gen = 0;
+    if (tid == 0) gen = atomicAdd(&ctl->bar_gen, 0u);
+    if (c == 0 && tid == 0) ctl->rng_seeded = 0;  // each QR starts the fill stream afresh (read after a barrier)
+    int par = 0;
+    uint64_t pos = 0;  // fill-stream position (identical in every CTA)
+    auto slot = [&](int pr) { return part + ((size_t)pr * G + c) * kHhSlot; };
+    auto slots = [&](int pr) { return part + (size_t)pr * G * kHhSlot; };
+
+    // copy A -> w; partials of T_j for column 0 (rows > 0) and ||A||^2 (slot KM)
+    {
+        double acc[KM + 1];
+#pragma unroll
+        for (int j = 0; j <= KM; ++j) acc[j] = 0.0;
+        for (uint64_t i = r0 + tid; i < r1; i += nt) {
+            double row[KM];
+#pragma unroll
+            for (int j = 0; j < KM; ++j) row[j] = j < n ? A[i * n + j] : 0.0;
+#pragma unroll
+            for (int j = 0; j < KM; ++j)
+                if (j < n) {
+                    w[i * n + j] = row[j];
+                    acc[KM] += row[j] * row[j];
+                    if (i > 0) acc[j] += row[0] * row[j];
+                }
+        }
+        hh_cta_partials<KM>(acc, KM + 1, red_w, slot(par));
+    }
+    hh_grid_sync(ctl, gen);
+    double ptol = 0.0;
     for (int k = 0; k < n; ++k) {
-        part = 0.0;
-        for (uint64_t i = k + tid; i < m; i += nt) part += w[i * n + k] * w[i * n + k];
-        double normx = sqrt(block_sum(part, red));
-        if (normx <= pivot_tol) {
-            do {
-                if (tid == 0)
-                    for (uint64_t i = k; i < m; ++i) w[i * n + k] = rng_normal(&rng);
-                __syncthreads();
-                part = 0.0;
-                for (uint64_t i = k + tid; i < m; i += nt) part += w[i * n + k] * w[i * n + k];
-                normx = sqrt(block_sum(part, red));
-            } while (normx == 0.0);
+        hh_reduce_all(slots(par), k == 0 ? KM + 1 : n, T);
+        if (k == 0) ptol = 1e-12 * sqrt(T[KM]);
+        double normx;
+        {
+            const double x0 = w[(uint64_t)k * n + k];
+            normx = sqrt(T[k] + x0 * x0);
         }
-        const double x0 = w[(uint64_t)k * n + k];
-        const double alpha = (x0 >= 0.0) ? -normx : normx;
-        double* v = refl + (uint64_t)k * m;
-        part = 0.0;
-        for (uint64_t i = k + tid; i < m; i += nt) {
-            double vi = (i == (uint64_t)k) ? x0 - alpha : w[i * n + k];
-            v[i - k] = vi;
-            part += vi * vi;
+        // rank-deficient column: rows >= k replaced by the next normals of the
+        // fill stream (dense_core.cpp:146-157), redrawn while the norm is zero
+        bool need = normx <= ptol;
+        while (need) {
+            const uint64_t cnt = m - (uint64_t)k;
+            if (table && pos + cnt <= table_len) {
+                for (uint64_t i = (r0 > (uint64_t)k ? r0 : (uint64_t)k) + tid; i < r1; i += nt)
+                    w[i * n + k] = table[pos + (i - k)];
+            } else if (c == 0 && tid == 0) {
+                if (!ctl->rng_seeded) {
+                    rng_seed(&ctl->rng, 0x48514F5251ull);
+                    for (uint64_t d = 0; d < pos; ++d) rng_normal(&ctl->rng);  // normals already taken from the table
+                    ctl->rng_seeded = 1;
+                }
+                for (uint64_t i = k; i < m; ++i) w[i * n + k] = rng_normal(&ctl->rng);
+            }
+            pos += cnt;
+            hh_grid_sync(ctl, gen);
+            {
+                double acc[KM + 1];
+#pragma unroll
+                for (int j = 0; j <= KM; ++j) acc[j] = 0.0;
+                for (uint64_t i = (r0 > (uint64_t)k + 1 ? r0 : (uint64_t)k + 1) + tid; i < r1; i += nt) {
+                    const double wk = w[i * n + k];
+#pragma unroll
+                    for (int j = 0; j < KM; ++j)
+                        if (j >= k && j < n) acc[j] += wk * w[i * n + j];
+                }
+                par ^= 1;
+                hh_cta_partials<KM>(acc, n, red_w, slot(par));
+            }
+            hh_grid_sync(ctl, gen);
+            hh_reduce_all(slots(par), n, T);
+            const double x0 = w[(uint64_t)k * n + k];
+            normx = sqrt(T[k] + x0 * x0);
+            need = normx == 0.0;
         }
-        const double vn2 = block_sum(part, red);
-        const double beta = (vn2 > 0.0) ? 2.0 / vn2 : 0.0;
-        for (int j = k; j < n; ++j) {
-            part = 0.0;
-            for (uint64_t i = k + tid; i < m; i += nt) part += v[i - k] * w[i * n + j];
-            const double dot = block_sum(part, red) * beta;
-            for (uint64_t i = k + tid; i < m; i += nt) w[i * n + j] -= dot * v[i - k];
-            __syncthreads();
-        }
+        // reflector (every CTA derives the same values)
         if (tid == 0) {
-            w[(uint64_t)k * n + k] = alpha;
+            const double x0 = w[(uint64_t)k * n + k];
+            const double alpha = (x0 >= 0.0) ? -normx : normx;
+            const double vk = x0 - alpha;
+            const double vn2 = T[k] + vk * vk;
+            sc[2] = vk;
+            betas[k] = (vn2 > 0.0) ? 2.0 / vn2 : 0.0;
             flip[k] = alpha < 0.0;
-            betas[k] = beta;
         }
         __syncthreads();
-    }
-    for (uint64_t i = tid; i < m * (uint64_t)n; i += nt) q[i] = 0.0;
-    __syncthreads();
-    for (int k = (int)tid; k < n; k += nt) q[(uint64_t)k * n + k] = 1.0;
-    __syncthreads();
-    for (int kk = n - 1; kk >= 0; --kk) {
-        const double beta = betas[kk];
-        if (beta == 0.0) continue;
-        const double* v = refl + (uint64_t)kk * m;
-        for (int j = kk; j < n; ++j) {
-            part = 0.0;
-            for (uint64_t i = kk + tid; i < m; i += nt) part += v[i - kk] * q[i * n + j];
-            const double dot = block_sum(part, red) * beta;
-            for (uint64_t i = kk + tid; i < m; i += nt) q[i * n + j] -= dot * v[i - kk];
-            __syncthreads();
+        for (int j = k + 1 + (int)tid; j < n; j += nt) dots[j] = betas[k] * (sc[2] * w[(uint64_t)k * n + j] + T[j]);
+        __syncthreads();
+        // apply to columns > k over rows >= k; partial T for column k+1 (rows > k+1)
+        {
+            double acc[KM + 1];
+#pragma unroll
+            for (int j = 0; j <= KM; ++j) acc[j] = 0.0;
+            const double vk = sc[2];
+            for (uint64_t i = (r0 > (uint64_t)k ? r0 : (uint64_t)k) + tid; i < r1; i += nt) {
+                double row[KM];
+#pragma unroll
+                for (int j = 0; j < KM; ++j) row[j] = (j >= k && j < n) ? w[i * n + j] : 0.0;
+                const double v = (i == (uint64_t)k) ? vk : pick<KM>(row, k);
+                refl[(uint64_t)k * m + i] = v;
+#pragma unroll
+                for (int j = 0; j < KM; ++j)
+                    if (j > k && j < n) {
+                        row[j] -= dots[j] * v;
+                        w[i * n + j] = row[j];
+                    }
+                if (i > (uint64_t)k + 1) {
+                    const double wn = pick<KM>(row, k + 1);
+#pragma unroll
+                    for (int j = 0; j < KM; ++j)
+                        if (j >= k + 1 && j < n) acc[j] += wn * row[j];
+                }
+            }
+            par ^= 1;
+            hh_cta_partials<KM>(acc, n, red_w, slot(par));
         }
+        hh_grid_sync(ctl, gen);
     }
-    for (uint64_t i = tid; i < m * (uint64_t)n; i += nt) {
-        int col = (int)(i % n);
-        if (flip[col]) q[i] = -q[i];
+    // ---- Q = H_0 ... H_{n-1} [I; 0] by backward accumulation; the pass
+    // applying reflector kk also forms the partial dots v_{kk-1}^T Q
+    {
+        double acc[KM + 1];
+#pragma unroll
+        for (int j = 0; j <= KM; ++j) acc[j] = 0.0;
+        const int kk = n - 1;
+        for (uint64_t i = r0 + tid; i < r1; i += nt) {
+            const double vi = (i >= (uint64_t)kk) ? refl[(uint64_t)kk * m + i] : 0.0;
+#pragma unroll
+            for (int j = 0; j < KM; ++j)
+                if (j < n) {
+                    const double e = (i == (uint64_t)j) ? 1.0 : 0.0;
+                    q[i * n + j] = e;
+                    if (j >= kk) acc[j] += vi * e;
+                }
+        }
+        par ^= 1;
+        hh_cta_partials<KM>(acc, n, red_w, slot(par));
     }
+    hh_grid_sync(ctl, gen);
+    for (int kk = n - 1; kk >= 0; --kk) {
+        hh_reduce_all(slots(par), n, T);
+        for (int j = kk + (int)tid; j < n; j += nt) dots[j] = betas[kk] * T[j];
+        __syncthreads();
+        double acc[KM + 1];
+#pragma unroll
+        for (int j = 0; j <= KM; ++j) acc[j] = 0.0;
+        const bool apply = betas[kk] != 0.0;
+        const int kn = kk - 1;
+        const uint64_t lo = kn >= 0 ? (uint64_t)kn : (uint64_t)kk;
+        for (uint64_t i = (r0 > lo ? r0 : lo) + tid; i < r1; i += nt) {
+            double row[KM];
+#pragma unroll
+            for (int j = 0; j < KM; ++j) row[j] = (j < n) ? q[i * n + j] : 0.0;
+            if (apply && i >= (uint64_t)kk) {
+                const double v = refl[(uint64_t)kk * m + i];
+#pragma unroll
+                for (int j = 0; j < KM; ++j)
+                    if (j >= kk && j < n) {
+                        row[j] -= dots[j] * v;
+                        q[i * n + j] = row[j];
+                    }
+            }
+            if (kn >= 0) {
+                const double vn = refl[(uint64_t)kn * m + i];
+#pragma unroll
+                for (int j = 0; j < KM; ++j)
+                    if (j >= kn && j < n) acc[j] += vn * row[j];
+            }
+        }
+        par ^= 1;
+        hh_cta_partials<KM>(acc, n, red_w, slot(par));
+        hh_grid_sync(ctl, gen);
+    }
+    // R_kk >= 0: flip the columns whose alpha was negative
+    for (uint64_t i = r0 + tid; i < r1; i += nt)
+        for (int j = 0; j < n; ++j)
+            if (flip[j]) q[i * n + j] = -q[i * n + j];
 }
 
 __global__ void k_gt(const double* __restrict__ core, ModeShape sh, int order, const int* __restrict__ dranks_unused,
@@ -257,21 +453,35 @@ void launch_gram(const double* A, uint64_t rows, int K, double* wpart, double* m
 }
 
 void launch_chol1(const double* w, const double* maxv, int K, double* r1inv, DevStatus* st, int degenerate_mode,
-                  cudaStream_t s, bool abort_on_fallback) {
-    k_chol1<<<1, 32, 0, s>>>(w, maxv, K, r1inv, st, degenerate_mode, abort_on_fallback ? 1 : 0);
+                  uint64_t m_rows, cudaStream_t s, bool abort_on_fallback) {
+    k_chol1<<<1, 32, 0, s>>>(w, maxv, K, r1inv, st, degenerate_mode, abort_on_fallback ? 1 : 0, m_rows);
     HQ_CHECK_LAUNCH();
 }
 
-void launch_gram2(const double* A, uint64_t rows, int K, const double* r1inv, double* wpart, const DevStatus* st,
-                  cudaStream_t s) {
-    launch_rowgemm(K, A, rows, r1inv, nullptr, nullptr, wpart, nullptr, st, kOnlyCholQR, s);
+void launch_gram2(const double* A, uint64_t rows, int K, const double* r1inv, double* q_out, double* wpart,
+                  const DevStatus* st, cudaStream_t s) {
+    launch_rowgemm(K, A, rows, r1inv, q_out, nullptr, wpart, nullptr, st, kOnlyCholQR, s);
 }
 
-void launch_chol2(const double* wpart, int nslots, int K, const double* r1inv, double* rinv, const double* m,
-                  const ModeShape* sh, double* core_out, DevStatus* st, cudaStream_t s, bool abort_on_fallback) {
+void launch_chol2(const double* wpart, int nslots, int K, const double* r1inv, double* rinv, double* rc,
+                  const double* m, const ModeShape* sh, double* core_out, DevStatus* st, cudaStream_t s,
+                  bool abort_on_fallback) {
     ModeShape z{};
-    k_chol2<<<1, 1024, 0, s>>>(wpart, nslots, K, r1inv, rinv, m, sh ? *sh : z, m != nullptr, core_out, st,
-                               abort_on_fallback ? 1 : 0);
+    k_chol2<<<1, 1024, 0, s>>>(wpart, nslots, K, r1inv, rinv, rc, m, sh ? *sh : z, m != nullptr, core_out, st,
+                               abort_on_fallback ? 1 : 0, 2, nullptr);
+    HQ_CHECK_LAUNCH();
+}
+
+void launch_gram3(double* q, uint64_t rows, int K, const double* r2inv, double* wpart, const DevStatus* st,
+                  cudaStream_t s) {
+    launch_rowgemm(K, q, rows, r2inv, q, nullptr, wpart, nullptr, st, kOnlyShifted, s);
+}
+
+void launch_chol3(const double* wpart, int nslots, int K, const double* rc, double* rinv, const double* wfull,
+                  DevStatus* st, cudaStream_t s, bool abort_on_fallback) {
+    ModeShape z{};
+    k_chol2<<<1, 1024, 0, s>>>(wpart, nslots, K, rc, rinv, nullptr, nullptr, z, 0, nullptr, st,
+                               abort_on_fallback ? 1 : 0, 3, wfull);
     HQ_CHECK_LAUNCH();
 }
 
@@ -311,9 +521,30 @@ void launch_drift_batch(const double* trp, int pairs, int order, const int* rank
     HQ_CHECK_LAUNCH();
 }
 
-void launch_householder(const double* A, uint64_t rows, int K, double* q_out, double* work, const DevStatus* st,
-                        int run_if, cudaStream_t s) {
-    k_householder<<<1, kHhThreads, 0, s>>>(A, rows, K, q_out, work, st, run_if);
+size_t householder_work_doubles(uint64_t rows, int K) {
+    return kHhCtlDoubles + hh_part_doubles(num_sms()) + 2 * rows * (uint64_t)K;
+}
+
+void householder_reset(double* work, cudaStream_t s) { HQ_CUDA(cudaMemsetAsync(work, 0, sizeof(HhCtl), s)); }
+
+void launch_householder(const double* A, uint64_t rows, int K, double* q_out, double* work, const double* table,
+                        uint64_t table_len, const DevStatus* st, int run_if, cudaStream_t s) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)num_sms());
+    cfg.blockDim = dim3(kHhThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (K <= 8)
+        HQ_CUDA(cudaLaunchKernelEx(&cfg, k_householder_mc<8>, A, rows, K, q_out, work, table, table_len, st, run_if));
+    else if (K <= 16)
+        HQ_CUDA(cudaLaunchKernelEx(&cfg, k_householder_mc<16>, A, rows, K, q_out, work, table, table_len, st, run_if));
+    else
+        HQ_CUDA(cudaLaunchKernelEx(&cfg, k_householder_mc<32>, A, rows, K, q_out, work, table, table_len, st, run_if));
     HQ_CHECK_LAUNCH();
 }
 

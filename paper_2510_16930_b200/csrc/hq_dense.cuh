@@ -1,6 +1,8 @@
 // hq_dense.cuh — tall-skinny orthogonalisation and the K x K steps.
 #pragma once
 
+#include <memory>
+
 #include "hq_plan.cuh"
 
 namespace hq {
@@ -39,17 +41,26 @@ void launch_gram(const double* A, uint64_t rows, int K, double* wpart, double* m
 // degenerate_mode > 0), Cholesky of W, inverse of R1; sets st->fallback when
 // CholeskyQR2 would lose accuracy
 void launch_chol1(const double* w, const double* maxv, int K, double* r1inv, DevStatus* st, int degenerate_mode,
-                  cudaStream_t s, bool abort_on_fallback = false);
-// W2 partials of (A R1^-1)^T (A R1^-1)
-void launch_gram2(const double* A, uint64_t rows, int K, const double* r1inv, double* wpart, const DevStatus* st,
-                  cudaStream_t s);
-// Cholesky of W2 (reduced from partials), Rinv = R1inv R2inv; if m != null,
-// G_(n) = Rinv^T M refolded into the core layout (core_out)
-void launch_chol2(const double* wpart, int nslots, int K, const double* r1inv, double* rinv, const double* m,
-                  const ModeShape* sh, double* core_out, DevStatus* st, cudaStream_t s,
+                  uint64_t m_rows, cudaStream_t s, bool abort_on_fallback = false);
+// Q1 = A R1^-1 written to q_out, and the partials of W2 = Q1^T Q1
+void launch_gram2(const double* A, uint64_t rows, int K, const double* r1inv, double* q_out, double* wpart,
+                  const DevStatus* st, cudaStream_t s);
+// Cholesky of W2 (reduced from partials): rinv = R2^-1, rc = R1^-1 R2^-1; if
+// m != null and the update is not shifted, G_(n) = rc^T M refolded into the
+// core layout (core_out)
+void launch_chol2(const double* wpart, int nslots, int K, const double* r1inv, double* rinv, double* rc,
+                  const double* m, const ModeShape* sh, double* core_out, DevStatus* st, cudaStream_t s,
                   bool abort_on_fallback = false);
-// U = A Rinv (written to u_out when non-null); P partials of U^T U_old when
-// u_old non-null.  apply=false: U read from u_out (fallback drift).
+// shifted CholeskyQR3 third pass (RunIf kOnlyShifted): Q2 = Q1 R2^-1 in place
+// and the partials of W3 = Q2^T Q2; then rinv = R3^-1 with the identity and
+// rank checks (rc = R1^-1 R2^-1 for diag R, wfull = A^T A for ||A||_F)
+void launch_gram3(double* q, uint64_t rows, int K, const double* r2inv, double* wpart, const DevStatus* st,
+                  cudaStream_t s);
+void launch_chol3(const double* wpart, int nslots, int K, const double* rc, double* rinv, const double* wfull,
+                  DevStatus* st, cudaStream_t s, bool abort_on_fallback = false);
+// U = A Rinv (written to u_out when non-null, which may alias A); P partials
+// of U^T U_old when u_old non-null.  apply=false: U read from u_out (fallback
+// drift).
 void launch_apply(const double* A, uint64_t rows, int K, const double* rinv, double* u_out, const double* u_old,
                   double* ppart, bool apply, const DevStatus* st, int run_if, cudaStream_t s);
 // drift = max(2K - 2 ||P||_*, 0) (manifold.cpp:55-60) from P partials; when
@@ -73,11 +84,27 @@ void launch_sweep_end(const double* core, uint64_t core_size, double dns, double
 // drifts of `pairs` (sweep, mode) trace slots; ranks: device array of the N ranks
 void launch_drift_batch(const double* trp, int pairs, int order, const int* ranks_dev, int kmax, double* drift,
                         cudaStream_t s);
-// Householder QR following dense_core.cpp:127-198 exactly (single CTA), with
-// the seeded rank-deficiency fill generated on the device (MT19937-64 +
-// Box-Muller, rng.hpp:13-35, seed 0x48514F5251).
-void launch_householder(const double* A, uint64_t rows, int K, double* q_out, double* work, const DevStatus* st,
-                        int run_if, cudaStream_t s);
+// Householder QR following dense_core.cpp:127-198 step for step, one CTA per
+// SM with grid barriers (cooperative launch).  The rank-deficiency fill
+// (rng.hpp:13-35, seed 0x48514F5251) reads the precomputed normal stream
+// `table` (table_len normals; see fill_table) and falls back to drawing on the
+// device when the table is absent or too short.  work: householder_work_doubles
+// doubles (any rows x K up to the size it was made for), its control block
+// zeroed once by householder_reset (barrier counters reset themselves).
+size_t householder_work_doubles(uint64_t rows, int K);
+void householder_reset(double* work, cudaStream_t s);
+void launch_householder(const double* A, uint64_t rows, int K, double* q_out, double* work, const double* table,
+                        uint64_t table_len, const DevStatus* st, int run_if, cudaStream_t s);
+// the fill stream: the first `count` normals of tucker::Rng(0x48514F5251)
+// (rng.hpp:13-35), generated on the host once per process (per device) and
+// kept on the device; a holder keeps its table alive (graphs capture the
+// pointer).  Null when count exceeds kFillTableCap.
+struct FillTable {
+    DBuf<double> buf;
+    uint64_t len = 0;
+};
+constexpr uint64_t kFillTableCap = 1ull << 28;
+std::shared_ptr<const FillTable> fill_table(uint64_t count);
 // G_(n)^T (L x K_n) from the core
 void launch_gt(const double* core, const ModeShape& sh, const int* ranks, double* gt, const DevStatus* st,
                cudaStream_t s);

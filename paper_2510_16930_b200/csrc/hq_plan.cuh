@@ -22,8 +22,11 @@ void build_tensor(DeviceTensor& T, int order, const uint64_t* dims, uint64_t nnz
 void export_buckets(const DeviceTensor& T, int mode, uint64_t* offsets, uint64_t* entries, cudaStream_t s);
 
 // Device status word shared by every kernel of a solve.  Kernels return early
-// when `abort` is set; the CholeskyQR2 kernels run only while `fallback` is 0,
-// the Householder fallback kernels only while it is 1.
+// when `abort` is set; the CholeskyQR kernels run only while `fallback` is 0,
+// the Householder fallback kernels only while it is 1.  `shifted` marks a
+// mode update whose Gram matrix was too ill-conditioned for plain CholeskyQR2:
+// it runs shifted CholeskyQR3 (a third Gram pass) and recomputes the core with
+// a sparse pass instead of R^-T M.
 struct DevStatus {
     int abort;
     int degenerate_mode;   // 1-based mode of the first A == 0 (solvers.cpp:124)
@@ -31,15 +34,19 @@ struct DevStatus {
     int fallback;          // current QR needs the Householder path
     unsigned int fallback_count;
     int sweep;             // 1-based sweep counter (advanced on the device)
+    int shifted;           // current QR runs shifted CholeskyQR3
+    unsigned int shifted_count;
 };
 
-enum RunIf { kAlways = 0, kOnlyFallback = 1, kOnlyCholQR = 2 };
+enum RunIf { kAlways = 0, kOnlyFallback = 1, kOnlyCholQR = 2, kOnlyShifted = 3, kFallbackOrShifted = 4 };
 
 __device__ __forceinline__ bool skip_kernel(const DevStatus* st, int run_if) {
     if (!st) return false;
     if (st->abort) return true;
     if (run_if == kOnlyFallback) return st->fallback == 0;
     if (run_if == kOnlyCholQR) return st->fallback != 0;
+    if (run_if == kOnlyShifted) return st->fallback != 0 || st->shifted == 0;
+    if (run_if == kFallbackOrShifted) return st->fallback == 0 && st->shifted == 0;
     return false;
 }
 

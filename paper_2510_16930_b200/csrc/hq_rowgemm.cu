@@ -3,7 +3,8 @@
 //
 // One kernel covers every dense I_n x K pass of a mode update:
 //   X = A T        (T = R1^-1, R^-1, or the identity)
-//   out <- X       (optional: the new factor U_new = A R^-1)
+//   out <- X       (optional; may alias A: each warp reads a row group before
+//                   writing it and owns its groups, so in-place is safe)
 //   part[c] += X^T Y over the CTA's rows, Y = X (Gram) or another matrix
 //              (U_old, for the drift product P = U_new^T U_old)
 //   max|A|         (optional)
@@ -38,7 +39,7 @@ struct RG {
 
 template <int K>
 __global__ void __launch_bounds__(kRgWarps * 32)
-    k_rowgemm(const double* __restrict__ A, uint64_t rows, const double* __restrict__ T, double* __restrict__ out,
+    k_rowgemm(const double* A, uint64_t rows, const double* __restrict__ T, double* out,
               const double* __restrict__ other, double* __restrict__ part, double* __restrict__ maxpart,
               const DevStatus* st, int run_if) {
     using C = RG<K>;

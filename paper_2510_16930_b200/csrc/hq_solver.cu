@@ -25,6 +25,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <map>
+#include <mutex>
+#include <vector>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -97,9 +99,34 @@ void gaussian_stream(uint64_t seed, uint64_t count, double* out) {
     for (auto& t : th) t.join();
 }
 
+}  // namespace
+
+std::shared_ptr<const FillTable> fill_table(uint64_t count) {
+    if (count == 0 || count > kFillTableCap) return nullptr;
+    static std::mutex mu;
+    static std::map<int, std::shared_ptr<FillTable>> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    int dev = 0;
+    HQ_CUDA(cudaGetDevice(&dev));
+    auto& t = cache[dev];
+    if (!t || t->len < count) {
+        const uint64_t len = std::min<uint64_t>(kFillTableCap, std::max<uint64_t>(count, t ? 2 * t->len : 0));
+        std::vector<double> h(len);
+        gaussian_stream(0x48514F5251ull, len, h.data());
+        auto nt = std::make_shared<FillTable>();
+        nt->buf.alloc(len);
+        HQ_CUDA(cudaMemcpy(nt->buf.get(), h.data(), sizeof(double) * len, cudaMemcpyHostToDevice));
+        nt->len = len;
+        t = nt;  // holders of the previous table keep it alive
+    }
+    return t;
+}
+
+namespace {
+
 // ---------------------------------------------------------------- QR -----
 struct QrWork {
-    DBuf<double> wpart, maxpart, w, maxv, r1inv, rinv, ppart, hh;
+    DBuf<double> wpart, maxpart, w, maxv, r1inv, rinv, rc, ppart, hh;
     DBuf<DevStatus> st;
     void ensure(uint64_t rows, int K) {
         size_t sl = dense_slots();
@@ -109,8 +136,14 @@ struct QrWork {
         if (w.n < (size_t)K * K) w.alloc(K * K);
         if (r1inv.n < (size_t)K * K) r1inv.alloc(K * K);
         if (rinv.n < (size_t)K * K) rinv.alloc(K * K);
+        if (rc.n < (size_t)K * K) rc.alloc(K * K);
         if (!maxv.n) maxv.alloc(1);
-        if (hh.n < 2 * rows * K + 8) hh.alloc(2 * rows * K + 8);
+        const size_t hw = householder_work_doubles(rows, K);
+        if (hh.n < hw) {
+            hh.alloc(hw);
+            householder_reset(hh.get(), 0);
+            HQ_CUDA(cudaDeviceSynchronize());
+        }
         if (!st.n) st.alloc(1);
     }
 };
@@ -124,11 +157,22 @@ void qr_device(const double* A, uint64_t rows, int K, double* Q, QrWork& w, cuda
     launch_gram(A, rows, K, w.wpart.get(), w.maxpart.get(), st, kAlways, s);
     launch_reduce_pass(nullptr, 0, w.wpart.get(), K * K, w.maxpart.get(), dense_slots(), nullptr, w.w.get(),
                        w.maxv.get(), st, kAlways, s);
-    launch_chol1(w.w.get(), w.maxv.get(), K, w.r1inv.get(), st, 0, s);
-    launch_gram2(A, rows, K, w.r1inv.get(), w.wpart.get(), st, s);
-    launch_chol2(w.wpart.get(), dense_slots(), K, w.r1inv.get(), w.rinv.get(), nullptr, nullptr, nullptr, st, s);
-    launch_apply(A, rows, K, w.rinv.get(), Q, nullptr, nullptr, true, st, kOnlyCholQR, s);
-    launch_householder(A, rows, K, Q, w.hh.get(), st, kOnlyFallback, s);
+    launch_chol1(w.w.get(), w.maxv.get(), K, w.r1inv.get(), st, 0, rows, s);
+    launch_gram2(A, rows, K, w.r1inv.get(), Q, w.wpart.get(), st, s);  // Q <- Q1
+    launch_chol2(w.wpart.get(), dense_slots(), K, w.r1inv.get(), w.rinv.get(), w.rc.get(), nullptr, nullptr, nullptr,
+                 st, s);
+    launch_gram3(Q, rows, K, w.rinv.get(), w.wpart.get(), st, s);  // shifted: Q <- Q2
+    launch_chol3(w.wpart.get(), dense_slots(), K, w.rc.get(), w.rinv.get(), w.w.get(), st, s);
+    launch_apply(Q, rows, K, w.rinv.get(), Q, nullptr, nullptr, true, st, kOnlyCholQR, s);
+    DevStatus h{};
+    HQ_CUDA(cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaStreamSynchronize(s));
+    if (h.fallback) {  // Householder with the reference's fill (its normal stream built only when needed)
+        auto table = fill_table(rows * (uint64_t)K);
+        launch_householder(A, rows, K, Q, w.hh.get(), table ? table->buf.get() : nullptr, table ? table->len : 0, st,
+                           kOnlyFallback, s);
+        HQ_CUDA(cudaStreamSynchronize(s));
+    }
 }
 
 void check_rank_limits(int K) {
@@ -150,7 +194,7 @@ struct Solver {
     double initial_objective = 0.0;
 
     DBuf<double> U[kMaxOrder][2];
-    DBuf<double> core, gt, A, mpart, wpart, maxpart, ypart, mred, wred, maxv, r1inv, rinv, w2part, hh;
+    DBuf<double> core, gt, A, mpart, wpart, maxpart, ypart, mred, wred, maxv, r1inv, rinv, rc, w2part, hh;
     DBuf<double> ppart[kMaxOrder];  // per-mode drift products (their drift kernels run on the side stream)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork[kMaxOrder] = {nullptr};
@@ -163,6 +207,8 @@ struct Solver {
     const Comm* comm = nullptr;
     std::vector<uint64_t> bnd[kMaxOrder];
     DBuf<double> w2red, pred;  // all-reduced K x K Gram / drift product (distributed path)
+    DBuf<double> core_alt;     // conditional core recompute (distributed path)
+    std::shared_ptr<const FillTable> fill;  // Householder fill stream (rank-deficient QR)
     uint64_t rb(int n) const { return comm ? bnd[n][comm->rank] : 0; }
     uint64_t re(int n) const { return comm ? bnd[n][comm->rank + 1] : dims[n]; }
     DBuf<DevStatus> st;
@@ -252,10 +298,19 @@ struct Solver {
         maxv.alloc(1);
         r1inv.alloc(kmax * kmax);
         rinv.alloc(kmax * kmax);
+        rc.alloc(kmax * kmax);
         w2part.alloc((size_t)dense_slots() * kmax * kmax);
         for (int v = 0; v < N; ++v) ppart[v].alloc((size_t)dense_slots() * ranks[v] * ranks[v]);
-        hh.alloc(2 * maxIK + 8);
+        {
+            size_t hw = 0;
+            for (int v = 0; v < N; ++v) hw = std::max(hw, householder_work_doubles(dims[v], ranks[v]));
+            hh.alloc(hw);
+            householder_reset(hh.get(), s);
+            // the reference's fill stream for the largest Householder this solve can run
+            fill = fill_table(maxIK);
+        }
         w2red.alloc(kmax * kmax);
+        if (comm) core_alt.alloc(core_size);
         pred.alloc(kmax * kmax);
         if (comm) {
             for (int v = 0; v < N; ++v) {
@@ -313,6 +368,11 @@ struct Solver {
     }
 
     // core = X x {U^T} with the parity-p factors, via the mode-0 pass
+    // core = X x {U^T} by a kCore sparse pass over mode 0 (setup; after a
+    // Householder fallback or a shifted CholeskyQR3 update, where R^-T M would
+    // carry the Gram matrix's conditioning into the core).  Multi-GPU: the
+    // all-reduce runs unconditionally in the captured graph, so a conditional
+    // recompute goes through core_alt and is copied into place only when it ran.
     void compute_core(int p, int run_if, int updated_mode = -1) {
         FactorPtrs f{};
         for (int v = 0; v < N; ++v) {
@@ -321,8 +381,15 @@ struct Solver {
             f.k[v] = ranks[v];
         }
         launch_pass(*T, 0, sh[0], f, kCore, nullptr, pass_out(nullptr), st.get(), run_if, s, rb(0), re(0));
-        launch_reduce_core(mpart.get(), pass_slots(T->modes[0], sh[0]), core_size, core.get(), st.get(), run_if, s);
-        if (comm && run_if != kOnlyFallback) comm->allreduce_sum(core.get(), core_size, s);
+        const int slots = pass_slots(T->modes[0], sh[0]);
+        if (comm && run_if != kAlways) {
+            launch_reduce_core(mpart.get(), slots, core_size, core_alt.get(), st.get(), run_if, s);
+            comm->allreduce_sum(core_alt.get(), core_size, s);
+            launch_reduce_core(core_alt.get(), 1, core_size, core.get(), st.get(), run_if, s);
+        } else {
+            launch_reduce_core(mpart.get(), slots, core_size, core.get(), st.get(), run_if, s);
+            if (comm) comm->allreduce_sum(core.get(), core_size, s);
+        }
     }
 
     void mode_update(int n, int p) {
@@ -344,7 +411,7 @@ struct Solver {
             comm->allreduce_sum(wred.get(), (size_t)K * K, s);
             comm->allreduce_max(maxv.get(), 1, s);
         }
-        launch_chol1(wred.get(), maxv.get(), K, r1inv.get(), S, n + 1, s, comm != nullptr);
+        launch_chol1(wred.get(), maxv.get(), K, r1inv.get(), S, n + 1, dims[n], s, comm != nullptr);
         mark("chol1");
         const double* a_loc = A.get() + r0 * K;
         double* unew = U[n][1 - p].get();
@@ -352,24 +419,37 @@ struct Solver {
         double* pp = ppart[n].get();
         int pslots = dense_slots();
         if (!comm) {
-            launch_gram2(a_loc, lrows, K, r1inv.get(), w2part.get(), S, s);
+            launch_gram2(a_loc, lrows, K, r1inv.get(), unew, w2part.get(), S, s);  // U_new <- Q1
             mark("gram2");
-            launch_chol2(w2part.get(), dense_slots(), K, r1inv.get(), rinv.get(), mred.get(), &m, core.get(), S, s);
+            launch_chol2(w2part.get(), dense_slots(), K, r1inv.get(), rinv.get(), rc.get(), mred.get(), &m, core.get(),
+                         S, s);
             mark("chol2");
-            launch_apply(a_loc, lrows, K, rinv.get(), unew, uold, pp, true, S, kOnlyCholQR, s);
+            // shifted CholeskyQR3 branch (device flag): U_new <- Q2, R3
+            launch_gram3(unew, lrows, K, rinv.get(), w2part.get(), S, s);
+            launch_chol3(w2part.get(), dense_slots(), K, rc.get(), rinv.get(), wred.get(), S, s);
+            mark("cholqr3(no-op)");
+            launch_apply(unew, lrows, K, rinv.get(), unew, uold, pp, true, S, kOnlyCholQR, s);
             mark("apply");
             // Householder branch (device flag)
-            launch_householder(A.get(), dims[n], K, unew, hh.get(), S, kOnlyFallback, s);
+            launch_householder(A.get(), dims[n], K, unew, hh.get(), fill ? fill->buf.get() : nullptr,
+                               fill ? fill->len : 0, S, kOnlyFallback, s);
             launch_apply(nullptr, dims[n], K, nullptr, unew, uold, pp, false, S, kOnlyFallback, s);
-            compute_core(p, kOnlyFallback, n);
+            compute_core(p, kFallbackOrShifted, n);
             mark("fallback(no-op)");
         } else {
-            launch_gram2(a_loc, lrows, K, r1inv.get(), w2part.get(), S, s);
+            double* uloc = unew + r0 * K;
+            launch_gram2(a_loc, lrows, K, r1inv.get(), uloc, w2part.get(), S, s);
             launch_reduce_pass(nullptr, 0, w2part.get(), K * K, nullptr, dense_slots(), nullptr, w2red.get(), nullptr, S,
                                kOnlyCholQR, s);
             comm->allreduce_sum(w2red.get(), (size_t)K * K, s);
-            launch_chol2(w2red.get(), 1, K, r1inv.get(), rinv.get(), mred.get(), &m, core.get(), S, s, true);
-            launch_apply(a_loc, lrows, K, rinv.get(), unew + r0 * K, uold + r0 * K, pp, true, S, kOnlyCholQR, s);
+            launch_chol2(w2red.get(), 1, K, r1inv.get(), rinv.get(), rc.get(), mred.get(), &m, core.get(), S, s, true);
+            // shifted CholeskyQR3 (device flag; the all-reduce always runs, on stale data when skipped)
+            launch_gram3(uloc, lrows, K, rinv.get(), w2part.get(), S, s);
+            launch_reduce_pass(nullptr, 0, w2part.get(), K * K, nullptr, dense_slots(), nullptr, w2red.get(), nullptr, S,
+                               kOnlyShifted, s);
+            comm->allreduce_sum(w2red.get(), (size_t)K * K, s);
+            launch_chol3(w2red.get(), 1, K, rc.get(), rinv.get(), wred.get(), S, s, true);
+            launch_apply(uloc, lrows, K, rinv.get(), uloc, uold + r0 * K, pp, true, S, kOnlyCholQR, s);
             launch_reduce_pass(nullptr, 0, pp, K * K, nullptr, dense_slots(), nullptr, pred.get(), nullptr, S, kAlways,
                                s);
             comm->allreduce_sum(pred.get(), (size_t)K * K, s);
@@ -378,6 +458,7 @@ struct Solver {
             HQ_CUDA(cudaMemcpyAsync(ppart[n].get(), pred.get(), sizeof(double) * K * K, cudaMemcpyDeviceToDevice, s));
             pp = ppart[n].get();
             pslots = 1;
+            compute_core(p, kOnlyShifted, n);
         }
         // the drift feeds only the trace: P is stored beside the next mode update (side stream) and the
         // drifts are evaluated in one batch at download
@@ -399,10 +480,17 @@ struct Solver {
 
     int launches_per_sweep() const {
         int c = 0;
-        for (int n = 0; n < N; ++n)
-            c += 1 + pass_launch_count(T->modes[n], sh[n]) + 1 + 1 + 1 + 1 + 1 + 1 + 1 +
-                 pass_launch_count(T->modes[0], sh[0]) + 1 + 1;
-        return c;
+        const int core_pass = pass_launch_count(T->modes[0], sh[0]);
+        for (int n = 0; n < N; ++n) {
+            const int pass = pass_launch_count(T->modes[n], sh[n]);
+            if (!comm)  // gt, pass, reduce, chol1, gram2, chol2, gram3, chol3, apply, householder, apply-P,
+                        // core pass + reduce, store_p
+                c += 1 + pass + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + core_pass + 1 + 1;
+            else        // gt, pass, reduce, chol1, gram2, reduce, chol2, gram3, reduce, chol3, apply, reduce-P,
+                        // core pass + 2 reduces, store_p (NCCL kernels not counted)
+                c += 1 + pass + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + core_pass + 2 + 1;
+        }
+        return c + 1;  // sweep_end
     }
 
     void build_graphs() {
@@ -888,6 +976,17 @@ int hq_solver_launch_mode_pass(hq_solver* sv, int mode) {
 }
 
 int hq_solver_launch_ttmctc(hq_solver* sv, int mode) { return hq_solver_launch_mode_pass(sv, mode); }
+
+int hq_solver_status(hq_solver* s, int64_t* out) {
+    return guard([&] {
+        DevStatus h = s->impl->status();
+        out[0] = h.sweep;
+        out[1] = h.fallback_count;
+        out[2] = h.abort;
+        out[3] = h.degenerate_mode;
+        out[4] = h.shifted_count;
+    });
+}
 
 int hq_solver_launches_per_sweep(const hq_solver* s, uint64_t* out) {
     return guard([&] { *out = (uint64_t)s->impl->launches_per_sweep(); });

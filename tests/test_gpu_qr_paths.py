@@ -1,0 +1,74 @@
+"""GPU: the three orthogonalisation paths of a mode update against the
+reference's Householder QR (oracle restatement of dense_core.cpp:127-198).
+
+* plain CholeskyQR2 (well-conditioned A);
+* shifted CholeskyQR3 (kappa(A) beyond CholeskyQR2's reach, full rank);
+* the multi-CTA Householder with the reference's seeded rank-deficiency fill
+  (columns with |R_kk| <= 1e-12 ||A||_F), at sizes that span many CTAs.
+and a HOQRI solve whose later sweeps need the shifted / Householder paths
+(positive-valued data drives the core towards rank deficiency), checked
+per sweep against the oracle."""
+import numpy as np
+import pytest
+
+import paper_2510_16930_b200 as hq
+from paper_2510_16930_b200.workloads import uniform_coo
+
+pytestmark = pytest.mark.gpu
+
+
+def _graded(m, k, cond, seed):
+    rng = np.random.default_rng(seed)
+    u, _ = np.linalg.qr(rng.standard_normal((m, k)))
+    v, _ = np.linalg.qr(rng.standard_normal((k, k)))
+    s = np.logspace(0, -np.log10(cond), k)
+    return (u * s) @ v.T
+
+
+@pytest.mark.parametrize("cond", [1e3, 1e7, 1e10, 1e13])
+def test_qr_conditioning_paths_match_householder(oracle, cond):
+    m, k = 120000, 10
+    a = _graded(m, k, cond, 11)
+    q = hq.qr_orthonormal(a)
+    qo = oracle.qr(a)
+    assert np.abs(q.T @ q - np.eye(k)).max() <= 1e-13
+    # both are backward-stable QRs with R_kk >= 0: Q agrees to O(kappa u)
+    assert np.abs(q - qo).max() <= max(1e-12, 50 * cond * 1.1e-16)
+    # column space identical to rounding
+    assert np.linalg.norm(a - q @ (q.T @ a)) <= 1e-13 * np.linalg.norm(a) * max(1.0, cond * 1e-6)
+
+
+@pytest.mark.parametrize("m,k,dead", [(200000, 10, [3, 7]), (150001, 16, [0]), (90000, 8, [2, 3, 4]), (70000, 24, [23])])
+def test_householder_fill_large_matches_reference(oracle, m, k, dead):
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((m, k))
+    for d in dead:  # column d a combination of the previous ones (or zero)
+        a[:, d] = a[:, :d] @ rng.standard_normal(d) if d else 0.0
+    q = hq.qr_orthonormal(a)
+    qo = oracle.qr(a)
+    assert np.abs(q.T @ q - np.eye(k)).max() <= 1e-12
+    # the filled columns come from the same seeded stream: the whole Q matches
+    assert np.abs(q - qo).max() <= 1e-9
+    assert (q == hq.qr_orthonormal(a)).all()  # deterministic
+
+
+def test_zero_matrix_fills_every_column(oracle):
+    a = np.zeros((50000, 6))
+    q = hq.qr_orthonormal(a)
+    np.testing.assert_allclose(q, oracle.qr(a), atol=1e-12)
+
+
+def test_hoqri_ill_conditioned_sweeps_match_oracle(oracle):
+    dims, k = [5000, 5000, 5000], 10
+    coords, vals = uniform_coo(dims, 50000, 3)
+    x = hq.SparseTensor(dims, coords, vals)
+    u = hq.random_factors(dims, [k] * 3, 4)
+    sweeps = 20
+    sol = hq.Solver(x, hq.SolverConfig(ranks=[k] * 3, max_sweeps=sweeps, tol_fit_change=0.0), init_factors=u.factors)
+    sol.run(sweeps)
+    sol.sync()
+    st = sol.status()
+    assert st["shifted"] > 0  # the case exercises shifted CholeskyQR3
+    r = sol.download()
+    ref = oracle.hoqri(dims, [k] * 3, x.coords(), x.values(), u.factors, sweeps)
+    np.testing.assert_allclose([s.objective for s in r.trace.sweeps], ref["objective"], rtol=1e-9)

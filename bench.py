@@ -337,11 +337,16 @@ def run_engine(args, ws, rank, local):
         sweeps = c["sweeps"]
         ecfg = hq.SolverConfig(ranks=ranks, max_sweeps=sweeps, tol_fit_change=0.0)
 
+        # page-locked result buffers, like the inputs (the D2H is a DMA either way)
+        po = [torch.empty((d, k), dtype=torch.float64).pin_memory() for d, k in zip(dims, ranks)]
+        pcore = torch.empty(int(np.prod(ranks)), dtype=torch.float64).pin_memory()
+        hout = ([t.numpy() for t in po], pcore.numpy())
+
         def e2e_step():
             xe = hq.SparseTensor(dims, hc, hv)  # H2D of the COO + device layout build
             se = hq.Solver(xe, ecfg, init_factors=hu, stream=stream.cuda_stream, comm=comm)  # H2D of the factors
             se.run(sweeps)
-            r = se.download()  # D2H of factors, core, trace
+            r = se.download(out=hout)  # D2H of factors, core, trace
             del se, xe
             return r
 

@@ -646,9 +646,21 @@ class Solver:
         _check(load_library().hq_solver_ttmctc_work(self._h, mode, C.byref(f), C.byref(b)))
         return f.value, b.value
 
-    def download(self):
-        fs = [np.empty((self.x.dims()[v], int(self.config.ranks[v])), np.float64) for v in range(self.n)]
-        core = np.empty(int(np.prod(self.config.ranks)), np.float64)
+    def download(self, out=None):
+        """Factors, core and trace to the host.  `out` = (factor arrays, core array) lets the caller supply
+        (e.g. page-locked) C-contiguous float64 destinations of the right shapes."""
+        if out is None:
+            fs = [np.empty((self.x.dims()[v], int(self.config.ranks[v])), np.float64) for v in range(self.n)]
+            core = np.empty(int(np.prod(self.config.ranks)), np.float64)
+        else:
+            fs, core = list(out[0]), out[1]
+            for v, f in enumerate(fs):
+                if (f.dtype != np.float64 or not f.flags.c_contiguous
+                        or f.shape != (self.x.dims()[v], int(self.config.ranks[v]))):
+                    raise ShapeError(f"download: factor {v} destination has the wrong shape/dtype/layout")
+            if core.dtype != np.float64 or not core.flags.c_contiguous or core.size != int(np.prod(self.config.ranks)):
+                raise ShapeError("download: core destination has the wrong size/dtype/layout")
+            core = core.reshape(-1)
         tb = _TraceBuffers(int(self.config.max_sweeps), self.n)
         _check(load_library().hq_solver_download(self._h, _ptr_array(fs), core.ctypes.data, C.byref(tb.c)))
         trace = tb.to_trace(self.n)

@@ -37,6 +37,24 @@ struct Error : std::runtime_error {
 
 // ---------------------------------------------------------------- memory --
 // RAII device buffer (stream-ordered allocation).
+// Device buffers come from the device's stream-ordered memory pool with a
+// high release threshold: a solve's buffers freed by one solver are re-used
+// by the next without unmapping / remapping (cudaMalloc / cudaFree cost
+// milliseconds per large buffer in an end-to-end solve).
+inline void device_pool_init() {
+    static int once = [] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = 64ull << 30;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        return 0;
+    }();
+    (void)once;
+}
+
 template <class T>
 struct DBuf {
     T* p = nullptr;
@@ -53,10 +71,18 @@ struct DBuf {
     void alloc(size_t count) {
         release();
         n = count;
-        if (count) HQ_CUDA(cudaMalloc(&p, sizeof(T) * count));
+        if (count) {
+            device_pool_init();
+            HQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, 0));
+            HQ_CUDA(cudaStreamSynchronize(0));  // usable from every stream
+        }
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) {
+            cudaDeviceSynchronize();  // like cudaFree: no pending work may still use it
+            cudaFreeAsync(p, 0);
+            cudaStreamSynchronize(0);
+        }
         p = nullptr;
         n = 0;
     }

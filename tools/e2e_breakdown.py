@@ -17,6 +17,8 @@ u0 = hq.random_factors(dims, ranks, 1)
 pu = [torch.from_numpy(np.ascontiguousarray(f)).pin_memory() for f in u0.factors]
 hc, hv, hu = pc.numpy(), pv.numpy(), [t.numpy() for t in pu]
 cfg = hq.SolverConfig(ranks=ranks, max_sweeps=c["sweeps"], tol_fit_change=0.0)
+po = [torch.empty((d, k), dtype=torch.float64).pin_memory().numpy() for d, k in zip(dims, ranks)]
+pcore = torch.empty(int(np.prod(ranks)), dtype=torch.float64).pin_memory().numpy()
 for it in range(3):
     t = [time.perf_counter()]
     x = hq.SparseTensor(dims, hc, hv); torch.cuda.synchronize(); t.append(time.perf_counter())
@@ -25,7 +27,7 @@ for it in range(3):
     st1 = sol.status()
     sol.run(c["sweeps"] - 1); sol.sync(); t.append(time.perf_counter())
     print("status after sweep 1:", st1, "after all:", sol.status())
-    r = sol.download(); t.append(time.perf_counter())
+    r = sol.download(out=(po, pcore)); t.append(time.perf_counter())
     del sol; torch.cuda.synchronize(); t.append(time.perf_counter())
     del x; torch.cuda.synchronize(); t.append(time.perf_counter())
     names = ["tensor", "solver", "sweep1", "sweeps", "download", "del_solver", "del_tensor"]

@@ -119,13 +119,17 @@ typedef struct hq_config {
     uint64_t seed;
     int init;                 /* 0 random, 2 = use init_factors */
     int kernel;               /* 0 element-wise, 1 matrix (same device path) */
-    int trace_gradients;      /* per-update diagnostics (ModeUpdateRecord) */
-    double tol_grad;          /* gradient stop, implies tracing */
+    int trace_gradients;      /* per-update diagnostics (ModeUpdateRecord), on the device */
+    double tol_grad;          /* gradient stop sqrt(sum grad) <= tol_grad f, implies tracing */
 } hq_config;
 
 void hq_config_default(hq_config* cfg);
 
-/* IterationTrace (solvers.hpp:37-63), caller-allocated for max_sweeps sweeps */
+/* IterationTrace (solvers.hpp:37-63), caller-allocated for max_sweeps sweeps.
+ * With trace_gradients (or tol_grad > 0) the per-update ModeUpdateRecords
+ * (solvers.hpp:40-49) are filled for update i = (sweep - 1) * order + mode:
+ * f_before / f_after / elapsed_s [max_sweeps * order], sigma / lambda
+ * [max_sweeps * order * sigma_stride] (first K_mode entries, descending). */
 typedef struct hq_trace {
     double data_norm_sq;
     double initial_objective;
@@ -133,8 +137,15 @@ typedef struct hq_trace {
     double* objective;         /* [max_sweeps] */
     double* fit;               /* [max_sweeps] */
     double* drift;             /* [max_sweeps * order] */
-    double* grad_norm_sq;      /* [max_sweeps * order] or NULL */
+    double* grad_norm_sq;      /* [max_sweeps * order] or NULL (zeros unless tracing) */
     double* elapsed_s;         /* [max_sweeps] or NULL: cumulative device time */
+    double* upd_f_before;      /* or NULL */
+    double* upd_f_after;       /* or NULL */
+    double* upd_elapsed_s;     /* or NULL: device time between successive updates' diagnostics points */
+    double* upd_sigma;         /* or NULL: singular values of A^(n) */
+    double* upd_lambda;        /* or NULL: eigenvalues of G_(n) G_(n)^T */
+    uint64_t sigma_stride;     /* caller: row stride of upd_sigma / upd_lambda (>= max rank) */
+    uint64_t updates;          /* filled: number of update records (0 unless tracing) */
 } hq_trace;
 
 /* hoqri (solvers.hpp:80; solvers.cpp:50-178, 217-219): the whole solve on the

@@ -189,6 +189,38 @@ def gen_hoqri(lib):
     np.savez_compressed(os.path.join(OUT, "hoqri.npz"), **out)
 
 
+def gen_grad(lib):
+    """Gradient tracing (trace_gradients / tol_grad, solvers.cpp:58, 126-150,
+    165-167) through tucker::hoqri with seeded random init: per-update
+    grad_norm_sq, f_before, f_after, sigma, lambda, and the sweep count."""
+    out, names = {}, []
+    for name, dims, nnz, tseed, ranks, sweeps, seed, tol_grad in (
+        ("g3", [20, 18, 16], 200, 41, [3, 3, 3], 12, 5, 0.0),
+        ("g4", [10, 9, 8, 7], 120, 44, [2, 3, 2, 2], 10, 17, 0.0),
+        ("gk", [60, 50, 40], 3000, 47, [10, 8, 6], 8, 9, 0.0),
+        ("gstop", [50, 50, 50], 500, 31, [5, 5, 5], 60, 8, 0.02),
+    ):
+        t = RefTensor.gen_synthetic(lib, dims, nnz, tseed)
+        c, v = t.export()
+        r = t.hoqri_traced(ranks, sweeps, 0.0, seed, tol_grad)
+        if r["status"]:
+            raise RuntimeError(f"{name}: reference status {r['status']}")
+        out[f"{name}_dims"] = np.asarray(dims, np.uint64)
+        out[f"{name}_ranks"] = np.asarray(ranks, np.uint64)
+        out[f"{name}_seed"] = np.array(seed, np.uint64)
+        out[f"{name}_max_sweeps"] = np.array(sweeps)
+        out[f"{name}_tol_grad"] = np.array(tol_grad)
+        out[f"{name}_coords"], out[f"{name}_vals"] = c, v
+        for k in ("sweeps", "objective", "fit", "grad", "updates", "f_before", "f_after", "sigma", "lambda_", "core"):
+            out[f"{name}_{k}"] = np.asarray(r[k])
+        u0 = ref_random_factors(lib, dims, ranks, seed)
+        for m in range(len(dims)):
+            out[f"{name}_U0_{m}"] = u0[m]
+        names.append(name)
+    out["names"] = np.array(names)
+    np.savez_compressed(os.path.join(OUT, "grad.npz"), **out)
+
+
 def gen_config1(lib):
     """BASELINE config 1 at full size: 10^4 cube, 10^5 uniform draws, U(0,1),
     rank 10^3, 20 sweeps.  Inputs come from workloads.uniform_coo(seed=1001);
@@ -223,6 +255,7 @@ def main():
     gen_kernels(lib)
     gen_qr(lib)
     gen_hoqri(lib)
+    gen_grad(lib)
     if "--skip-config1" not in sys.argv:
         gen_config1(lib)
     for f in sorted(os.listdir(OUT)):

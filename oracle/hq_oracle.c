@@ -26,6 +26,8 @@
 #define HQO_ERR_SHAPE 1
 #define HQO_ERR_RANGE 2
 #define HQO_ERR_VALUE 3
+#define HQO_ERR_CONTRACT 6
+#define HQO_ERR_DIAGNOSTIC 7
 #define HQO_ERR_DEGENERATE 8
 
 /* ------------------------------------------------------------------ RNG --
@@ -510,6 +512,100 @@ int hqo_random_factors(int N, const uint64_t* dims, const uint64_t* ranks, uint6
     return HQO_OK;
 }
 
+/* ------------------------------------------------- gradient diagnostics --
+ * unfold_core (dense_core.cpp:350-369): G_(n) is K_n x L, column
+ * sum_{v != n} k_v * stride_v with the last other mode fastest. */
+static void unfold_core(int N, const uint64_t* ranks, int n, const double* core, double* gn) {
+    uint64_t L = prod_ranks(N, ranks) / ranks[n];
+    uint64_t stride[16];
+    uint64_t sacc = 1;
+    for (int v = N - 1; v >= 0; --v) {
+        if (v == n) continue;
+        stride[v] = sacc;
+        sacc *= ranks[v];
+    }
+    uint64_t idx[16] = {0};
+    uint64_t size = prod_ranks(N, ranks);
+    for (uint64_t lin = 0; lin < size; ++lin) {
+        uint64_t col = 0;
+        for (int v = 0; v < N; ++v)
+            if (v != n) col += idx[v] * stride[v];
+        gn[idx[n] * L + col] = core[lin];
+        for (int v = N - 1; v >= 0; --v) {
+            if (++idx[v] < ranks[v]) break;
+            idx[v] = 0;
+        }
+    }
+}
+
+/* gram_eigvals_desc (dense_core.cpp:371-386); m is consumed.  Returns
+ * HQO_ERR_CONTRACT when not symmetric / not PSD. */
+static int gram_eigvals_desc(uint64_t k, double* m, double* ev) {
+    double fro = 0.0;
+    for (uint64_t i = 0; i < k * k; ++i) fro += m[i] * m[i];
+    double scale = sqrt(fro) > 1.0 ? sqrt(fro) : 1.0;
+    for (uint64_t i = 0; i < k; ++i)
+        for (uint64_t j = i + 1; j < k; ++j)
+            if (fabs(m[i * k + j] - m[j * k + i]) > 1e-10 * scale) return HQO_ERR_CONTRACT;
+    hqo_jacobi_eigvals(k, m, ev);
+    for (uint64_t i = 0; i < k; ++i) {
+        if (ev[i] < -1e-10 * scale) return HQO_ERR_CONTRACT;
+        if (ev[i] < 0.0) ev[i] = 0.0;
+    }
+    return HQO_OK;
+}
+
+/* diagnose_update (solvers.cpp:39-46) = grad_norm_sq (manifold.cpp:37-55) +
+ * interlacing_check (manifold.cpp:63-84) for A (m x k) and G_(n) (k x L). */
+int hqo_update_diag(uint64_t m, uint64_t k, const double* a, uint64_t L, const double* gn, double* grad,
+                    double* sigma, double* lambda, int* bad_k) {
+    *bad_k = 0;
+    double a_sq = 0.0;
+    for (uint64_t i = 0; i < m * k; ++i) a_sq += a[i] * a[i];
+    double* gg = (double*)calloc(k * k, sizeof(double));
+    double* ata = (double*)calloc(k * k, sizeof(double));
+    for (uint64_t i = 0; i < k; ++i) /* matmul_nt (dense_core.cpp:63-77) */
+        for (uint64_t j = 0; j < k; ++j) {
+            double acc = 0.0;
+            for (uint64_t l = 0; l < L; ++l) acc += gn[i * L + l] * gn[j * L + l];
+            gg[i * k + j] = acc;
+        }
+    double gg_sq = 0.0;
+    for (uint64_t i = 0; i < k * k; ++i) gg_sq += gg[i] * gg[i];
+    double r = 4.0 * (a_sq - gg_sq);
+    double scale = 4.0 * a_sq > 1.0 ? 4.0 * a_sq : 1.0;
+    int st = HQO_OK;
+    if (r < -1e-8 * scale) {
+        st = HQO_ERR_DIAGNOSTIC;
+        goto out;
+    }
+    *grad = (fabs(r) <= 1e-10) ? 0.0 : (r > 0.0 ? r : 0.0);
+    for (uint64_t row = 0; row < m; ++row) /* matmul_tn (dense_core.cpp:47-61) */
+        for (uint64_t i = 0; i < k; ++i) {
+            double ai = a[row * k + i];
+            if (ai == 0.0) continue;
+            for (uint64_t j = 0; j < k; ++j) ata[i * k + j] += ai * a[row * k + j];
+        }
+    st = gram_eigvals_desc(k, ata, sigma);
+    if (st) goto out;
+    for (uint64_t i = 0; i < k; ++i) sigma[i] = sqrt(sigma[i]);
+    st = gram_eigvals_desc(k, gg, lambda);
+    if (st) goto out;
+    {
+        double sc = (k && sigma[0] > 1.0) ? sigma[0] : 1.0;
+        for (uint64_t i = 0; i < k; ++i)
+            if (sigma[i] - lambda[i] < -1e-9 * sc) {
+                *bad_k = (int)i + 1;
+                st = HQO_ERR_DIAGNOSTIC;
+                goto out;
+            }
+    }
+out:
+    free(gg);
+    free(ata);
+    return st;
+}
+
 /* ---------------------------------------------------------------- solve --
  * solvers.cpp:50-178 for HOQRI with the element-wise kernel (core kept fresh
  * after every mode update, solvers.cpp:73-74, 143-144), no gradient tracing.
@@ -521,12 +617,23 @@ int hqo_random_factors(int N, const uint64_t* dims, const uint64_t* ranks, uint6
  *   factor_snap  optional, factors after each sweep (max_sweeps * sum I_n K_n)
  * Returns HQO_ERR_DEGENERATE with *degenerate_mode (1-based) on A == 0
  * (solvers.cpp:124). */
-int hqo_hoqri(int N, const uint64_t* dims, const uint64_t* ranks, uint64_t nnz,
-              const uint32_t* coords, const double* vals, double* factors_io,
-              uint64_t max_sweeps, double tol_fit_change, double* core_out,
-              uint64_t* sweeps_done, double* initial_objective, double* objective,
-              double* fit, double* drift, double* core_snap, double* factor_snap,
-              int* degenerate_mode) {
+typedef struct hqo_trace_out {
+    double tol_grad;  /* solvers.cpp:165-167 */
+    uint64_t ks;      /* row stride of sigma / lambda */
+    double* grad;     /* [max_sweeps * N] */
+    double* f_before;
+    double* f_after;
+    double* sigma;    /* [max_sweeps * N * ks] */
+    double* lambda;
+    uint64_t* updates;
+    int* bad_k;
+} hqo_trace_out;
+
+static int hoqri_impl(int N, const uint64_t* dims, const uint64_t* ranks, uint64_t nnz, const uint32_t* coords,
+                      const double* vals, double* factors_io, uint64_t max_sweeps, double tol_fit_change,
+                      double* core_out, uint64_t* sweeps_done, double* initial_objective, double* objective,
+                      double* fit, double* drift, double* core_snap, double* factor_snap, int* degenerate_mode,
+                      const hqo_trace_out* tr) {
     uint64_t off[16];
     factor_offsets(N, dims, ranks, off);
     uint64_t total_f = off[N - 1] + dims[N - 1] * ranks[N - 1];
@@ -543,8 +650,12 @@ int hqo_hoqri(int N, const uint64_t* dims, const uint64_t* ranks, uint64_t nnz,
     double fit_prev = dns - f0;
     *sweeps_done = 0;
     int st = HQO_OK;
+    double* gn = (double*)malloc(sizeof(double) * (pk ? pk : 1));
+    if (tr) *tr->updates = 0;
     for (uint64_t sweep = 1; sweep <= max_sweeps; ++sweep) {
+        double total_g = 0.0;
         for (int n = 0; n < N; ++n) {
+            const uint64_t u = (sweep - 1) * N + n;
             hqo_ttmctc(N, dims, ranks, nnz, coords, vals, factors_io, n, core_out, a);
             double mx = 0.0;
             for (uint64_t i = 0; i < dims[n] * ranks[n]; ++i)
@@ -554,11 +665,23 @@ int hqo_hoqri(int N, const uint64_t* dims, const uint64_t* ranks, uint64_t nnz,
                 st = HQO_ERR_DEGENERATE;
                 goto done;
             }
+            if (tr) { /* solvers.cpp:126-137: diagnostics at the pre-update state */
+                tr->f_before[u] = hqo_norm_sq(pk, core_out);
+                unfold_core(N, ranks, n, core_out, gn);
+                st = hqo_update_diag(dims[n], ranks[n], a, pk / ranks[n], gn, &tr->grad[u], tr->sigma + u * tr->ks,
+                                     tr->lambda + u * tr->ks, tr->bad_k);
+                if (st) goto done;
+                total_g += tr->grad[u];
+            }
             hqo_qr(dims[n], ranks[n], a, qn);
             drift[(sweep - 1) * N + n] =
                 hqo_subspace_distance(dims[n], ranks[n], qn, factors_io + off[n]);
             memcpy(factors_io + off[n], qn, sizeof(double) * dims[n] * ranks[n]);
             hqo_ttmc_core(N, dims, ranks, nnz, coords, vals, factors_io, core_out);
+            if (tr) {
+                tr->f_after[u] = hqo_norm_sq(pk, core_out);
+                *tr->updates = u + 1;
+            }
         }
         double obj = hqo_norm_sq(pk, core_out);
         objective[sweep - 1] = obj;
@@ -568,12 +691,41 @@ int hqo_hoqri(int N, const uint64_t* dims, const uint64_t* ranks, uint64_t nnz,
         if (factor_snap)
             memcpy(factor_snap + (sweep - 1) * total_f, factors_io, sizeof(double) * total_f);
         if (fabs(fit_prev - (dns - obj)) < tol_fit_change) break;
+        if (tr && tr->tol_grad > 0.0 && sqrt(total_g) <= tr->tol_grad * (obj > 1e-300 ? obj : 1e-300)) break;
         fit_prev = dns - obj;
     }
 done:
     free(a);
     free(qn);
+    free(gn);
     return st;
+}
+
+int hqo_hoqri(int N, const uint64_t* dims, const uint64_t* ranks, uint64_t nnz,
+              const uint32_t* coords, const double* vals, double* factors_io,
+              uint64_t max_sweeps, double tol_fit_change, double* core_out,
+              uint64_t* sweeps_done, double* initial_objective, double* objective,
+              double* fit, double* drift, double* core_snap, double* factor_snap,
+              int* degenerate_mode) {
+    return hoqri_impl(N, dims, ranks, nnz, coords, vals, factors_io, max_sweeps, tol_fit_change, core_out,
+                      sweeps_done, initial_objective, objective, fit, drift, core_snap, factor_snap, degenerate_mode,
+                      NULL);
+}
+
+/* hqo_hoqri with gradient tracing (trace_gradients / tol_grad > 0,
+ * solvers.cpp:58, 126-137, 146-150, 165-167): per update u = (sweep-1)*N + n
+ * grad, f_before, f_after, sigma / lambda (stride ks).  Returns
+ * HQO_ERR_DIAGNOSTIC (bad_k = 1-based interlacing index, 0 for a negative
+ * gradient) or HQO_ERR_CONTRACT like the reference. */
+int hqo_hoqri_traced(int N, const uint64_t* dims, const uint64_t* ranks, uint64_t nnz, const uint32_t* coords,
+                     const double* vals, double* factors_io, uint64_t max_sweeps, double tol_fit_change,
+                     double tol_grad, uint64_t ks, double* core_out, uint64_t* sweeps_done,
+                     double* initial_objective, double* objective, double* fit, double* drift, double* grad,
+                     double* f_before, double* f_after, double* sigma, double* lambda, uint64_t* updates,
+                     int* degenerate_mode, int* bad_k) {
+    hqo_trace_out tr = {tol_grad, ks, grad, f_before, f_after, sigma, lambda, updates, bad_k};
+    return hoqri_impl(N, dims, ranks, nnz, coords, vals, factors_io, max_sweeps, tol_fit_change, core_out,
+                      sweeps_done, initial_objective, objective, fit, drift, NULL, NULL, degenerate_mode, &tr);
 }
 
 /* solvers.cpp:225-236 */

@@ -232,6 +232,49 @@ int ref_hoqri(void* h, const uint64_t* ranks, uint64_t max_sweeps, double tol, u
     }
 }
 
+// tucker::hoqri with gradient tracing (trace_gradients, tol_grad: solvers.cpp:58,
+// 126-150, 165-167), random init from `seed`: the per-sweep trace plus every
+// ModeUpdateRecord (sigma / lambda rows of stride ks).
+int ref_hoqri_traced(void* h, const uint64_t* ranks, uint64_t max_sweeps, double tol, uint64_t seed, double tol_grad,
+                     uint64_t ks, double* factors_out, double* core_out, uint64_t* sweeps_done, double* objective,
+                     double* fit, double* grad, uint64_t* updates, double* f_before, double* f_after, double* sigma,
+                     double* lambda) {
+    try {
+        const SparseTensor& x = static_cast<RefTensor*>(h)->x;
+        SolverConfig cfg;
+        cfg.ranks.assign(ranks, ranks + x.order());
+        cfg.max_sweeps = max_sweeps;
+        cfg.tol_fit_change = tol;
+        cfg.seed = seed;
+        cfg.trace_gradients = true;
+        cfg.tol_grad = tol_grad;
+        SolveResult r = hoqri(x, cfg);
+        from_factors(r.model.factors, factors_out);
+        std::memcpy(core_out, r.model.core.data.data(), sizeof(double) * r.model.core.size());
+        const std::size_t n = x.order();
+        *sweeps_done = r.trace.sweeps.size();
+        for (std::size_t s = 0; s < r.trace.sweeps.size(); ++s) {
+            objective[s] = r.trace.sweeps[s].objective;
+            fit[s] = r.trace.sweeps[s].fit;
+            for (std::size_t m = 0; m < n; ++m) grad[s * n + m] = r.trace.sweeps[s].grad_norm_sq[m];
+        }
+        *updates = r.trace.updates.size();
+        for (std::size_t i = 0; i < r.trace.updates.size(); ++i) {
+            const ModeUpdateRecord& up = r.trace.updates[i];
+            f_before[i] = up.f_before;
+            f_after[i] = up.f_after;
+            for (std::size_t k = 0; k < up.sigma.size() && k < ks; ++k) sigma[i * ks + k] = up.sigma[k];
+            for (std::size_t k = 0; k < up.lambda.size() && k < ks; ++k) lambda[i * ks + k] = up.lambda[k];
+        }
+        return 0;
+    } catch (const DegenerateStateError& e) {
+        g_payload = static_cast<int64_t>(e.mode);
+        return 8;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
 // Per-update replay with the reference's own kernels (the acceptance.cpp:268-304
 // pattern), recording the core and factors after every sweep.  Starts from the
 // given factors.

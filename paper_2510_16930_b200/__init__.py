@@ -104,7 +104,10 @@ class HqConfig(C.Structure):
 class HqTrace(C.Structure):
     _fields_ = [("data_norm_sq", C.c_double), ("initial_objective", C.c_double), ("sweeps", C.c_uint64),
                 ("objective", C.c_void_p), ("fit", C.c_void_p), ("drift", C.c_void_p),
-                ("grad_norm_sq", C.c_void_p), ("elapsed_s", C.c_void_p)]
+                ("grad_norm_sq", C.c_void_p), ("elapsed_s", C.c_void_p),
+                ("upd_f_before", C.c_void_p), ("upd_f_after", C.c_void_p), ("upd_elapsed_s", C.c_void_p),
+                ("upd_sigma", C.c_void_p), ("upd_lambda", C.c_void_p), ("sigma_stride", C.c_uint64),
+                ("updates", C.c_uint64)]
 
 
 EXPORTED_SYMBOLS = [
@@ -470,6 +473,19 @@ class SweepRecord:
 
 
 @dataclasses.dataclass
+class ModeUpdateRecord:
+    """solvers.hpp:40-49 (filled only when gradients are traced)"""
+    sweep: int
+    mode: int
+    f_before: float
+    f_after: float
+    grad_norm_sq: float
+    sigma: List[float]
+    lambda_: List[float]
+    elapsed_s: float
+
+
+@dataclasses.dataclass
 class IterationTrace:
     data_norm_sq: float
     initial_objective: float
@@ -493,14 +509,23 @@ def _check_ranks(x: SparseTensor, ranks):
 
 
 class _TraceBuffers:
-    def __init__(self, sweeps, order):
+    def __init__(self, sweeps, order, ranks=None):
+        self.ranks = [int(k) for k in ranks] if ranks is not None else [1] * order
+        nu = max(1, sweeps * order)
+        self.ks = max(self.ranks)
         self.obj = np.zeros(max(1, sweeps))
         self.fit = np.zeros(max(1, sweeps))
-        self.drift = np.zeros(max(1, sweeps * order))
-        self.grad = np.zeros(max(1, sweeps * order))
+        self.drift = np.zeros(nu)
+        self.grad = np.zeros(nu)
         self.el = np.zeros(max(1, sweeps))
+        self.fb = np.zeros(nu)
+        self.fa = np.zeros(nu)
+        self.uel = np.zeros(nu)
+        self.sig = np.zeros(nu * self.ks)
+        self.lam = np.zeros(nu * self.ks)
         self.c = HqTrace(0.0, 0.0, 0, self.obj.ctypes.data, self.fit.ctypes.data, self.drift.ctypes.data,
-                         self.grad.ctypes.data, self.el.ctypes.data)
+                         self.grad.ctypes.data, self.el.ctypes.data, self.fb.ctypes.data, self.fa.ctypes.data,
+                         self.uel.ctypes.data, self.sig.ctypes.data, self.lam.ctypes.data, self.ks, 0)
 
     def to_trace(self, order):
         s = int(self.c.sweeps)
@@ -509,7 +534,14 @@ class _TraceBuffers:
             g = [float(v) for v in self.grad[i * order:(i + 1) * order]]
             recs.append(SweepRecord(i + 1, float(self.el[i]), float(self.obj[i]), float(self.fit[i]), float(sum(g)), g,
                                     [float(v) for v in self.drift[i * order:(i + 1) * order]]))
-        return IterationTrace(float(self.c.data_norm_sq), float(self.c.initial_objective), recs, [])
+        ups = []
+        for i in range(int(self.c.updates)):
+            n = i % order
+            k = self.ranks[n]
+            ups.append(ModeUpdateRecord(i // order + 1, n, float(self.fb[i]), float(self.fa[i]), float(self.grad[i]),
+                                        [float(v) for v in self.sig[i * self.ks:i * self.ks + k]],
+                                        [float(v) for v in self.lam[i * self.ks:i * self.ks + k]], float(self.uel[i])))
+        return IterationTrace(float(self.c.data_norm_sq), float(self.c.initial_objective), recs, ups)
 
 
 def hoqri(x: SparseTensor, config: SolverConfig, init_factors: Optional[Sequence[np.ndarray]] = None) -> SolveResult:
@@ -530,7 +562,7 @@ def hoqri(x: SparseTensor, config: SolverConfig, init_factors: Optional[Sequence
         init_arr = _ptr_array(fs0)
     fs = [np.empty((x.dims()[v], int(config.ranks[v])), np.float64) for v in range(n)]
     core = np.empty(int(np.prod(config.ranks)), np.float64)
-    tb = _TraceBuffers(int(config.max_sweeps), n)
+    tb = _TraceBuffers(int(config.max_sweeps), n, config.ranks)
     _check(L.hq_hoqri(x.handle, C.byref(cfg), init_arr, _ptr_array(fs), core.ctypes.data, C.byref(tb.c)))
     trace = tb.to_trace(n)
     model = TuckerModel(FactorSet(fs), CoreTensor([int(k) for k in config.ranks], core), trace.data_norm_sq)
@@ -661,7 +693,7 @@ class Solver:
             if core.dtype != np.float64 or not core.flags.c_contiguous or core.size != int(np.prod(self.config.ranks)):
                 raise ShapeError("download: core destination has the wrong size/dtype/layout")
             core = core.reshape(-1)
-        tb = _TraceBuffers(int(self.config.max_sweeps), self.n)
+        tb = _TraceBuffers(int(self.config.max_sweeps), self.n, self.config.ranks)
         _check(load_library().hq_solver_download(self._h, _ptr_array(fs), core.ctypes.data, C.byref(tb.c)))
         trace = tb.to_trace(self.n)
         return SolveResult(TuckerModel(FactorSet(fs), CoreTensor(list(self.config.ranks), core), trace.data_norm_sq),

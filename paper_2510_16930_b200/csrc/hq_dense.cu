@@ -514,6 +514,12 @@ void launch_sweep_end(const double* core, uint64_t core_size, double dns, double
     HQ_CHECK_LAUNCH();
 }
 
+void launch_update_diag(const double* w, const double* gt, int K, int L, int mode, int order, const UpdTrace& tr,
+                        DevStatus* st, cudaStream_t s) {
+    k_update_diag<<<1, 256, 0, s>>>(w, gt, K, L, mode, order, tr, st);
+    HQ_CHECK_LAUNCH();
+}
+
 void launch_drift_batch(const double* trp, int pairs, int order, const int* ranks_dev, int kmax, double* drift,
                         cudaStream_t s) {
     if (pairs <= 0) return;

@@ -71,7 +71,26 @@ struct SweepTrace {
     double* fit;         // [max_sweeps]
     double* drift;       // [max_sweeps * order]
     double* fit_prev;    // 1
+    const double* grad;  // [max_sweeps * order] per-update grad_norm_sq, or null (no gradient stop)
+    int order;
+    double tol_grad;     // solvers.cpp:165-167 stop when > 0
+    unsigned long long* t_end;  // [max_sweeps] device timestamp (ns) at the end of each sweep, or null
 };
+
+// Per-update gradient diagnostics (ModeUpdateRecord, solvers.hpp:40-49)
+struct UpdTrace {
+    double* grad;        // [max_sweeps * order]
+    double* f_before;    // [max_sweeps * order]
+    double* sigma;       // [max_sweeps * order * kstride]
+    double* lambda;      // [max_sweeps * order * kstride]
+    unsigned long long* t;  // [max_sweeps * order] device timestamp (ns) of the diagnostics point
+    int kstride;
+};
+// pre-update diagnostics of mode `mode` (solvers.cpp:126-137; manifold.cpp:37-84):
+// W = A^T A (reduced), gt = G_(n)^T (L x K).  Raises abort 5 (DiagnosticError)
+// or 6 (ContractError) like the reference.
+void launch_update_diag(const double* w, const double* gt, int K, int L, int mode, int order, const UpdTrace& tr,
+                        DevStatus* st, cudaStream_t s);
 void launch_drift(const double* ppart, int nslots, int K, const double* core, uint64_t core_size, double dns,
                   int order, int mode, bool end_of_sweep, double tol, uint64_t max_sweeps, const SweepTrace& tr,
                   DevStatus* st, cudaStream_t s);

@@ -36,6 +36,8 @@ struct DevStatus {
     int sweep;             // 1-based sweep counter (advanced on the device)
     int shifted;           // current QR runs shifted CholeskyQR3
     unsigned int shifted_count;
+    int diag_code;         // abort 5/6 detail: 1 negative gradient, 2 interlacing, 3 not PSD
+    int diag_k;            // 1-based index for interlacing
 };
 
 enum RunIf { kAlways = 0, kOnlyFallback = 1, kOnlyCholQR = 2, kOnlyShifted = 3, kFallbackOrShifted = 4 };

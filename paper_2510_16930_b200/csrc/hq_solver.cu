@@ -201,6 +201,10 @@ struct Solver {
     cudaEvent_t ev_join = nullptr;
     DBuf<double> tr_obj, tr_fit, tr_drift, fit_prev;
     DBuf<double> tr_p;      // P = U_new^T U_old per (sweep, mode): drifts evaluated at download
+    // gradient tracing (trace_gradients / tol_grad > 0, solvers.cpp:58): per-update diagnostics
+    bool tracing = false;
+    DBuf<double> tr_grad, tr_fb, tr_sig, tr_lam;
+    DBuf<unsigned long long> tr_t, tr_tend;
     DBuf<int> dranks;
     int kmax_ = 1;
     // multi-GPU: this rank owns rows [bnd[n][rank], bnd[n][rank+1]) of every mode n
@@ -330,6 +334,15 @@ struct Solver {
         tr_fit.alloc(cfg.max_sweeps);
         tr_drift.alloc(cfg.max_sweeps * N);
         kmax_ = kmax;
+        tracing = cfg.trace_gradients || cfg.tol_grad > 0.0;
+        if (tracing) {
+            tr_grad.alloc(cfg.max_sweeps * N);
+            tr_fb.alloc(cfg.max_sweeps * N);
+            tr_sig.alloc(cfg.max_sweeps * N * kmax);
+            tr_lam.alloc(cfg.max_sweeps * N * kmax);
+            tr_t.alloc(cfg.max_sweeps * N);
+            tr_tend.alloc(cfg.max_sweeps);
+        }
         tr_p.alloc((size_t)cfg.max_sweeps * N * kmax * kmax);
         dranks.alloc(N);
         HQ_CUDA(cudaMemcpyAsync(dranks.get(), ranks, sizeof(int) * N, cudaMemcpyHostToDevice, s));
@@ -411,6 +424,10 @@ struct Solver {
             comm->allreduce_sum(wred.get(), (size_t)K * K, s);
             comm->allreduce_max(maxv.get(), 1, s);
         }
+        if (tracing) {  // pre-update diagnostics (solvers.cpp:126-137): W = A^T A and G_(n) at hand
+            UpdTrace ut{tr_grad.get(), tr_fb.get(), tr_sig.get(), tr_lam.get(), tr_t.get(), kmax_};
+            launch_update_diag(wred.get(), gt.get(), K, m.L, n, N, ut, S, s);
+        }
         launch_chol1(wred.get(), maxv.get(), K, r1inv.get(), S, n + 1, dims[n], s, comm != nullptr);
         mark("chol1");
         const double* a_loc = A.get() + r0 * K;
@@ -468,7 +485,8 @@ struct Solver {
         if (n == N - 1) {
             HQ_CUDA(cudaEventRecord(ev_join, side));
             HQ_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
-            SweepTrace tr{tr_obj.get(), tr_fit.get(), tr_drift.get(), fit_prev.get()};
+            SweepTrace tr{tr_obj.get(), tr_fit.get(), tr_drift.get(), fit_prev.get(),
+                          tracing ? tr_grad.get() : nullptr, N, cfg.tol_grad, tracing ? tr_tend.get() : nullptr};
             launch_sweep_end(core.get(), core_size, dns, cfg.tol_fit_change, cfg.max_sweeps, tr, S, s);
             mark("sweep_end");
         }
@@ -483,6 +501,7 @@ struct Solver {
         const int core_pass = pass_launch_count(T->modes[0], sh[0]);
         for (int n = 0; n < N; ++n) {
             const int pass = pass_launch_count(T->modes[n], sh[n]);
+            if (tracing) c += 1;  // update diagnostics
             if (!comm)  // gt, pass, reduce, chol1, gram2, chol2, gram3, chol3, apply, householder, apply-P,
                         // core pass + reduce, store_p
                 c += 1 + pass + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + core_pass + 1 + 1;
@@ -567,6 +586,12 @@ struct Solver {
     }
 
     void check_status(const DevStatus& h) {
+        if (h.abort == 5 && h.diag_code == 1)  // manifold.cpp:45-47
+            fail(HQ_ERR_DIAGNOSTIC, "grad_norm_sq is negative beyond rounding; orthonormality is broken upstream");
+        if (h.abort == 5)  // manifold.cpp:79-81
+            fail(HQ_ERR_DIAGNOSTIC, "interlacing violated at k=" + std::to_string(h.diag_k) +
+                                        "; upstream state is numerically corrupted");
+        if (h.abort == 6) fail(HQ_ERR_CONTRACT, "gram_eigvals_desc: matrix is not PSD");  // dense_core.cpp:381-382
         if (h.abort == 3)
             fail(HQ_ERR_DIAGNOSTIC, "rank-deficient TTMcTC output in a multi-GPU solve (CholeskyQR2 breakdown); the "
                                     "Householder fallback runs on one GPU: rerun with a single rank");
@@ -623,8 +648,43 @@ struct Solver {
                     tr->elapsed_s[i - 1] = ms * 1e-3;
                 }
             }
-            if (tr->grad_norm_sq)
-                for (uint64_t i = 0; i < (uint64_t)h.sweep * N; ++i) tr->grad_norm_sq[i] = 0.0;
+            const uint64_t nu = (uint64_t)h.sweep * N;
+            if (tr->grad_norm_sq) {
+                if (tracing && nu)
+                    HQ_CUDA(cudaMemcpy(tr->grad_norm_sq, tr_grad.get(), 8 * nu, cudaMemcpyDeviceToHost));
+                else
+                    for (uint64_t i = 0; i < nu; ++i) tr->grad_norm_sq[i] = 0.0;  // solvers.cpp:82
+            }
+            tr->updates = 0;
+            if (tracing && nu) {
+                // ModeUpdateRecords (solvers.hpp:40-49): f_after of update n is f_before of update n+1, the
+                // sweep's objective for the last mode; elapsed between successive diagnostics points
+                std::vector<double> fb(nu), obj(h.sweep), sig(nu * kmax_), lam(nu * kmax_);
+                std::vector<unsigned long long> t(nu), tend(h.sweep);
+                HQ_CUDA(cudaMemcpy(fb.data(), tr_fb.get(), 8 * nu, cudaMemcpyDeviceToHost));
+                HQ_CUDA(cudaMemcpy(obj.data(), tr_obj.get(), 8 * h.sweep, cudaMemcpyDeviceToHost));
+                HQ_CUDA(cudaMemcpy(sig.data(), tr_sig.get(), 8 * nu * kmax_, cudaMemcpyDeviceToHost));
+                HQ_CUDA(cudaMemcpy(lam.data(), tr_lam.get(), 8 * nu * kmax_, cudaMemcpyDeviceToHost));
+                HQ_CUDA(cudaMemcpy(t.data(), tr_t.get(), 8 * nu, cudaMemcpyDeviceToHost));
+                HQ_CUDA(cudaMemcpy(tend.data(), tr_tend.get(), 8 * h.sweep, cudaMemcpyDeviceToHost));
+                tr->updates = nu;
+                for (uint64_t i = 0; i < nu; ++i) {
+                    const uint64_t sw = i / N;
+                    const int n = (int)(i % N);
+                    const bool last = n == N - 1;
+                    if (tr->upd_f_before) tr->upd_f_before[i] = fb[i];
+                    if (tr->upd_f_after) tr->upd_f_after[i] = last ? obj[sw] : fb[i + 1];
+                    if (tr->upd_elapsed_s) {
+                        const unsigned long long t1 = last ? tend[sw] : t[i + 1];
+                        tr->upd_elapsed_s[i] = t1 > t[i] ? (double)(t1 - t[i]) * 1e-9 : 0.0;
+                    }
+                    const uint64_t ks = tr->sigma_stride;
+                    for (int k = 0; k < ranks[n] && ks; ++k) {
+                        if (tr->upd_sigma && (uint64_t)k < ks) tr->upd_sigma[i * ks + k] = sig[i * kmax_ + k];
+                        if (tr->upd_lambda && (uint64_t)k < ks) tr->upd_lambda[i * ks + k] = lam[i * kmax_ + k];
+                    }
+                }
+            }
         }
         HQ_CUDA(cudaStreamSynchronize(s));
         // solvers.cpp:171-172
@@ -864,7 +924,7 @@ int hq_subspace_distance(uint64_t rows, uint64_t cols, const double* u, const do
         HQ_CUDA(cudaMemcpyAsync(U.get(), u, sizeof(double) * rows * cols, cudaMemcpyHostToDevice, s));
         HQ_CUDA(cudaMemcpyAsync(V.get(), v, sizeof(double) * rows * cols, cudaMemcpyHostToDevice, s));
         launch_apply(nullptr, rows, (int)cols, nullptr, U.get(), V.get(), pp.get(), false, nullptr, kAlways, s);
-        SweepTrace tr{obj.get(), fit.get(), d.get(), fp.get()};
+        SweepTrace tr{obj.get(), fit.get(), d.get(), fp.get(), nullptr, 1, 0.0, nullptr};
         launch_drift(pp.get(), dense_slots(), (int)cols, nullptr, 0, 0.0, 1, 0, false, 0.0, 1, tr, st.get(), s);
         HQ_CUDA(cudaMemcpyAsync(out, d.get(), 8, cudaMemcpyDeviceToHost, s));
         HQ_CUDA(cudaStreamSynchronize(s));
@@ -905,8 +965,6 @@ int hq_solver_create(const hq_tensor* t, const hq_config* cfg, const double* con
         auto h = std::make_unique<hq_solver>();
         h->impl = std::make_unique<Solver>();
         cudaStream_t s = stream ? as_stream(stream) : t->stream;
-        if (cfg->trace_gradients || cfg->tol_grad > 0.0)
-            fail(HQ_ERR_CAPACITY, "gradient tracing is not implemented on the device engine yet");
         h->impl->setup(&t->t, cfg, init_factors, s);
         *out = h.release();
     });
@@ -947,8 +1005,6 @@ int hq_solver_create_dist(const hq_tensor* t, const hq_config* cfg, const double
         auto h = std::make_unique<hq_solver>();
         h->impl = std::make_unique<Solver>();
         cudaStream_t s = stream ? as_stream(stream) : t->stream;
-        if (cfg->trace_gradients || cfg->tol_grad > 0.0)
-            fail(HQ_ERR_CAPACITY, "gradient tracing is not implemented on the device engine yet");
         h->impl->setup(&t->t, cfg, init_factors, s, comm ? comm->impl : nullptr);
         *out = h.release();
     });
@@ -1031,8 +1087,6 @@ int hq_solver_ttmctc_work(const hq_solver* sv, int mode, double* flops, double* 
 int hq_hoqri(const hq_tensor* t, const hq_config* cfg, const double* const* init_factors, double* const* factors_out,
              double* core_out, hq_trace* trace) {
     return guard([&] {
-        if (cfg->trace_gradients || cfg->tol_grad > 0.0)
-            fail(HQ_ERR_CAPACITY, "gradient tracing is not implemented on the device engine yet");
         Solver S;
         S.setup(&t->t, cfg, init_factors, t->stream);
         S.solve();

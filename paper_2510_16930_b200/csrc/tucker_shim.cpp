@@ -440,8 +440,6 @@ static SolveResult solve_impl(const SparseTensor& x, const SolverConfig& config,
     check_ranks(x, config.ranks);
     if (config.max_sweeps < 1) throw ShapeError("max_sweeps must be at least 1");
     if (config.tol_fit_change < 0.0) throw ShapeError("tolerance must be nonnegative");
-    if (config.trace_gradients || config.tol_grad > 0.0)
-        throw CapacityError("gradient tracing is not available on the B200 engine yet");
     if (!start && config.init != InitMode::kRandom)
         throw CapacityError("HOSVD initialisation is desk-scale only and outside the B200 engine; use random init");
     const std::size_t n = x.order();
@@ -453,6 +451,8 @@ static SolveResult solve_impl(const SparseTensor& x, const SolverConfig& config,
     c.tol_fit_change = config.tol_fit_change;
     c.seed = config.seed;
     c.kernel = config.kernel == KernelVariant::kMatrix ? 1 : 0;
+    c.trace_gradients = config.trace_gradients ? 1 : 0;
+    c.tol_grad = config.tol_grad;
     std::vector<const double*> init;
     if (start) {
         if (start->order() != n) throw ShapeError("factor count does not match tensor order");
@@ -464,13 +464,23 @@ static SolveResult solve_impl(const SparseTensor& x, const SolverConfig& config,
     res.model.core = CoreTensor(config.ranks);
     std::vector<double*> fo;
     for (auto& m : res.model.factors.factors) fo.push_back(m.data.data());
-    std::vector<double> obj(config.max_sweeps), fit(config.max_sweeps), drift(config.max_sweeps * n),
-        el(config.max_sweeps);
+    const std::size_t nu = config.max_sweeps * n;
+    std::size_t ks = 1;
+    for (std::size_t k : config.ranks) ks = std::max(ks, k);
+    std::vector<double> obj(config.max_sweeps), fit(config.max_sweeps), drift(nu), el(config.max_sweeps), grad(nu),
+        fb(nu), fa(nu), uel(nu), sig(nu * ks), lam(nu * ks);
     hq_trace tr{};
     tr.objective = obj.data();
     tr.fit = fit.data();
     tr.drift = drift.data();
     tr.elapsed_s = el.data();
+    tr.grad_norm_sq = grad.data();
+    tr.upd_f_before = fb.data();
+    tr.upd_f_after = fa.data();
+    tr.upd_elapsed_s = uel.data();
+    tr.upd_sigma = sig.data();
+    tr.upd_lambda = lam.data();
+    tr.sigma_stride = ks;
     check(hq_hoqri(x.device(), &c, start ? init.data() : nullptr, fo.data(), res.model.core.data.data(), &tr));
     res.model.data_norm_sq = tr.data_norm_sq;
     res.trace.data_norm_sq = tr.data_norm_sq;
@@ -481,9 +491,22 @@ static SolveResult solve_impl(const SparseTensor& x, const SolverConfig& config,
         r.elapsed_s = el[s];
         r.objective = obj[s];
         r.fit = fit[s];
-        r.grad_norm_sq.assign(n, 0.0);
+        r.grad_norm_sq.assign(grad.begin() + s * n, grad.begin() + (s + 1) * n);
+        for (double g : r.grad_norm_sq) r.total_grad_norm_sq += g;
         r.drift.assign(drift.begin() + s * n, drift.begin() + (s + 1) * n);
         res.trace.sweeps.push_back(std::move(r));
+    }
+    for (std::size_t i = 0; i < tr.updates; ++i) {  // solvers.cpp:127-150
+        ModeUpdateRecord up;
+        up.sweep = i / n + 1;
+        up.mode = i % n;
+        up.f_before = fb[i];
+        up.f_after = fa[i];
+        up.grad_norm_sq = grad[i];
+        up.sigma.assign(sig.begin() + i * ks, sig.begin() + i * ks + config.ranks[up.mode]);
+        up.lambda.assign(lam.begin() + i * ks, lam.begin() + i * ks + config.ranks[up.mode]);
+        up.elapsed_s = uel[i];
+        res.trace.updates.push_back(std::move(up));
     }
     return res;
 }

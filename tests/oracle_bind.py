@@ -68,6 +68,10 @@ class Oracle:
                                 f64p, C.POINTER(C.c_uint64), C.POINTER(C.c_double), f64p, f64p, f64p,
                                 C.c_void_p, C.c_void_p, C.POINTER(C.c_int)]
         L.hqo_fit_error.argtypes = [C.c_double, C.c_uint64, f64p, C.POINTER(C.c_double)]
+        L.hqo_hoqri_traced.argtypes = [C.c_int, u64p, u64p, C.c_uint64, u32p, f64p, f64p, C.c_uint64, C.c_double,
+                                       C.c_double, C.c_uint64, f64p, C.POINTER(C.c_uint64), C.POINTER(C.c_double),
+                                       f64p, f64p, f64p, f64p, f64p, f64p, f64p, f64p, C.POINTER(C.c_uint64),
+                                       C.POINTER(C.c_int), C.POINTER(C.c_int)]
 
     # rng
     def raw_stream(self, seed, n):
@@ -184,6 +188,33 @@ class Oracle:
         return out
 
 
+def _oracle_hoqri_traced(self, dims, ranks, coords, vals, init_factors, max_sweeps, tol=0.0, tol_grad=0.0):
+    """hqo_hoqri_traced: the oracle solve with per-update gradient diagnostics."""
+    dims, ranks = _u64(dims), _u64(ranks)
+    coords, vals = _u32(coords).reshape(-1), _f64(vals)
+    N = dims.size
+    ks = int(ranks.max())
+    f = _f64(np.concatenate([np.asarray(u).reshape(-1) for u in init_factors]))
+    core = np.empty(int(np.prod(ranks)), np.float64)
+    sd, nu = C.c_uint64(0), C.c_uint64(0)
+    f0 = C.c_double(0)
+    obj, fit = np.zeros(max_sweeps), np.zeros(max_sweeps)
+    drift, grad = np.zeros(max_sweeps * N), np.zeros(max_sweeps * N)
+    fb, fa = np.zeros(max_sweeps * N), np.zeros(max_sweeps * N)
+    sig, lam = np.zeros(max_sweeps * N * ks), np.zeros(max_sweeps * N * ks)
+    deg, bad = C.c_int(0), C.c_int(0)
+    st = self.L.hqo_hoqri_traced(N, dims, ranks, vals.size, coords, vals, f, max_sweeps, tol, tol_grad, ks, core,
+                                 C.byref(sd), C.byref(f0), obj, fit, drift, grad, fb, fa, sig, lam, C.byref(nu),
+                                 C.byref(deg), C.byref(bad))
+    s, u = int(sd.value), int(nu.value)
+    return dict(status=st, bad_k=bad.value, sweeps=s, objective=obj[:s], fit=fit[:s], grad=grad[:u], updates=u,
+                f_before=fb[:u], f_after=fa[:u], sigma=sig[:u * ks].reshape(u, ks),
+                lambda_=lam[:u * ks].reshape(u, ks), core=core)
+
+
+Oracle.hoqri_traced = _oracle_hoqri_traced
+
+
 def _split(flat, dims, ranks):
     out, o = [], 0
     for d, r in zip(dims, ranks):
@@ -226,6 +257,9 @@ class RefLib:
         L.ref_hoqri.argtypes = [vp, u64p, C.c_uint64, C.c_double, C.c_uint64, C.c_int, f64p, f64p,
                                 C.POINTER(C.c_uint64), C.POINTER(C.c_double), f64p, f64p, f64p, f64p]
         L.ref_hoqri_replay.argtypes = [vp, u64p, f64p, C.c_uint64, f64p, f64p, f64p]
+        L.ref_hoqri_traced.argtypes = [vp, u64p, C.c_uint64, C.c_double, C.c_uint64, C.c_double, C.c_uint64, f64p,
+                                       f64p, C.POINTER(C.c_uint64), f64p, f64p, f64p, C.POINTER(C.c_uint64), f64p,
+                                       f64p, f64p, f64p]
         L.ref_last_payload.restype = C.c_int64
         L.ref_slices_create.argtypes = [vp, C.c_int]
         L.ref_slices_create.restype = vp
@@ -317,6 +351,25 @@ class RefTensor:
         return dict(status=st, payload=int(self.lib.L.ref_last_payload()), sweeps=s, initial_objective=f0.value,
                     objective=obj[:s], fit=fit[:s], drift=drift[: s * N].reshape(s, N), elapsed=el[:s],
                     factors=_split(f, self.dims, ranks), core=core.reshape(tuple(int(r) for r in ranks)))
+
+    def hoqri_traced(self, ranks, sweeps, tol, seed, tol_grad=0.0):
+        """tucker::hoqri with trace_gradients (per-update ModeUpdateRecords)."""
+        ranks = _u64(ranks)
+        n = len(self.dims)
+        ks = int(ranks.max())
+        fs = np.empty(sum(d * int(k) for d, k in zip(self.dims, ranks)), np.float64)
+        core = np.empty(int(np.prod(ranks)), np.float64)
+        sw, nu = C.c_uint64(0), C.c_uint64(0)
+        obj, fit = np.zeros(sweeps), np.zeros(sweeps)
+        grad = np.zeros(sweeps * n)
+        fb, fa = np.zeros(sweeps * n), np.zeros(sweeps * n)
+        sig, lam = np.zeros(sweeps * n * ks), np.zeros(sweeps * n * ks)
+        st = self.lib.L.ref_hoqri_traced(self.h, ranks, sweeps, tol, seed, tol_grad, ks, fs, core, C.byref(sw), obj,
+                                         fit, grad, C.byref(nu), fb, fa, sig, lam)
+        s, u = int(sw.value), int(nu.value)
+        return dict(status=st, sweeps=s, objective=obj[:s], fit=fit[:s], grad=grad[:u], updates=u, f_before=fb[:u],
+                    f_after=fa[:u], sigma=sig[:u * ks].reshape(u, ks), lambda_=lam[:u * ks].reshape(u, ks),
+                    core=core)
 
     def replay(self, ranks, init_factors, sweeps):
         ranks = _u64(ranks)

@@ -302,3 +302,34 @@ def test_hoqri_config1_full():
     assert rel <= 1e-9, rel
     for m in range(3):
         assert subspace_gap(r.model.factors.factors[m], g[f"U{m}"]) <= 1e-8
+
+
+@pytest.mark.parametrize("name", ["g3", "g4", "gk", "gstop"])
+def test_hoqri_gradient_trace_matches_reference(name):
+    """trace_gradients / tol_grad on the device (solvers.cpp:126-150, 165-167):
+    every ModeUpdateRecord and the gradient stop against tucker::hoqri."""
+    g = golden("grad.npz")
+    dims = [int(d) for d in g[f"{name}_dims"]]
+    ranks = [int(r) for r in g[f"{name}_ranks"]]
+    x = hq.SparseTensor(dims, g[f"{name}_coords"], g[f"{name}_vals"])
+    tol_grad = float(g[f"{name}_tol_grad"])
+    cfg = hq.SolverConfig(ranks=ranks, max_sweeps=int(g[f"{name}_max_sweeps"]), tol_fit_change=0.0,
+                          seed=int(g[f"{name}_seed"]), trace_gradients=True, tol_grad=tol_grad)
+    r = hq.hoqri(x, cfg)
+    assert len(r.trace.sweeps) == int(g[f"{name}_sweeps"])
+    ups = r.trace.updates
+    assert len(ups) == int(g[f"{name}_updates"])
+    gr = np.array([u.grad_norm_sq for u in ups])
+    scale = max(1.0, float(np.max(g[f"{name}_f_before"])) * 4)
+    assert np.abs(gr - g[f"{name}_grad"]).max() <= 1e-9 * scale
+    np.testing.assert_allclose([u.f_before for u in ups], g[f"{name}_f_before"], rtol=1e-9)
+    np.testing.assert_allclose([u.f_after for u in ups], g[f"{name}_f_after"], rtol=1e-9)
+    for i, u in enumerate(ups):
+        k = ranks[u.mode]
+        assert u.sweep == i // len(dims) + 1 and u.mode == i % len(dims)
+        np.testing.assert_allclose(u.sigma, g[f"{name}_sigma"][i][:k], rtol=1e-9, atol=1e-12)
+        np.testing.assert_allclose(u.lambda_, g[f"{name}_lambda_"][i][:k], rtol=1e-9, atol=1e-12)
+        assert u.elapsed_s >= 0.0
+    sw = np.array([s.grad_norm_sq for s in r.trace.sweeps]).reshape(-1)
+    np.testing.assert_allclose(sw, gr, rtol=0, atol=0)
+    np.testing.assert_allclose([s.objective for s in r.trace.sweeps], g[f"{name}_objective"], rtol=1e-9)

@@ -116,3 +116,19 @@ def test_config1_layout_and_trace(oracle):
     np.testing.assert_allclose(r["objective"], g["objective"], rtol=1e-12)
     np.testing.assert_allclose(r["fit"], g["fit"], rtol=1e-12)
     assert np.abs(r["core"] - g["core"]).max() <= 1e-12 * np.abs(g["core"]).max()
+
+
+def test_oracle_gradient_trace_matches_reference(oracle):
+    """hqo_hoqri_traced (solvers.cpp:126-150, 165-167; manifold.cpp:37-84)
+    against tucker::hoqri with trace_gradients: per-update diagnostics and the
+    tol_grad stop."""
+    g = golden("grad.npz")
+    for n in g["names"]:
+        dims = [int(d) for d in g[f"{n}_dims"]]
+        ranks = [int(r) for r in g[f"{n}_ranks"]]
+        u0 = [g[f"{n}_U0_{m}"] for m in range(len(dims))]
+        r = oracle.hoqri_traced(dims, ranks, g[f"{n}_coords"], g[f"{n}_vals"], u0, int(g[f"{n}_max_sweeps"]), 0.0,
+                                float(g[f"{n}_tol_grad"]))
+        assert r["status"] == 0 and r["sweeps"] == int(g[f"{n}_sweeps"]), n
+        for k in ("grad", "f_before", "f_after", "sigma", "lambda_", "objective"):
+            np.testing.assert_allclose(r[k], g[f"{n}_{k}"], rtol=1e-13, atol=1e-14, err_msg=f"{n}:{k}")

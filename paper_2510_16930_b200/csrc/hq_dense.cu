@@ -292,6 +292,9 @@ __global__ void __launch_bounds__(kHhThreads) k_householder_mc(const double* __r
                 for (int j = 0; j < KM; ++j) row[j] = (j >= k && j < n) ? w[i * n + j] : 0.0;
                 const double v = (i == (uint64_t)k) ? vk : pick<KM>(row, k);
                 refl[(uint64_t)k * m + i] = v;
+                // row k becomes R's row k, which no later step reads -- and other CTAs may still be
+                // reading it for their dots in this phase, so it is left untouched
+                if (i == (uint64_t)k) continue;
 #pragma unroll
                 for (int j = 0; j < KM; ++j)
                     if (j > k && j < n) {

@@ -55,7 +55,6 @@ struct LS_ {
     static constexpr int FW = (RW + 4) / 8 * 8 + 4;
     static constexpr int CH = 128;                  // nonzeros per chunk
     static constexpr int WARPS = 8, THREADS = 256;
-    static constexpr int PP = RW / 2;               // 16-byte pieces per nonzero
     static constexpr size_t row_doubles = (size_t)CH * FW;           // one gathered-row buffer
     static constexpr size_t red_doubles = (size_t)WARPS * MT * NTL * 64;
     static constexpr size_t rec_words = (size_t)NO * CH;             // one index-record buffer
@@ -171,7 +170,6 @@ __global__ void __launch_bounds__(256) k_longseg_mma(LongArgs a) {
     const int gid = lane >> 2, tig = lane & 3;
     const uint64_t G = gridDim.x, c = blockIdx.x;
     const uint64_t rend = a.rbase + a.rows;
-    constexpr int P0 = K0 / 2, P1 = K1 / 2;
     const uint32_t* idx[3] = {a.i0, a.i1, a.i2};
 
     ChunkCursor cr{a.nseg * c / G, a.nseg * (c + 1) / G, 0, 0};

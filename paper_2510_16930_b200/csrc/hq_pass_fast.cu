@@ -93,13 +93,6 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ double2 ldg2(const double* p, uint64_t pol) {
-    double2 d;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
-                 : "=d"(d.x), "=d"(d.y)
-                 : "l"(p), "l"(pol));
-    return d;
-}
 __device__ __forceinline__ void cp16(void* dst, const void* src, uint64_t pol) {
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
                  "l"(pol));

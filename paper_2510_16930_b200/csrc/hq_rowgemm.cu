@@ -34,7 +34,7 @@ struct RG {
     static constexpr int NT = (K + 7) / 8;  // 8-wide tiles of the K dimension
     static constexpr int KP = NT * 8;
     static constexpr int KS = (K + 3) / 4;  // k-steps of X = A T
-    static constexpr int LD = KP + 1;       // smem row stride
+    static constexpr int LD = KP + 4;       // smem row stride (= 4 mod 8 doubles: fragment reads conflict-free)
 };
 
 template <int K>
@@ -77,39 +77,37 @@ __global__ void __launch_bounds__(kRgWarps * 32)
     const uint64_t gb = groups * w / W, ge = groups * (w + 1) / W;
     double mx = 0.0;
     double* sx = sX[warp];
+    double* sa = sx;  // the A tile and the X tile share storage (A read into fragments first)
     double* sy = sY[warp];
-    constexpr int OQ = (8 * K + 31) / 32;  // elements of an 8-row group of `other` per lane
-    double an[C::KS], on[OQ];  // next group's operands (one group of 8 rows in flight ahead)
-    auto load_a = [&](uint64_t g, double (&dst)[C::KS], double (&od)[OQ]) {
-        const uint64_t row = g * 8 + gid;
-        const bool rv = g < ge && row < rows;
+    // an 8-row group of A / `other` is 8K contiguous doubles: loaded coalesced
+    // (lane-strided), re-laid out through shared memory
+    constexpr int OQ = (8 * K + 31) / 32;
+    auto load_g = [&](uint64_t g, double (&ad)[OQ], double (&od)[OQ]) {
 #pragma unroll
-        for (int ks = 0; ks < C::KS; ++ks) {
-            const int k = 4 * ks + tig;
-            dst[ks] = (rv && k < K) ? A[row * K + k] : 0.0;
-        }
-        if (other) {
-#pragma unroll
-            for (int i = 0; i < OQ; ++i) {
-                const int q = lane + 32 * i;
-                const uint64_t e = g * 8 * K + q;
-                od[i] = (g < ge && q < 8 * K && e < rows * K) ? other[e] : 0.0;
-            }
+        for (int i = 0; i < OQ; ++i) {
+            const int q = lane + 32 * i;
+            const uint64_t e = g * 8 * K + q;
+            const bool v = g < ge && q < 8 * K && e < rows * K;
+            ad[i] = v ? A[e] : 0.0;
+            od[i] = (other && v) ? other[e] : 0.0;
         }
     };
-    load_a(gb, an, on);
-    for (uint64_t g = gb; g < ge; ++g) {
-        const uint64_t row = g * 8 + gid;
-        const bool rv = row < rows;
-        double a[C::KS], o[OQ];
+    auto process = [&](uint64_t g, const double (&ad)[OQ], const double (&od)[OQ]) {
 #pragma unroll
-        for (int ks = 0; ks < C::KS; ++ks) {
-            a[ks] = an[ks];
-            mx = fmax(mx, fabs(a[ks]));
+        for (int i = 0; i < OQ; ++i) {
+            const int q = lane + 32 * i;
+            if (q < 8 * K) {
+                const int r = q / K, cc = q - r * K;
+                sa[r * C::LD + cc] = ad[i];
+                mx = fmax(mx, fabs(ad[i]));
+                if (other) sy[r * C::LD + cc] = od[i];
+            }
         }
+        __syncwarp();
+        double a[C::KS];
 #pragma unroll
-        for (int i = 0; i < OQ; ++i) o[i] = on[i];
-        load_a(g + 1, an, on);
+        for (int ks = 0; ks < C::KS; ++ks) a[ks] = sa[gid * C::LD + 4 * ks + tig];
+        __syncwarp();
         // X = A T (C fragment: row gid, cols 8nt + 2 tig + {0,1})
 #pragma unroll
         for (int nt = 0; nt < C::NT; ++nt) {
@@ -119,22 +117,19 @@ __global__ void __launch_bounds__(kRgWarps * 32)
             const int col = 8 * nt + 2 * tig;
             sx[gid * C::LD + col] = c0;
             sx[gid * C::LD + col + 1] = c1;
-            if (out && rv) {
-                if (col < K) out[row * K + col] = c0;
-                if (col + 1 < K) out[row * K + col + 1] = c1;
-            }
         }
-        if (other) {
+        __syncwarp();
+        if (out) {
 #pragma unroll
             for (int i = 0; i < OQ; ++i) {
                 const int q = lane + 32 * i;
-                if (q < 8 * K) {
+                const uint64_t e = g * 8 * K + q;
+                if (q < 8 * K && e < rows * K) {
                     const int r = q / K, cc = q - r * K;
-                    sy[r * C::LD + cc] = o[i];
+                    out[e] = sx[r * C::LD + cc];
                 }
             }
         }
-        __syncwarp();
         const double* y = other ? sy : sx;
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks)
@@ -146,6 +141,18 @@ __global__ void __launch_bounds__(kRgWarps * 32)
                     dmma884(acc[mt][nt][0], acc[mt][nt][1], av, y[(4 * ks + tig) * C::LD + 8 * nt + gid]);
             }
         __syncwarp();
+    };
+    // two row groups in flight ahead of the one being multiplied
+    double a0[OQ], o0[OQ], a1[OQ], o1[OQ];
+    load_g(gb, a0, o0);
+    load_g(gb + 1, a1, o1);
+    for (uint64_t g = gb; g < ge; g += 2) {
+        process(g, a0, o0);
+        load_g(g + 2, a0, o0);
+        if (g + 1 < ge) {
+            process(g + 1, a1, o1);
+            load_g(g + 3, a1, o1);
+        }
     }
     // fixed-order combination of the warps' fragments: ((w0 + w1) + w2) + ...
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));

@@ -180,7 +180,7 @@ def test_qr_against_reference():
         q = hq.qr_orthonormal(g[f"{name}_A"])
         assert np.abs(q - g[f"{name}_Q"]).max() <= 1e-12, name
         q2 = hq.qr_orthonormal(g[f"{name}_A"])
-        assert (q == q2).all()
+        assert (q == q2).all(), (name, float(np.abs(q - q2).max()), np.argwhere(q != q2)[:5].tolist())
     np.testing.assert_allclose(hq.qr_orthonormal(np.array([[3.0], [4.0]]))[:, 0], [0.6, 0.8], rtol=1e-14)
     with pytest.raises(hq.ShapeError):
         hq.qr_orthonormal(np.zeros((2, 3)))

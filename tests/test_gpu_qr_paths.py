@@ -49,7 +49,8 @@ def test_householder_fill_large_matches_reference(oracle, m, k, dead):
     assert np.abs(q.T @ q - np.eye(k)).max() <= 1e-12
     # the filled columns come from the same seeded stream: the whole Q matches
     assert np.abs(q - qo).max() <= 1e-9
-    assert (q == hq.qr_orthonormal(a)).all()  # deterministic
+    for _ in range(4):  # deterministic (grid barriers order every cross-CTA read)
+        assert (q == hq.qr_orthonormal(a)).all()
 
 
 def test_zero_matrix_fills_every_column(oracle):

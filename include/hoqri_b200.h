@@ -153,6 +153,20 @@ typedef struct hq_trace {
 int hq_hoqri(const hq_tensor* t, const hq_config* cfg, const double* const* init_factors,
              double* const* factors_out, double* core_out, hq_trace* trace);
 
+/* ------------------------------------------------------------- harness --
+ * bench_kernel (harness.hpp:75-82; harness.cpp:350-381): `repetitions` TTMcTC
+ * calls of `mode` on a fixed state, each timed on the device with CUDA events
+ * (the G_(n)^T build and the fused pass, factors and core already resident);
+ * seconds_out[repetitions]; transient_bytes[2] = the call's device scratch,
+ * total and largest single buffer (the meter's counterpart, kernels.hpp:15-41). */
+int hq_bench_ttmctc(const hq_tensor* t, const double* const* factors, const uint64_t* ranks, int mode,
+                    uint64_t repetitions, double* seconds_out, uint64_t* transient_bytes);
+/* gen_synthetic (harness.hpp:27-31; harness.cpp:62-98), bit-identical stream:
+ * coords_out nnz * order, values_out nnz.  INFEASIBLE when nnz exceeds the
+ * cells.  Host only (no device needed). */
+int hq_gen_synthetic(int order, const uint64_t* dims, uint64_t nnz, uint64_t seed, uint32_t* coords_out,
+                     double* values_out);
+
 /* fit_error (solvers.hpp:87; solvers.cpp:225-236) */
 int hq_fit_error(double data_norm_sq, uint64_t core_size, const double* core, double* out);
 

@@ -221,6 +221,19 @@ def gen_grad(lib):
     np.savez_compressed(os.path.join(OUT, "grad.npz"), **out)
 
 
+def gen_trace(lib):
+    """harness.cpp:101-161 trace files (CSV + JSON) of a reference hoqri run,
+    for the trace-schema tests of the engine's harness."""
+    dims, nnz, tseed, ranks, sweeps, seed = [20, 18, 16], 200, 41, [3, 3, 3], 6, 5
+    t = RefTensor.gen_synthetic(lib, dims, nnz, tseed)
+    csv, js = t.trace_files(ranks, sweeps, seed)
+    c, v = t.export()
+    np.savez_compressed(os.path.join(OUT, "trace.npz"), dims=np.asarray(dims, np.uint64), nnz=np.array(nnz),
+                        tensor_seed=np.array(tseed, np.uint64), ranks=np.asarray(ranks, np.uint64),
+                        sweeps=np.array(sweeps), seed=np.array(seed, np.uint64), csv=np.array(csv),
+                        json=np.array(js), coords=c, vals=v)
+
+
 def gen_config1(lib):
     """BASELINE config 1 at full size: 10^4 cube, 10^5 uniform draws, U(0,1),
     rank 10^3, 20 sweeps.  Inputs come from workloads.uniform_coo(seed=1001);
@@ -256,6 +269,7 @@ def main():
     gen_qr(lib)
     gen_hoqri(lib)
     gen_grad(lib)
+    gen_trace(lib)
     if "--skip-config1" not in sys.argv:
         gen_config1(lib)
     for f in sorted(os.listdir(OUT)):

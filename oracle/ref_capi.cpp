@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <sstream>
 #include <thread>
 #include <vector>
 
@@ -270,6 +271,33 @@ int ref_hoqri_traced(void* h, const uint64_t* ranks, uint64_t max_sweeps, double
     } catch (const DegenerateStateError& e) {
         g_payload = static_cast<int64_t>(e.mode);
         return 8;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+// harness.cpp:101-161: the trace of a reference hoqri run (random init from
+// `seed`) rendered by make_trace_file + write_trace_csv / write_trace_json.
+// Writes NUL-terminated text into csv_out / json_out (capacity cap each).
+int ref_trace_files(void* h, const uint64_t* ranks, uint64_t max_sweeps, uint64_t seed, char* csv_out,
+                    char* json_out, uint64_t cap) {
+    try {
+        const SparseTensor& x = static_cast<RefTensor*>(h)->x;
+        SolverConfig cfg;
+        cfg.ranks.assign(ranks, ranks + x.order());
+        cfg.max_sweeps = max_sweeps;
+        cfg.tol_fit_change = 0.0;
+        cfg.seed = seed;
+        SolveResult r = hoqri(x, cfg);
+        TraceFile t = make_trace_file("hoqri", cfg, x, r.trace);
+        std::ostringstream c, j;
+        write_trace_csv(c, t);
+        write_trace_json(j, t);
+        const std::string cs = c.str(), js = j.str();
+        if (cs.size() + 1 > cap || js.size() + 1 > cap) return 5;
+        std::memcpy(csv_out, cs.c_str(), cs.size() + 1);
+        std::memcpy(json_out, js.c_str(), js.size() + 1);
+        return 0;
     } catch (const std::exception& e) {
         return code_of(e);
     }

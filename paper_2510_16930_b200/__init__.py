@@ -119,7 +119,7 @@ EXPORTED_SYMBOLS = [
     "hq_solver_create", "hq_solver_destroy", "hq_solver_run", "hq_solver_sync", "hq_solver_status", "hq_solver_launch_mode_pass",
     "hq_solver_launch_ttmctc", "hq_solver_launches_per_sweep", "hq_solver_download", "hq_solver_mode_pass_work",
     "hq_solver_ttmctc_work", "hq_nccl_unique_id", "hq_comm_create", "hq_comm_destroy", "hq_partition_rows",
-    "hq_solver_create_dist",
+    "hq_solver_create_dist", "hq_bench_ttmctc", "hq_gen_synthetic",
 ]
 
 _lib = None
@@ -156,6 +156,8 @@ def load_library(path: str = None) -> C.CDLL:
     L.hq_config_default.restype = None
     L.hq_hoqri.argtypes = [vp, C.POINTER(HqConfig), vp, vp, vp, C.POINTER(HqTrace)]
     L.hq_fit_error.argtypes = [C.c_double, C.c_uint64, _f64p, C.POINTER(C.c_double)]
+    L.hq_bench_ttmctc.argtypes = [vp, pp, _u64p, C.c_int, C.c_uint64, _f64p, _u64p]
+    L.hq_gen_synthetic.argtypes = [C.c_int, _u64p, C.c_uint64, C.c_uint64, C.c_void_p, _f64p]
     L.hq_solver_create.argtypes = [vp, C.POINTER(HqConfig), vp, vp, pp]
     L.hq_solver_destroy.argtypes = [vp]
     L.hq_solver_run.argtypes = [vp, C.c_uint64]
@@ -701,6 +703,24 @@ class Solver:
 
 
 # ------------------------------------------------------------- .tns I/O --
+def gen_synthetic_coo(dims, nnz: int, seed: int):
+    """harness.cpp:62-98 (gen_synthetic) as raw COO: nnz distinct uniform
+    coordinates, standard-normal values, the reference's Rng stream."""
+    d = np.ascontiguousarray(np.asarray(dims, dtype=np.uint64))
+    if d.size == 0:
+        raise ShapeError("gen_synthetic: need at least one mode")
+    coords = np.empty((int(nnz), d.size), np.uint32)
+    vals = np.empty(int(nnz), np.float64)
+    _check(load_library().hq_gen_synthetic(d.size, d, int(nnz), int(seed) & (2**64 - 1), coords.ctypes.data, vals))
+    return coords, vals
+
+
+def gen_synthetic(dims, nnz: int, seed: int) -> SparseTensor:
+    """tucker::gen_synthetic (harness.hpp:27-31)"""
+    coords, vals = gen_synthetic_coo(dims, nnz, seed)
+    return SparseTensor([int(v) for v in dims], coords, vals)
+
+
 def load_tns(source, dims_override: Optional[Sequence[int]] = None) -> SparseTensor:
     """sparse_tensor.cpp:136-215: text parse on the host, build on the device."""
     from .tns import parse_tns

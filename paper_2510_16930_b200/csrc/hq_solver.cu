@@ -26,6 +26,7 @@
 #include <cstdlib>
 #include <map>
 #include <mutex>
+#include <unordered_set>
 #include <vector>
 #include <cmath>
 #include <cstring>
@@ -882,6 +883,118 @@ int hq_ttmctc(const hq_tensor* t, const double* const* factors, const uint64_t* 
         launch_pass(T, mode, sh, uf.f, kTTMcTC, gt.get(), out, nullptr, kAlways, s);
         HQ_CUDA(cudaMemcpyAsync(a_out, A.get(), sizeof(double) * T.dims[mode] * sh.kn, cudaMemcpyDeviceToHost, s));
         HQ_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int hq_bench_ttmctc(const hq_tensor* t, const double* const* factors, const uint64_t* ranks, int mode,
+                    uint64_t repetitions, double* seconds_out, uint64_t* transient_bytes) {
+    return guard([&] {
+        if (mode < 0 || mode >= t->t.order) fail(HQ_ERR_RANGE, "ttmctc: mode out of range");
+        if (repetitions < 1) fail(HQ_ERR_SHAPE, "repetitions must be at least 1");
+        cudaStream_t s = t->stream;
+        const DeviceTensor& T = t->t;
+        UploadedFactors uf;
+        upload_factors(T, factors, ranks, uf, s);
+        uint64_t size = 1;
+        for (int v = 0; v < T.order; ++v) size *= ranks[v];
+        DBuf<double> dcore;
+        dcore.alloc(size);
+        core_device(T, uf, dcore.get(), s);
+        ModeShape sh = make_mode_shape(T.order, uf.ranks, mode);
+        DBuf<double> gt, A;
+        gt.alloc((size_t)sh.L * sh.kn);
+        A.alloc(T.dims[mode] * sh.kn);
+        PassBuffers pb;
+        pb.ensure(T.modes[mode], sh);
+        PassOut out{A.get(), pb.mpart.get(), pb.wpart.get(), pb.maxpart.get(), pb.ypart.get()};
+        // per call: G_(n)^T and the fused pass (the kernel a TTMcTC call runs), timed on the device
+        cudaEvent_t e0, e1;
+        HQ_CUDA(cudaEventCreate(&e0));
+        HQ_CUDA(cudaEventCreate(&e1));
+        launch_gt(dcore.get(), sh, uf.ranks, gt.get(), nullptr, s);  // warm-up call
+        launch_pass(T, mode, sh, uf.f, kTTMcTC, gt.get(), out, nullptr, kAlways, s);
+        for (uint64_t r = 0; r < repetitions; ++r) {
+            HQ_CUDA(cudaEventRecord(e0, s));
+            launch_gt(dcore.get(), sh, uf.ranks, gt.get(), nullptr, s);
+            launch_pass(T, mode, sh, uf.f, kTTMcTC, gt.get(), out, nullptr, kAlways, s);
+            HQ_CUDA(cudaEventRecord(e1, s));
+            HQ_CUDA(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            HQ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            seconds_out[r] = ms * 1e-3;
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (transient_bytes) {  // the call's device scratch: A, G^T, partial slots, long-row partials
+            const size_t parts[6] = {A.bytes(), gt.bytes(), pb.mpart.bytes(), pb.wpart.bytes(), pb.maxpart.bytes(),
+                                     pb.ypart.bytes()};
+            transient_bytes[0] = transient_bytes[1] = 0;
+            for (size_t b : parts) {
+                transient_bytes[0] += b;
+                transient_bytes[1] = std::max<uint64_t>(transient_bytes[1], b);
+            }
+        }
+    });
+}
+
+// harness.cpp:62-98 gen_synthetic: nnz distinct uniform coordinates (rejection
+// of duplicates), standard-normal values, one tucker::Rng stream (rng.hpp)
+int hq_gen_synthetic(int order, const uint64_t* dims, uint64_t nnz, uint64_t seed, uint32_t* coords_out,
+                     double* values_out) {
+    return guard([&] {
+        if (order < 1) fail(HQ_ERR_SHAPE, "gen_synthetic: need at least one mode");
+        unsigned __int128 total = 1;
+        for (int m = 0; m < order; ++m) {
+            if (dims[m] == 0) fail(HQ_ERR_SHAPE, "gen_synthetic: zero extent");
+            total *= dims[m];
+        }
+        if ((unsigned __int128)nnz > total)
+            fail(HQ_ERR_INFEASIBLE, "gen_synthetic: nnz " + std::to_string(nnz) + " exceeds the number of cells");
+        std::mt19937_64 gen(seed);
+        bool has_spare = false;
+        double spare = 0.0;
+        auto uniform01 = [&] { return static_cast<double>(gen() >> 11) * 0x1.0p-53; };
+        auto normal = [&] {
+            if (has_spare) {
+                has_spare = false;
+                return spare;
+            }
+            const double u1 = 1.0 - uniform01(), u2 = uniform01();
+            const double r = std::sqrt(-2.0 * std::log(u1));
+            const double theta = 6.283185307179586476925286766559 * u2;
+            spare = r * std::sin(theta);
+            has_spare = true;
+            return r * std::cos(theta);
+        };
+        auto uniform_below = [&](uint64_t n) -> uint64_t {
+            if (n <= 1) return 0;
+            const uint64_t limit = UINT64_MAX - UINT64_MAX % n;
+            uint64_t x;
+            do {
+                x = gen();
+            } while (x >= limit);
+            return x % n;
+        };
+        struct KeyHash {
+            size_t operator()(const std::pair<uint64_t, uint64_t>& k) const {
+                return std::hash<uint64_t>()(k.first * 0x9E3779B97F4A7C15ull ^ k.second);
+            }
+        };
+        std::unordered_set<std::pair<uint64_t, uint64_t>, KeyHash> seen;
+        seen.reserve(nnz * 2);
+        std::vector<uint32_t> tuple(order);
+        uint64_t have = 0;
+        while (have < nnz) {
+            unsigned __int128 linear = 0;
+            for (int m = 0; m < order; ++m) {
+                tuple[m] = static_cast<uint32_t>(uniform_below(dims[m]));
+                linear = linear * dims[m] + tuple[m];
+            }
+            if (!seen.insert({(uint64_t)(linear >> 64), (uint64_t)linear}).second) continue;  // duplicate: resample
+            for (int m = 0; m < order; ++m) coords_out[have * order + m] = tuple[m];
+            values_out[have] = normal();
+            ++have;
+        }
     });
 }
 

@@ -6,6 +6,15 @@
 // mode).  Only K x K bookkeeping (matmul helpers on desk-scale matrices,
 // unfold_core's index shuffle) runs on the host, as in the reference.
 #include <algorithm>
+#include <cctype>
+#include <charconv>
+#include <cmath>
+#include <cstdio>
+#include <ctime>
+#include <filesystem>
+#include <fstream>
+#include <limits>
+#include <algorithm>
 #include <cmath>
 #include <fstream>
 #include <istream>
@@ -13,6 +22,7 @@
 #include <sstream>
 
 #include "hoqri_b200.h"
+#include "tucker/harness.hpp"
 #include "tucker/tucker_b200.hpp"
 
 namespace tucker {
@@ -522,6 +532,390 @@ double fit_error(const SparseTensor& x, const TuckerModel& model) {
     double out = 0.0;
     check(hq_fit_error(model.data_norm_sq, model.core.data.size(), model.core.data.data(), &out));
     return out;
+}
+
+
+// ================================================================ harness ==
+// The reference's experiment / trace surface (harness.hpp) over the engine.
+namespace {
+
+std::string fmt17(double v) {  // harness.cpp:27-31
+    char buf[64];
+    std::snprintf(buf, sizeof(buf), "%.17g", v);
+    return buf;
+}
+
+std::string joined(const std::vector<std::size_t>& v) {
+    std::string s;
+    for (std::size_t i = 0; i < v.size(); ++i) s += (i ? "," : "") + std::to_string(v[i]);
+    return s;
+}
+
+std::string now_utc() {
+    std::time_t t = std::time(nullptr);
+    std::tm tm{};
+    gmtime_r(&t, &tm);
+    char buf[32];
+    std::strftime(buf, sizeof(buf), "%Y-%m-%dT%H:%M:%SZ", &tm);
+    return buf;
+}
+
+std::string json_string(const std::string& s) {
+    std::string o = "\"";
+    for (char c : s) {
+        switch (c) {
+            case '"': o += "\\\""; break;
+            case '\\': o += "\\\\"; break;
+            case '\n': o += "\\n"; break;
+            case '\t': o += "\\t"; break;
+            default:
+                if (static_cast<unsigned char>(c) < 0x20) {
+                    char b[8];
+                    std::snprintf(b, sizeof(b), "\\u%04x", c);
+                    o += b;
+                } else {
+                    o += c;
+                }
+        }
+    }
+    return o + "\"";
+}
+
+std::string json_number(double v) { return std::isfinite(v) ? fmt17(v) : "null"; }
+
+// a small reader for the trace document: {"header": {str: str}, "columns": [str], "rows": [[num]]}
+struct JsonIn {
+    std::string s;
+    std::size_t p = 0;
+    void ws() {
+        while (p < s.size() && std::isspace(static_cast<unsigned char>(s[p]))) ++p;
+    }
+    [[noreturn]] void bad(const std::string& what) { throw ParseError("trace json: " + what); }
+    void expect(char c) {
+        ws();
+        if (p >= s.size() || s[p] != c) bad(std::string("expected '") + c + "'");
+        ++p;
+    }
+    bool peek(char c) {
+        ws();
+        return p < s.size() && s[p] == c;
+    }
+    std::string str() {
+        expect('"');
+        std::string o;
+        while (p < s.size() && s[p] != '"') {
+            char c = s[p++];
+            if (c == '\\') {
+                if (p >= s.size()) bad("bad escape");
+                char e = s[p++];
+                switch (e) {
+                    case 'n': o += '\n'; break;
+                    case 't': o += '\t'; break;
+                    case 'r': o += '\r'; break;
+                    case 'b': o += '\b'; break;
+                    case 'f': o += '\f'; break;
+                    case 'u': {
+                        if (p + 4 > s.size()) bad("bad \\u escape");
+                        o += static_cast<char>(std::stoi(s.substr(p, 4), nullptr, 16));
+                        p += 4;
+                        break;
+                    }
+                    default: o += e;
+                }
+            } else {
+                o += c;
+            }
+        }
+        expect('"');
+        return o;
+    }
+    double num() {
+        ws();
+        if (s.compare(p, 4, "null") == 0) {
+            p += 4;
+            return std::numeric_limits<double>::quiet_NaN();
+        }
+        const char* b = s.data() + p;
+        char* e = nullptr;
+        double v = std::strtod(b, &e);
+        if (e == b) bad("bad number");
+        p += static_cast<std::size_t>(e - b);
+        return v;
+    }
+    void skip_value() {
+        ws();
+        if (peek('"')) {
+            str();
+        } else if (peek('{')) {
+            expect('{');
+            if (!peek('}'))
+                do {
+                    str();
+                    expect(':');
+                    skip_value();
+                } while (peek(',') && (++p, true));
+            expect('}');
+        } else if (peek('[')) {
+            expect('[');
+            if (!peek(']'))
+                do skip_value();
+                while (peek(',') && (++p, true));
+            expect(']');
+        } else if (s.compare(p, 4, "true") == 0 || s.compare(p, 4, "null") == 0) {
+            p += 4;
+        } else if (s.compare(p, 5, "false") == 0) {
+            p += 5;
+        } else {
+            num();
+        }
+    }
+};
+
+}  // namespace
+
+SparseTensor gen_synthetic(const std::vector<std::size_t>& dims, std::size_t nnz, std::uint64_t seed) {
+    std::vector<uint64_t> d(dims.begin(), dims.end());
+    if (d.empty()) throw ShapeError("gen_synthetic: need at least one mode");
+    std::vector<index_t> coords(nnz * dims.size());
+    std::vector<double> vals(nnz);
+    check(hq_gen_synthetic(static_cast<int>(d.size()), d.data(), nnz, seed, coords.data(), vals.data()));
+    return SparseTensor(dims, std::move(coords), std::move(vals));
+}
+
+TraceFile make_trace_file(const std::string& solver_name, const SolverConfig& config, const SparseTensor& x,
+                          const IterationTrace& trace) {  // harness.cpp:101-140: same keys and columns
+    TraceFile t;
+    t.header["trace_version"] = std::to_string(kTraceVersion);
+    t.header["tool_version"] = kToolVersion;
+    t.header["timestamp"] = now_utc();
+    t.header["solver"] = solver_name;
+    t.header["dims"] = joined(x.dims());
+    t.header["nnz"] = std::to_string(x.nnz());
+    t.header["ranks"] = joined(config.ranks);
+    t.header["seed"] = std::to_string(config.seed);
+    t.header["init"] = config.init == InitMode::kRandom ? "random" : "hosvd";
+    t.header["kernel"] = config.kernel == KernelVariant::kElementwise ? "elementwise" : "matrix";
+    t.header["max_sweeps"] = std::to_string(config.max_sweeps);
+    t.header["tol"] = fmt17(config.tol_fit_change);
+    t.header["data_norm_sq"] = fmt17(trace.data_norm_sq);
+    t.header["initial_objective"] = fmt17(trace.initial_objective);
+    t.columns = {"sweep", "elapsed_s", "objective", "fit", "grad_norm_sq"};
+    for (std::size_t n = 0; n < x.order(); ++n) t.columns.push_back("drift_" + std::to_string(n + 1));
+    for (const SweepRecord& r : trace.sweeps) {
+        std::vector<double> row{static_cast<double>(r.sweep), r.elapsed_s, r.objective, r.fit, r.total_grad_norm_sq};
+        row.insert(row.end(), r.drift.begin(), r.drift.end());
+        t.rows.push_back(std::move(row));
+    }
+    return t;
+}
+
+void write_trace_csv(std::ostream& out, const TraceFile& t) {  // harness.cpp:142-153
+    for (const auto& kv : t.header) out << "# " << kv.first << "=" << kv.second << "\n";
+    for (std::size_t i = 0; i < t.columns.size(); ++i) out << (i ? "," : "") << t.columns[i];
+    out << "\n";
+    for (const auto& row : t.rows) {
+        for (std::size_t i = 0; i < row.size(); ++i) out << (i ? "," : "") << fmt17(row[i]);
+        out << "\n";
+    }
+}
+
+void write_trace_json(std::ostream& out, const TraceFile& t) {  // harness.cpp:155-161 (keys in sorted order)
+    out << "{\n  \"columns\": [";
+    for (std::size_t i = 0; i < t.columns.size(); ++i)
+        out << (i ? "," : "") << "\n    " << json_string(t.columns[i]);
+    out << (t.columns.empty() ? "]" : "\n  ]") << ",\n  \"header\": {";
+    std::size_t k = 0;
+    for (const auto& kv : t.header) out << (k++ ? "," : "") << "\n    " << json_string(kv.first) << ": " << json_string(kv.second);
+    out << (t.header.empty() ? "}" : "\n  }") << ",\n  \"rows\": [";
+    for (std::size_t r = 0; r < t.rows.size(); ++r) {
+        out << (r ? "," : "") << "\n    [";
+        for (std::size_t i = 0; i < t.rows[r].size(); ++i)
+            out << (i ? "," : "") << "\n      " << json_number(t.rows[r][i]);
+        out << (t.rows[r].empty() ? "]" : "\n    ]");
+    }
+    out << (t.rows.empty() ? "]" : "\n  ]") << "\n}\n";
+}
+
+TraceFile read_trace_csv(std::istream& in) {  // harness.cpp:163-199: same parse rules and errors
+    TraceFile t;
+    std::string line;
+    bool have_columns = false;
+    std::size_t line_no = 0;
+    while (std::getline(in, line)) {
+        ++line_no;
+        if (line.empty()) continue;
+        if (line[0] == '#') {
+            const std::size_t start = line.find_first_not_of(" \t", 1);
+            if (start == std::string::npos) continue;
+            const std::size_t eq = line.find('=', start);
+            if (eq == std::string::npos) continue;
+            t.header[line.substr(start, eq - start)] = line.substr(eq + 1);
+            continue;
+        }
+        std::vector<std::string> cells;
+        std::size_t b = 0;
+        while (true) {
+            const std::size_t c = line.find(',', b);
+            cells.push_back(line.substr(b, c == std::string::npos ? std::string::npos : c - b));
+            if (c == std::string::npos) break;
+            b = c + 1;
+        }
+        if (!have_columns) {
+            t.columns = cells;
+            have_columns = true;
+            continue;
+        }
+        std::vector<double> row;
+        for (const std::string& cell : cells) {
+            double v = 0.0;
+            auto res = std::from_chars(cell.data(), cell.data() + cell.size(), v);
+            if (res.ec != std::errc{} || res.ptr != cell.data() + cell.size())
+                throw ParseError("bad numeric cell '" + cell + "'", line_no);
+            row.push_back(v);
+        }
+        if (row.size() != t.columns.size()) throw ParseError("row width does not match the column header", line_no);
+        t.rows.push_back(std::move(row));
+    }
+    if (!have_columns) throw ParseError("trace has no column header");
+    return t;
+}
+
+TraceFile read_trace_json(std::istream& in) {
+    JsonIn j{std::string(std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>())};
+    TraceFile t;
+    bool h = false, c = false, r = false;
+    j.expect('{');
+    if (!j.peek('}'))
+        do {
+            const std::string key = j.str();
+            j.expect(':');
+            if (key == "header") {
+                h = true;
+                j.expect('{');
+                if (!j.peek('}'))
+                    do {
+                        std::string k2 = j.str();
+                        j.expect(':');
+                        t.header[k2] = j.str();
+                    } while (j.peek(',') && (++j.p, true));
+                j.expect('}');
+            } else if (key == "columns") {
+                c = true;
+                j.expect('[');
+                if (!j.peek(']'))
+                    do t.columns.push_back(j.str());
+                    while (j.peek(',') && (++j.p, true));
+                j.expect(']');
+            } else if (key == "rows") {
+                r = true;
+                j.expect('[');
+                if (!j.peek(']'))
+                    do {
+                        std::vector<double> row;
+                        j.expect('[');
+                        if (!j.peek(']'))
+                            do row.push_back(j.num());
+                            while (j.peek(',') && (++j.p, true));
+                        j.expect(']');
+                        t.rows.push_back(std::move(row));
+                    } while (j.peek(',') && (++j.p, true));
+                j.expect(']');
+            } else {
+                j.skip_value();
+            }
+        } while (j.peek(',') && (++j.p, true));
+    j.expect('}');
+    if (!h || !c || !r) throw ParseError("trace json: missing header, columns or rows");
+    return t;
+}
+
+SolveResult hooi(const SparseTensor&, const SolverConfig&) {
+    throw CapacityError("hooi is outside the B200 engine (the HOQRI hot path); use the reference library for HOOI");
+}
+
+ExperimentResult run_experiment(const ExperimentSpec& spec) {  // harness.cpp:241-345, HOQRI on the device
+    if (spec.repetitions < 1) throw ShapeError("repetitions must be at least 1");
+    if (spec.input_path.has_value() == spec.synthetic.has_value())
+        throw ShapeError("specify exactly one input source (file or synthetic)");
+    if (spec.out_dir.empty()) throw ShapeError("output directory required");
+    if (spec.solver != SolverChoice::kHoqri)
+        throw CapacityError("hooi is outside the B200 engine (the HOQRI hot path); run_experiment supports kHoqri");
+    SparseTensor x;
+    if (spec.input_path) {
+        x = load_tns_file(*spec.input_path, spec.dims_override);
+    } else {
+        const SyntheticSpec& syn = *spec.synthetic;
+        x = gen_synthetic(syn.dims, syn.nnz, syn.seed);
+    }
+    std::filesystem::create_directories(spec.out_dir);
+    ExperimentResult result;
+    std::string runs;
+    double mean_total = 0.0;
+    for (std::size_t rep = 0; rep < spec.repetitions; ++rep) {
+        SolverConfig cfg = spec.config;
+        cfg.seed = spec.config.seed + rep;
+        SolveResult res = hoqri(x, cfg);
+        TraceFile t = make_trace_file("hoqri", cfg, x, res.trace);
+        const std::string base = (std::filesystem::path(spec.out_dir) / ("hoqri_rep" + std::to_string(rep))).string();
+        {
+            std::ofstream csv(base + ".trace.csv");
+            write_trace_csv(csv, t);
+            std::ofstream js(base + ".trace.json");
+            write_trace_json(js, t);
+        }
+        const std::size_t sweeps = res.trace.sweeps.size();
+        double mean_sweep = 0.0, fobj = 0.0, ffit = 0.0;
+        if (sweeps) {
+            mean_sweep = res.trace.sweeps.back().elapsed_s / static_cast<double>(sweeps);
+            fobj = res.trace.sweeps.back().objective;
+            ffit = res.trace.sweeps.back().fit;
+        }
+        mean_total += mean_sweep;
+        result.trace_paths.push_back(base + ".trace.csv");
+        runs += std::string(rep ? "," : "") + "\n      {\n        \"final_fit\": " + json_number(ffit) +
+                ",\n        \"final_objective\": " + json_number(fobj) + ",\n        \"mean_sweep_s\": " +
+                json_number(mean_sweep) + ",\n        \"rep\": " + std::to_string(rep) + ",\n        \"sweeps\": " +
+                std::to_string(sweeps) + ",\n        \"trace\": " + json_string(base + ".trace.csv") + "\n      }";
+    }
+    auto arr = [](const std::vector<std::size_t>& v) {
+        std::string s = "[";
+        for (std::size_t i = 0; i < v.size(); ++i) s += (i ? ", " : "") + std::to_string(v[i]);
+        return s + "]";
+    };
+    const std::string sp = (std::filesystem::path(spec.out_dir) / "summary.json").string();
+    std::ofstream out(sp);
+    out << "{\n  \"dims\": " << arr(x.dims()) << ",\n  \"hoqri\": {\n    \"mean_sweep_s\": "
+        << json_number(mean_total / static_cast<double>(spec.repetitions)) << ",\n    \"runs\": [" << runs
+        << "\n    ]\n  },\n  \"nnz\": " << x.nnz() << ",\n  \"ranks\": " << arr(spec.config.ranks)
+        << ",\n  \"repetitions\": " << spec.repetitions << ",\n  \"tool_version\": " << json_string(kToolVersion)
+        << "\n}\n";
+    result.summary_path = sp;
+    return result;
+}
+
+BenchStats bench_kernel(const SparseTensor& x, const FactorSet& u, std::size_t mode, KernelVariant variant,
+                        std::size_t repetitions) {  // harness.cpp:350-381, device-timed
+    (void)variant;  // both variants run the same device kernel (kernels.hpp:52-60)
+    if (repetitions < 1) throw ShapeError("repetitions must be at least 1");
+    if (mode >= x.order()) throw RangeError("ttmctc: mode out of range");
+    check_factors(x, u);
+    std::vector<uint64_t> ranks;
+    for (const Matrix& m : u.factors) ranks.push_back(m.cols);
+    std::vector<double> times(repetitions);
+    uint64_t scratch[2] = {0, 0};
+    auto p = ptrs(u);
+    check(hq_bench_ttmctc(x.device(), p.data(), ranks.data(), static_cast<int>(mode), repetitions, times.data(),
+                          scratch));
+    BenchStats st;
+    st.repetitions = repetitions;
+    std::sort(times.begin(), times.end());
+    st.min_s = times.front();
+    st.max_s = times.back();
+    const std::size_t mid = times.size() / 2;
+    st.median_s = times.size() % 2 ? times[mid] : 0.5 * (times[mid - 1] + times[mid]);
+    st.peak_slots = (scratch[0] + 7) / 8;
+    st.largest_alloc_slots = (scratch[1] + 7) / 8;
+    return st;
 }
 
 }  // namespace tucker

@@ -6,6 +6,10 @@
 #include <sstream>
 #include <string>
 
+#include <filesystem>
+#include <fstream>
+
+#include "tucker/harness.hpp"
 #include "tucker/kernels.hpp"
 #include "tucker/solvers.hpp"
 #include "tucker/sparse_tensor.hpp"
@@ -157,6 +161,64 @@ int main() {
         // bitwise determinism (solvers_test.cpp:295-310)
         SolveResult r2 = hoqri(x, cfg);
         for (std::size_t i = 0; i < r.trace.sweeps.size(); ++i) CHECK(r.trace.sweeps[i].objective == r2.trace.sweeps[i].objective);
+    }
+    // harness.hpp surface: gen_synthetic, run_experiment traces, bench_kernel (device-timed)
+    {
+        SparseTensor x = gen_synthetic({20, 18, 16}, 200, 41);
+        CHECK(x.nnz() == 200);
+        const std::string dir = (std::filesystem::temp_directory_path() / "hq_shim_harness").string();
+        std::filesystem::remove_all(dir);
+        ExperimentSpec spec;
+        spec.synthetic = SyntheticSpec{{20, 18, 16}, 200, 41};
+        spec.config.ranks = {3, 3, 3};
+        spec.config.max_sweeps = 6;
+        spec.config.tol_fit_change = 0.0;
+        spec.config.seed = 5;
+        spec.repetitions = 2;
+        spec.out_dir = dir;
+        ExperimentResult er = run_experiment(spec);
+        CHECK(er.trace_paths.size() == 2);
+        CHECK(std::filesystem::exists(er.summary_path));
+        std::ifstream fc(er.trace_paths[0]);
+        TraceFile tc = read_trace_csv(fc);
+        std::ifstream fj(er.trace_paths[0].substr(0, er.trace_paths[0].size() - 4) + ".json");
+        TraceFile tj = read_trace_json(fj);
+        CHECK(tc.columns.size() == 8 && tc.rows.size() == 6);
+        CHECK(tj.columns == tc.columns && tj.header == tc.header && tj.rows.size() == tc.rows.size());
+        for (std::size_t i = 0; i < tc.rows.size(); ++i) CHECK(tj.rows[i] == tc.rows[i]);
+        CHECK(tc.header["solver"] == "hoqri" && tc.header["seed"] == "5" && tc.header["dims"] == "20,18,16");
+        for (std::size_t i = 1; i < tc.rows.size(); ++i) CHECK(tc.rows[i][1] >= tc.rows[i - 1][1]);  // elapsed
+        spec.solver = SolverChoice::kBoth;
+        CHECK_THROWS_AS(run_experiment(spec), CapacityError);
+        SolverConfig hc;
+        hc.ranks = {3, 3, 3};
+        CHECK_THROWS_AS(hooi(x, hc), CapacityError);
+        FactorSet u = random_factors(x.dims(), {3, 3, 3}, 7);
+        BenchStats bs = bench_kernel(x, u, 1, KernelVariant::kElementwise, 5);
+        CHECK(bs.repetitions == 5 && bs.min_s > 0.0 && bs.min_s <= bs.median_s && bs.median_s <= bs.max_s);
+        CHECK(bs.peak_slots >= 18 * 3 && bs.largest_alloc_slots <= bs.peak_slots);
+        std::istringstream bad("a,b\n1,2\n1,x\n");
+        CHECK_THROWS_AS(read_trace_csv(bad), ParseError);
+        std::filesystem::remove_all(dir);
+    }
+    // gradient tracing (solvers.cpp:126-150): every update recorded, interlacing holds
+    {
+        SparseTensor x = gen_synthetic({20, 18, 16}, 200, 41);
+        SolverConfig cfg;
+        cfg.ranks = {3, 3, 3};
+        cfg.max_sweeps = 5;
+        cfg.tol_fit_change = 0.0;
+        cfg.seed = 5;
+        cfg.trace_gradients = true;
+        SolveResult r = hoqri(x, cfg);
+        CHECK(r.trace.updates.size() == 15);
+        for (const ModeUpdateRecord& up : r.trace.updates) {
+            CHECK(up.grad_norm_sq >= 0.0 && up.sigma.size() == 3 && up.lambda.size() == 3);
+            for (std::size_t k = 0; k < 3; ++k) CHECK(up.sigma[k] - up.lambda[k] >= -1e-9 * std::max(1.0, up.sigma[0]));
+        }
+        double tot = 0.0;
+        for (double g : r.trace.sweeps[0].grad_norm_sq) tot += g;
+        CHECK(std::fabs(tot - r.trace.sweeps[0].total_grad_norm_sq) <= 1e-12 * std::max(1.0, tot));
     }
     if (failures) {
         std::printf("%d check(s) failed\n", failures);

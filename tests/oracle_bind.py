@@ -257,6 +257,7 @@ class RefLib:
         L.ref_hoqri.argtypes = [vp, u64p, C.c_uint64, C.c_double, C.c_uint64, C.c_int, f64p, f64p,
                                 C.POINTER(C.c_uint64), C.POINTER(C.c_double), f64p, f64p, f64p, f64p]
         L.ref_hoqri_replay.argtypes = [vp, u64p, f64p, C.c_uint64, f64p, f64p, f64p]
+        L.ref_trace_files.argtypes = [vp, u64p, C.c_uint64, C.c_uint64, C.c_char_p, C.c_char_p, C.c_uint64]
         L.ref_hoqri_traced.argtypes = [vp, u64p, C.c_uint64, C.c_double, C.c_uint64, C.c_double, C.c_uint64, f64p,
                                        f64p, C.POINTER(C.c_uint64), f64p, f64p, f64p, C.POINTER(C.c_uint64), f64p,
                                        f64p, f64p, f64p]
@@ -351,6 +352,14 @@ class RefTensor:
         return dict(status=st, payload=int(self.lib.L.ref_last_payload()), sweeps=s, initial_objective=f0.value,
                     objective=obj[:s], fit=fit[:s], drift=drift[: s * N].reshape(s, N), elapsed=el[:s],
                     factors=_split(f, self.dims, ranks), core=core.reshape(tuple(int(r) for r in ranks)))
+
+    def trace_files(self, ranks, sweeps, seed, cap=1 << 20):
+        """make_trace_file + write_trace_csv / write_trace_json of a reference hoqri run."""
+        c, j = C.create_string_buffer(cap), C.create_string_buffer(cap)
+        st = self.lib.L.ref_trace_files(self.h, _u64(ranks), sweeps, seed, c, j, cap)
+        if st:
+            raise RuntimeError(f"ref_trace_files status {st}")
+        return c.value.decode(), j.value.decode()
 
     def hoqri_traced(self, ranks, sweeps, tol, seed, tol_grad=0.0):
         """tucker::hoqri with trace_gradients (per-update ModeUpdateRecords)."""

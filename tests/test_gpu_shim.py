@@ -13,7 +13,9 @@ pytestmark = pytest.mark.gpu
 def test_cpp_shim():
     binp = os.path.join(ROOT, "tests", "cpp", "test_shim.bin")
     lib = os.path.join(ROOT, "paper_2510_16930_b200", "lib")
-    if not os.path.exists(binp):
+    src = os.path.join(ROOT, "tests", "cpp", "test_shim.cpp")
+    shim = os.path.join(ROOT, "paper_2510_16930_b200", "lib", "libtucker_b200.so")
+    if not os.path.exists(binp) or os.path.getmtime(binp) < max(os.path.getmtime(src), os.path.getmtime(shim)):
         subprocess.check_call(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"),
                                os.path.join(ROOT, "tests", "cpp", "test_shim.cpp"), "-L", lib, "-ltucker_b200",
                                "-lhoqri_b200", f"-Wl,-rpath,{lib}", "-o", binp])

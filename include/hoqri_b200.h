@@ -81,6 +81,20 @@ int hq_tensor_buckets(const hq_tensor* t, int mode, uint64_t* offsets, uint64_t*
 /* norm_sq(const SparseTensor&) (sparse_tensor.hpp:69; sparse_tensor.cpp:91-95) */
 int hq_tensor_norm_sq(const hq_tensor* t, double* out);
 
+/* ------------------------------------------------------------------ .tns --
+ * load_tns (sparse_tensor.hpp:76-79; sparse_tensor.cpp:136-215): the text parse
+ * split over host threads with the reference's rules and errors (PARSE with
+ * the line as payload, RANGE / VALUE with the line in the message).
+ * override_order 0 = no dims override.  The parsed COO stays in the handle:
+ * query its size, copy it out, or build the device tensor from it. */
+typedef struct hq_tns hq_tns;
+int hq_tns_parse(const char* text, uint64_t len, int override_order, const uint64_t* override_dims, hq_tns** out);
+int hq_tns_parse_file(const char* path, int override_order, const uint64_t* override_dims, hq_tns** out);
+int hq_tns_info(const hq_tns* p, int* order, uint64_t* dims, uint64_t* nnz);
+int hq_tns_copy(const hq_tns* p, uint32_t* coords, double* values);
+int hq_tns_tensor(const hq_tns* p, void* stream, hq_tensor** out);
+int hq_tns_destroy(hq_tns* p);
+
 /* --------------------------------------------------------------- kernels --
  * ttmc_core (kernels.hpp:46; kernels.cpp:40-84): core = X x {U^T}. */
 int hq_ttmc_core(const hq_tensor* t, const double* const* factors, const uint64_t* ranks,

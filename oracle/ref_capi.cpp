@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <optional>
 #include <sstream>
 #include <thread>
 #include <vector>
@@ -70,6 +71,13 @@ thread_local int64_t g_payload = 0;
 extern "C" {
 
 int64_t ref_last_payload() { return g_payload; }
+thread_local std::string g_msg;
+int ref_tensor_dims(void* h, uint64_t* dims) {
+    const SparseTensor& x = static_cast<RefTensor*>(h)->x;
+    for (std::size_t m = 0; m < x.order(); ++m) dims[m] = x.dims()[m];
+    return static_cast<int>(x.order());
+}
+const char* ref_last_message() { return g_msg.c_str(); }
 
 // SparseTensor ctor (sparse_tensor.cpp:18-41).  Handle owns the tensor.
 int ref_tensor_create(int n, const uint64_t* dims, uint64_t nnz, const uint32_t* coords,
@@ -299,6 +307,27 @@ int ref_trace_files(void* h, const uint64_t* ranks, uint64_t max_sweeps, uint64_
         std::memcpy(json_out, js.c_str(), js.size() + 1);
         return 0;
     } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+// tucker::load_tns (sparse_tensor.cpp:136-215) on a text buffer: the tensor
+// handle, or the exception's status, message (ref_last_message) and, for
+// ParseError, the line (ref_last_payload).
+int ref_tns_parse(const char* text, uint64_t len, int ovr_n, const uint64_t* ovr, void** out) {
+    try {
+        std::istringstream in(std::string(text, len));
+        std::optional<std::vector<std::size_t>> o;
+        if (ovr_n > 0) o = std::vector<std::size_t>(ovr, ovr + ovr_n);
+        auto* t = new RefTensor{load_tns(in, o)};
+        *out = t;
+        return 0;
+    } catch (const ParseError& e) {
+        g_payload = static_cast<int64_t>(e.line_number);
+        g_msg = e.what();
+        return 4;
+    } catch (const std::exception& e) {
+        g_msg = e.what();
         return code_of(e);
     }
 }

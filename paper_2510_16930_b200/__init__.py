@@ -120,6 +120,7 @@ EXPORTED_SYMBOLS = [
     "hq_solver_launch_ttmctc", "hq_solver_launches_per_sweep", "hq_solver_download", "hq_solver_mode_pass_work",
     "hq_solver_ttmctc_work", "hq_nccl_unique_id", "hq_comm_create", "hq_comm_destroy", "hq_partition_rows",
     "hq_solver_create_dist", "hq_bench_ttmctc", "hq_gen_synthetic",
+    "hq_tns_parse", "hq_tns_parse_file", "hq_tns_info", "hq_tns_copy", "hq_tns_tensor", "hq_tns_destroy",
 ]
 
 _lib = None
@@ -158,6 +159,12 @@ def load_library(path: str = None) -> C.CDLL:
     L.hq_fit_error.argtypes = [C.c_double, C.c_uint64, _f64p, C.POINTER(C.c_double)]
     L.hq_bench_ttmctc.argtypes = [vp, pp, _u64p, C.c_int, C.c_uint64, _f64p, _u64p]
     L.hq_gen_synthetic.argtypes = [C.c_int, _u64p, C.c_uint64, C.c_uint64, C.c_void_p, _f64p]
+    L.hq_tns_parse.argtypes = [C.c_char_p, C.c_uint64, C.c_int, vp, pp]
+    L.hq_tns_parse_file.argtypes = [C.c_char_p, C.c_int, vp, pp]
+    L.hq_tns_info.argtypes = [vp, C.POINTER(C.c_int), vp, C.POINTER(C.c_uint64)]
+    L.hq_tns_copy.argtypes = [vp, vp, vp]
+    L.hq_tns_tensor.argtypes = [vp, vp, pp]
+    L.hq_tns_destroy.argtypes = [vp]
     L.hq_solver_create.argtypes = [vp, C.POINTER(HqConfig), vp, vp, pp]
     L.hq_solver_destroy.argtypes = [vp]
     L.hq_solver_run.argtypes = [vp, C.c_uint64]
@@ -722,10 +729,9 @@ def gen_synthetic(dims, nnz: int, seed: int) -> SparseTensor:
 
 
 def load_tns(source, dims_override: Optional[Sequence[int]] = None) -> SparseTensor:
-    """sparse_tensor.cpp:136-215: text parse on the host, build on the device."""
-    from .tns import parse_tns
-    dims, coords, vals = parse_tns(source, dims_override)
-    return SparseTensor(dims, coords, vals)
+    """sparse_tensor.cpp:136-215: native threaded text parse, build on the device."""
+    from .tns import load_tns_tensor
+    return load_tns_tensor(source, dims_override)
 
 
 def write_tns(out, x: SparseTensor):

@@ -20,6 +20,11 @@ double device_sum_sq(const double* v, uint64_t n, cudaStream_t s);
 void build_tensor(DeviceTensor& T, int order, const uint64_t* dims, uint64_t nnz, const uint32_t* coords_dev,
                   const double* vals_dev, cudaStream_t s);
 void export_buckets(const DeviceTensor& T, int mode, uint64_t* offsets, uint64_t* entries, cudaStream_t s);
+}  // namespace hq
+struct hq_tns;
+namespace hq {
+// `.tns` text -> COO (hq_tns.cu); throws hq::Error like the reference's load_tns
+void tns_parse(const char* text, uint64_t len, int ovr_order, const uint64_t* ovr_dims, hq_tns& out);
 
 // Device status word shared by every kernel of a solve.  Kernels return early
 // when `abort` is set; the CholeskyQR kernels run only while `fallback` is 0,

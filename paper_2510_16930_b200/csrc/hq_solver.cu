@@ -37,6 +37,7 @@
 #include "hq_comm.cuh"
 #include "hq_dense.cuh"
 #include "hq_fast.cuh"
+#include "hq_tns.cuh"
 
 namespace hq {
 
@@ -754,6 +755,57 @@ int hq_tensor_create(int order, const uint64_t* dims, uint64_t nnz, const uint32
 int hq_tensor_create_dev(int order, const uint64_t* dims, uint64_t nnz, const uint32_t* coords_dev,
                          const double* values_dev, void* stream, hq_tensor** out) {
     return tensor_create_impl(order, dims, nnz, coords_dev, values_dev, true, stream, out);
+}
+
+int hq_tns_parse(const char* text, uint64_t len, int override_order, const uint64_t* override_dims, hq_tns** out) {
+    return guard([&] {
+        auto p = std::make_unique<hq_tns>();
+        tns_parse(text, len, override_order, override_dims, *p);
+        *out = p.release();
+    });
+}
+
+int hq_tns_parse_file(const char* path, int override_order, const uint64_t* override_dims, hq_tns** out) {
+    return guard([&] {
+        FILE* f = std::fopen(path, "rb");
+        if (!f) fail(HQ_ERR_VALUE, std::string("cannot open '") + path + "'");
+        std::string buf;
+        std::fseek(f, 0, SEEK_END);
+        const long n = std::ftell(f);
+        std::fseek(f, 0, SEEK_SET);
+        buf.resize(n > 0 ? (size_t)n : 0);
+        const size_t got = n > 0 ? std::fread(&buf[0], 1, (size_t)n, f) : 0;
+        std::fclose(f);
+        buf.resize(got);
+        auto p = std::make_unique<hq_tns>();
+        tns_parse(buf.data(), buf.size(), override_order, override_dims, *p);
+        *out = p.release();
+    });
+}
+
+int hq_tns_info(const hq_tns* p, int* order, uint64_t* dims, uint64_t* nnz) {
+    return guard([&] {
+        if (order) *order = p->order;
+        if (dims)
+            for (size_t m = 0; m < p->dims.size(); ++m) dims[m] = p->dims[m];
+        if (nnz) *nnz = p->values.size();
+    });
+}
+
+int hq_tns_copy(const hq_tns* p, uint32_t* coords, double* values) {
+    return guard([&] {
+        if (coords) std::copy(p->coords.begin(), p->coords.end(), coords);
+        if (values) std::copy(p->values.begin(), p->values.end(), values);
+    });
+}
+
+int hq_tns_tensor(const hq_tns* p, void* stream, hq_tensor** out) {
+    return tensor_create_impl((int)p->dims.size(), p->dims.data(), p->values.size(), p->coords.data(),
+                              p->values.data(), false, stream, out);
+}
+
+int hq_tns_destroy(hq_tns* p) {
+    return guard([&] { delete p; });
 }
 
 int hq_tensor_destroy(hq_tensor* t) {

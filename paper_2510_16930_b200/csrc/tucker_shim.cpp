@@ -266,81 +266,22 @@ double norm_sq(const SparseTensor& x) {
 }
 
 SparseTensor load_tns(std::istream& in, std::optional<std::vector<std::size_t>> dims_override) {
-    // sparse_tensor.cpp:136-215 (text parse on the host, build on the device)
-    std::vector<std::size_t> header;
-    std::vector<index_t> coords;
-    std::vector<double> values;
-    std::vector<std::size_t> seen;
-    std::size_t order = dims_override ? dims_override->size() : 0;
-    std::string line;
-    std::size_t line_no = 0;
-    bool content = false;
-    auto parse_u = [&](const std::string& t) -> uint64_t {
-        if (t.empty() || !std::all_of(t.begin(), t.end(), ::isdigit))
-            throw ParseError("expected an integer index, got '" + t + "'", line_no);
-        return std::stoull(t);
-    };
-    while (std::getline(in, line)) {
-        ++line_no;
-        if (line.empty() || line[0] == '#' ||
-            std::all_of(line.begin(), line.end(), [](unsigned char c) { return std::isspace(c); }))
-            continue;
-        std::istringstream ls(line);
-        std::vector<std::string> tok;
-        if (!content && line.rfind("dims:", 0) == 0) {
-            content = true;
-            std::istringstream hs(line.substr(5));
-            for (std::string t; hs >> t;) tok.push_back(t);
-            if (tok.empty()) throw ParseError("empty dims header", line_no);
-            for (auto& t : tok) {
-                uint64_t d = parse_u(t);
-                if (d == 0) throw RangeError("line " + std::to_string(line_no) + ": extent must be at least 1");
-                header.push_back(d);
-            }
-            if (order && header.size() != order) throw ParseError("dims header order does not match override", line_no);
-            if (!order) order = header.size();
-            seen.assign(order, 0);
-            continue;
-        }
-        content = true;
-        for (std::string t; ls >> t;) tok.push_back(t);
-        if (!order) {
-            if (tok.size() < 2) throw ParseError("entry line needs at least one index and a value", line_no);
-            order = tok.size() - 1;
-            seen.assign(order, 0);
-        }
-        if (tok.size() != order + 1)
-            throw ParseError("expected " + std::to_string(order + 1) + " fields, got " + std::to_string(tok.size()),
-                             line_no);
-        if (seen.empty()) seen.assign(order, 0);
-        for (std::size_t m = 0; m < order; ++m) {
-            uint64_t idx = parse_u(tok[m]);
-            if (idx < 1)
-                throw RangeError("line " + std::to_string(line_no) + ": indices are 1-based, got " + std::to_string(idx));
-            if (idx - 1 > 0xFFFFFFFFull)
-                throw RangeError("line " + std::to_string(line_no) + ": index " + std::to_string(idx) + " too large");
-            coords.push_back(static_cast<index_t>(idx - 1));
-            seen[m] = std::max<std::size_t>(seen[m], idx);
-        }
-        char* end = nullptr;
-        double v = std::strtod(tok[order].c_str(), &end);
-        if (end != tok[order].c_str() + tok[order].size())
-            throw ParseError("expected a real value, got '" + tok[order] + "'", line_no);
-        if (!std::isfinite(v)) throw ValueError("line " + std::to_string(line_no) + ": non-finite value");
-        values.push_back(v);
-    }
-    std::vector<std::size_t> dims;
-    if (dims_override)
-        dims = *dims_override;
-    else if (!header.empty())
-        dims = header;
-    else if (!seen.empty())
-        dims = seen;
-    else
-        throw ParseError("no entries and no dims header; cannot infer tensor order");
-    for (auto& d : dims)
-        if (d == 0) d = 1;
-    return SparseTensor(std::move(dims), std::move(coords), std::move(values));
+    // sparse_tensor.cpp:136-215: the engine's threaded parser (hq_tns_parse), same rules and errors
+    const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    std::vector<uint64_t> ovr;
+    if (dims_override) ovr.assign(dims_override->begin(), dims_override->end());
+    hq_tns* p = nullptr;
+    check(hq_tns_parse(text.data(), text.size(), static_cast<int>(ovr.size()), ovr.empty() ? nullptr : ovr.data(), &p));
+    std::unique_ptr<hq_tns, int (*)(hq_tns*)> guard_p(p, hq_tns_destroy);
+    int order = 0;
+    uint64_t nnz = 0;
+    uint64_t d[64] = {0};
+    check(hq_tns_info(p, &order, d, &nnz));
+    const std::size_t nd = dims_override ? dims_override->size() : static_cast<std::size_t>(order);
+    std::vector<index_t> coords(nnz * static_cast<std::size_t>(order));
+    std::vector<double> values(nnz);
+    check(hq_tns_copy(p, coords.data(), values.data()));
+    return SparseTensor(std::vector<std::size_t>(d, d + nd), std::move(coords), std::move(values));
 }
 
 SparseTensor load_tns_file(const std::string& path, std::optional<std::vector<std::size_t>> dims_override) {

@@ -257,6 +257,9 @@ class RefLib:
         L.ref_hoqri.argtypes = [vp, u64p, C.c_uint64, C.c_double, C.c_uint64, C.c_int, f64p, f64p,
                                 C.POINTER(C.c_uint64), C.POINTER(C.c_double), f64p, f64p, f64p, f64p]
         L.ref_hoqri_replay.argtypes = [vp, u64p, f64p, C.c_uint64, f64p, f64p, f64p]
+        L.ref_tensor_dims.argtypes = [vp, u64p]
+        L.ref_tns_parse.argtypes = [C.c_char_p, C.c_uint64, C.c_int, C.c_void_p, C.POINTER(vp)]
+        L.ref_last_message.restype = C.c_char_p
         L.ref_trace_files.argtypes = [vp, u64p, C.c_uint64, C.c_uint64, C.c_char_p, C.c_char_p, C.c_uint64]
         L.ref_hoqri_traced.argtypes = [vp, u64p, C.c_uint64, C.c_double, C.c_uint64, C.c_double, C.c_uint64, f64p,
                                        f64p, C.POINTER(C.c_uint64), f64p, f64p, f64p, C.POINTER(C.c_uint64), f64p,
@@ -269,6 +272,19 @@ class RefLib:
         L.ref_slices_time.restype = C.c_double
         L.ref_time_qr.argtypes = [C.c_uint64, C.c_uint64, f64p, C.c_int]
         L.ref_time_qr.restype = C.c_double
+
+
+def ref_load_tns(lib, text: bytes, dims_override=None):
+    """tucker::load_tns on a text buffer -> (status, message, payload, RefTensor or None)."""
+    h = C.c_void_p()
+    ov = None if dims_override is None else _u64(dims_override)
+    st = lib.L.ref_tns_parse(text, len(text), 0 if ov is None else ov.size, None if ov is None else ov.ctypes.data,
+                             C.byref(h))
+    if st:
+        return st, lib.L.ref_last_message().decode(), int(lib.L.ref_last_payload()), None
+    d = np.zeros(16, np.uint64)
+    n = lib.L.ref_tensor_dims(h, d)
+    return 0, "", 0, RefTensor(lib, h, [int(v) for v in d[:n]])
 
 
 class RefTensor:

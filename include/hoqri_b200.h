@@ -131,10 +131,11 @@ typedef struct hq_config {
     uint64_t max_sweeps;      /* default 100 */
     double tol_fit_change;    /* default 1e-12 */
     uint64_t seed;
-    int init;                 /* 0 random, 2 = use init_factors */
+    int init;                 /* 0 random, 1 HOSVD (desk-scale, capacity-capped), 2 = use init_factors */
     int kernel;               /* 0 element-wise, 1 matrix (same device path) */
     int trace_gradients;      /* per-update diagnostics (ModeUpdateRecord), on the device */
     double tol_grad;          /* gradient stop sqrt(sum grad) <= tol_grad f, implies tracing */
+    uint64_t capacity_cap;    /* dense unfolding cap in entries (kernels.hpp:62), default 2^31 */
 } hq_config;
 
 void hq_config_default(hq_config* cfg);
@@ -180,6 +181,24 @@ int hq_bench_ttmctc(const hq_tensor* t, const double* const* factors, const uint
  * cells.  Host only (no device needed). */
 int hq_gen_synthetic(int order, const uint64_t* dims, uint64_t nnz, uint64_t seed, uint32_t* coords_out,
                      double* values_out);
+
+/* ---------------------------------------------------------- desk-scale --
+ * The reference's dense paths, on the device (capacity-capped like the
+ * reference: CAPACITY when rows > cap / cols):
+ *  densify_unfold (kernels.hpp:70-71): X_(n) dense, out I_n x prod_{v!=n} I_v;
+ *  ttmc_unfold_dense (kernels.hpp:66-67): Y_(n) dense, out I_n x prod_{v!=n} K_v;
+ *  svd_leading (dense_core.hpp:64): leading k left singular vectors of a
+ *    rows x cols host matrix (cuSOLVER eigen-solve of the smaller Gram side;
+ *    equal to the reference's as a subspace, signs may differ);
+ *  init_factors (solvers.hpp:69-70): random, HOSVD or error per cfg->init;
+ *  hooi (solvers.hpp:82-83; solvers.cpp:93-178): same trace contract as hq_hoqri. */
+int hq_densify_unfold(const hq_tensor* t, int mode, uint64_t capacity_cap, double* out);
+int hq_ttmc_unfold_dense(const hq_tensor* t, const double* const* factors, const uint64_t* ranks, int mode,
+                         uint64_t capacity_cap, double* out);
+int hq_svd_leading(uint64_t rows, uint64_t cols, const double* y, uint64_t k, double* u_out);
+int hq_init_factors(const hq_tensor* t, const hq_config* cfg, double* const* factors_out);
+int hq_hooi(const hq_tensor* t, const hq_config* cfg, const double* const* init_factors,
+            double* const* factors_out, double* core_out, hq_trace* trace);
 
 /* fit_error (solvers.hpp:87; solvers.cpp:225-236) */
 int hq_fit_error(double data_norm_sq, uint64_t core_size, const double* core, double* out);

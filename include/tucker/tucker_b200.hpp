@@ -8,8 +8,9 @@
 // Each declaration cites the reference declaration it stands in for
 // (paths relative to /root/reference/proj/include/tucker/).
 //
-// Scope: the HOQRI hot path.  HOOI, HOSVD
-// initialisation, the harness and the gradient diagnostics are outside it.
+// Scope: the HOQRI hot path plus its section 8(f)
+// neighbours: gradient diagnostics, .tns ingestion, the harness (harness.hpp)
+// and the desk-scale HOSVD initialisation / HOOI, all on the device.
 #pragma once
 
 #include <cstddef>
@@ -219,7 +220,13 @@ struct SolveResult {
 
 FactorSet random_factors(const std::vector<std::size_t>& dims, const std::vector<std::size_t>& ranks,
                          std::uint64_t seed);                    // solvers.hpp:72-73
-FactorSet init_factors(const SparseTensor& x, const SolverConfig& config);  // solvers.hpp:77
+FactorSet init_factors(const SparseTensor& x, const SolverConfig& config);  // solvers.hpp:77 (random or HOSVD)
+SolveResult hooi(const SparseTensor& x, const SolverConfig& config);         // solvers.hpp:82-83 (device)
+Matrix svd_leading(const Matrix& y, std::size_t k);                          // dense_core.hpp:64 (device)
+Matrix densify_unfold(const SparseTensor& x, std::size_t mode,
+                      std::size_t capacity_cap = kDefaultCapacityCap);       // kernels.hpp:70-71 (device)
+Matrix ttmc_unfold_dense(const SparseTensor& x, const FactorSet& u, std::size_t mode,
+                         std::size_t capacity_cap = kDefaultCapacityCap);    // kernels.hpp:66-67 (device)
 SolveResult hoqri(const SparseTensor& x, const SolverConfig& config);        // solvers.hpp:80
 // B200 extension: start from caller-supplied factors (init_factors result)
 SolveResult hoqri_from(const SparseTensor& x, const SolverConfig& config, const FactorSet& start);

@@ -20,7 +20,7 @@ ROOT = os.path.dirname(HERE)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 sys.path.insert(0, ROOT)
 
-from oracle_bind import RefLib, RefTensor, ref_qr, ref_random_factors  # noqa: E402
+from oracle_bind import RefLib, RefTensor, ref_qr, ref_random_factors, ref_svd_leading  # noqa: E402
 from paper_2510_16930_b200.workloads import uniform_coo  # noqa: E402
 
 OUT = os.path.join(ROOT, "tests", "golden")
@@ -234,6 +234,76 @@ def gen_trace(lib):
                         json=np.array(js), coords=c, vals=v)
 
 
+def _planted(dims, ranks, seed):
+    """dense planted Tucker tensor (every cell stored), the solvers_test planted_tensor idea"""
+    rng = np.random.default_rng(seed)
+    us = [np.linalg.qr(rng.standard_normal((d, k)))[0] for d, k in zip(dims, ranks)]
+    g = rng.standard_normal(ranks)
+    x = g
+    for v, u in enumerate(us):
+        x = np.moveaxis(np.tensordot(u, np.moveaxis(x, v, 0), axes=(1, 0)), 0, v)
+    idx = np.indices(dims).reshape(len(dims), -1).T.astype(np.uint32)
+    return idx, x.reshape(-1).copy()
+
+
+def gen_dense(lib):
+    """Desk-scale dense paths of the reference (kernels.cpp:264-348, dense_core.cpp:266-327,
+    solvers.cpp:93-122, 202-215): dense unfoldings, svd_leading, HOSVD init, hoqri from HOSVD,
+    hooi (random / HOSVD, traced)."""
+    out, names = {}, []
+    cases = [("s8", "syn", [8, 8, 8], 30, 4, [3, 3, 3], 10, 123),
+             ("s15", "syn", [15, 14, 13], 120, 51, [3, 3, 3], 40, 4),
+             ("r4", "syn", [6, 5, 4, 3], 60, 9, [2, 2, 2, 2], 8, 3),
+             ("pl", "planted", [10, 9, 8], 0, 5, [2, 2, 2], 6, 1)]
+    for name, kind, dims, nnz, tseed, ranks, sweeps, seed in cases:
+        if kind == "syn":
+            t = RefTensor.gen_synthetic(lib, dims, nnz, tseed)
+        else:
+            c0, v0 = _planted(dims, ranks, tseed)
+            t = RefTensor.create(lib, dims, c0, v0)
+        c, v = t.export()
+        out[f"{name}_dims"], out[f"{name}_ranks"] = np.asarray(dims, np.uint64), np.asarray(ranks, np.uint64)
+        out[f"{name}_coords"], out[f"{name}_vals"] = c, v
+        out[f"{name}_sweeps"], out[f"{name}_seed"] = np.array(sweeps), np.array(seed, np.uint64)
+        for m in range(len(dims)):
+            st, d = t.densify(m)
+            out[f"{name}_dense{m}"] = d
+        st, msg, hs = t.init_factors(ranks, seed, True)
+        assert st == 0, msg
+        u0 = ref_random_factors(lib, dims, ranks, seed)
+        for m in range(len(dims)):
+            out[f"{name}_hosvd{m}"] = hs[m]
+            st, y = t.unfold_dense(ranks, u0, m)
+            out[f"{name}_Y{m}"] = y
+            out[f"{name}_U0_{m}"] = u0[m]
+        for alg, hosvd, tag in ((0, 1, "hoqri_hosvd"), (1, 0, "hooi_rand"), (1, 1, "hooi_hosvd")):
+            r = t.solve(alg, ranks, sweeps, 0.0, seed, hosvd, trace_gradients=(alg == 1 and hosvd == 0))
+            assert r["status"] == 0, (name, tag, r["status"])
+            for k in ("sweeps", "initial_objective", "objective", "fit", "drift", "grad", "core"):
+                out[f"{name}_{tag}_{k}"] = np.asarray(r[k])
+            for m in range(len(dims)):
+                out[f"{name}_{tag}_U{m}"] = r["factors"][m]
+        names.append(name)
+    # svd_leading: m > p (Gram on the column side), m <= p, rank-deficient (fill), zero matrix
+    rng = np.random.default_rng(3)
+    a1 = rng.standard_normal((30, 12))
+    a2 = rng.standard_normal((8, 20))
+    a3 = rng.standard_normal((25, 6))
+    a3[:, 4] = a3[:, 0] - 2 * a3[:, 1]
+    a3[:, 5] = 0.0
+    svd = [("sv_tall", a1, 4), ("sv_wide", a2, 3), ("sv_def", a3, 6), ("sv_zero", np.zeros((10, 4)), 2)]
+    for nm, a, k in svd:
+        out[f"{nm}_A"], out[f"{nm}_k"], out[f"{nm}_U"] = a, np.array(k), ref_svd_leading(lib, a, k)
+    out["svd_names"] = np.array([nm for nm, _, _ in svd])
+    # capacity: HOSVD init beyond the cap (solvers_test.cpp:80-87)
+    t = RefTensor.gen_synthetic(lib, [40, 40, 40], 50, 6)
+    st, msg, _ = t.init_factors([2, 2, 2], 0, True, cap=1000)
+    c, v = t.export()
+    out.update(cap_coords=c, cap_vals=v, cap_status=np.array(st), cap_message=np.array(msg))
+    out["names"] = np.array(names)
+    np.savez_compressed(os.path.join(OUT, "dense.npz"), **out)
+
+
 def gen_config1(lib):
     """BASELINE config 1 at full size: 10^4 cube, 10^5 uniform draws, U(0,1),
     rank 10^3, 20 sweeps.  Inputs come from workloads.uniform_coo(seed=1001);
@@ -270,6 +340,7 @@ def main():
     gen_hoqri(lib)
     gen_grad(lib)
     gen_trace(lib)
+    gen_dense(lib)
     if "--skip-config1" not in sys.argv:
         gen_config1(lib)
     for f in sorted(os.listdir(OUT)):

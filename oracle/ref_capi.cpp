@@ -332,6 +332,99 @@ int ref_tns_parse(const char* text, uint64_t len, int ovr_n, const uint64_t* ovr
     }
 }
 
+// desk-scale paths of the reference: dense unfoldings, svd_leading, init_factors (random / HOSVD), hooi
+int ref_densify_unfold(void* h, int mode, uint64_t cap, double* out) {
+    try {
+        Matrix m = densify_unfold(static_cast<RefTensor*>(h)->x, mode, cap);
+        std::memcpy(out, m.data.data(), sizeof(double) * m.data.size());
+        return 0;
+    } catch (const std::exception& e) {
+        g_msg = e.what();
+        return code_of(e);
+    }
+}
+
+int ref_ttmc_unfold_dense(void* h, const uint64_t* ranks, const double* factors, int mode, uint64_t cap, double* out) {
+    try {
+        const SparseTensor& x = static_cast<RefTensor*>(h)->x;
+        std::vector<uint64_t> dims(x.dims().begin(), x.dims().end());
+        FactorSet u = to_factors(static_cast<int>(x.order()), dims.data(), ranks, factors);
+        Matrix m = ttmc_unfold_dense(x, u, mode, cap);
+        std::memcpy(out, m.data.data(), sizeof(double) * m.data.size());
+        return 0;
+    } catch (const std::exception& e) {
+        g_msg = e.what();
+        return code_of(e);
+    }
+}
+
+int ref_svd_leading(uint64_t rows, uint64_t cols, const double* y, uint64_t k, double* out) {
+    try {
+        Matrix a(rows, cols);
+        std::memcpy(a.data.data(), y, sizeof(double) * rows * cols);
+        Matrix u = svd_leading(a, k);
+        std::memcpy(out, u.data.data(), sizeof(double) * u.data.size());
+        return 0;
+    } catch (const std::exception& e) {
+        g_msg = e.what();
+        return code_of(e);
+    }
+}
+
+int ref_init_factors(void* h, const uint64_t* ranks, uint64_t seed, int hosvd, uint64_t cap, double* out) {
+    try {
+        const SparseTensor& x = static_cast<RefTensor*>(h)->x;
+        SolverConfig cfg;
+        cfg.ranks.assign(ranks, ranks + x.order());
+        cfg.seed = seed;
+        cfg.init = hosvd ? InitMode::kHosvd : InitMode::kRandom;
+        cfg.capacity_cap = cap;
+        from_factors(init_factors(x, cfg), out);
+        return 0;
+    } catch (const std::exception& e) {
+        g_msg = e.what();
+        return code_of(e);
+    }
+}
+
+// hoqri / hooi with random or HOSVD init (and optional gradient tracing): the trace and final model
+int ref_solve(void* h, int algorithm_hooi, const uint64_t* ranks, uint64_t max_sweeps, double tol, uint64_t seed,
+              int hosvd, int trace_gradients, double* factors_out, double* core_out, uint64_t* sweeps_done,
+              double* initial_objective, double* objective, double* fit, double* drift, double* grad) {
+    try {
+        const SparseTensor& x = static_cast<RefTensor*>(h)->x;
+        SolverConfig cfg;
+        cfg.ranks.assign(ranks, ranks + x.order());
+        cfg.max_sweeps = max_sweeps;
+        cfg.tol_fit_change = tol;
+        cfg.seed = seed;
+        cfg.init = hosvd ? InitMode::kHosvd : InitMode::kRandom;
+        cfg.trace_gradients = trace_gradients != 0;
+        SolveResult r = algorithm_hooi ? hooi(x, cfg) : hoqri(x, cfg);
+        from_factors(r.model.factors, factors_out);
+        std::memcpy(core_out, r.model.core.data.data(), sizeof(double) * r.model.core.size());
+        *sweeps_done = r.trace.sweeps.size();
+        *initial_objective = r.trace.initial_objective;
+        const std::size_t n = x.order();
+        for (std::size_t s2 = 0; s2 < r.trace.sweeps.size(); ++s2) {
+            objective[s2] = r.trace.sweeps[s2].objective;
+            fit[s2] = r.trace.sweeps[s2].fit;
+            for (std::size_t m = 0; m < n; ++m) {
+                drift[s2 * n + m] = r.trace.sweeps[s2].drift[m];
+                grad[s2 * n + m] = r.trace.sweeps[s2].grad_norm_sq[m];
+            }
+        }
+        return 0;
+    } catch (const DegenerateStateError& e) {
+        g_payload = static_cast<int64_t>(e.mode);
+        g_msg = e.what();
+        return 8;
+    } catch (const std::exception& e) {
+        g_msg = e.what();
+        return code_of(e);
+    }
+}
+
 // Per-update replay with the reference's own kernels (the acceptance.cpp:268-304
 // pattern), recording the core and factors after every sweep.  Starts from the
 // given factors.

@@ -98,7 +98,7 @@ _f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
 class HqConfig(C.Structure):
     _fields_ = [("order", C.c_int), ("ranks", C.c_uint64 * 8), ("max_sweeps", C.c_uint64),
                 ("tol_fit_change", C.c_double), ("seed", C.c_uint64), ("init", C.c_int), ("kernel", C.c_int),
-                ("trace_gradients", C.c_int), ("tol_grad", C.c_double)]
+                ("trace_gradients", C.c_int), ("tol_grad", C.c_double), ("capacity_cap", C.c_uint64)]
 
 
 class HqTrace(C.Structure):
@@ -121,6 +121,7 @@ EXPORTED_SYMBOLS = [
     "hq_solver_ttmctc_work", "hq_nccl_unique_id", "hq_comm_create", "hq_comm_destroy", "hq_partition_rows",
     "hq_solver_create_dist", "hq_bench_ttmctc", "hq_gen_synthetic",
     "hq_tns_parse", "hq_tns_parse_file", "hq_tns_info", "hq_tns_copy", "hq_tns_tensor", "hq_tns_destroy",
+    "hq_densify_unfold", "hq_ttmc_unfold_dense", "hq_svd_leading", "hq_init_factors", "hq_hooi",
 ]
 
 _lib = None
@@ -165,6 +166,11 @@ def load_library(path: str = None) -> C.CDLL:
     L.hq_tns_copy.argtypes = [vp, vp, vp]
     L.hq_tns_tensor.argtypes = [vp, vp, pp]
     L.hq_tns_destroy.argtypes = [vp]
+    L.hq_densify_unfold.argtypes = [vp, C.c_int, C.c_uint64, _f64p]
+    L.hq_ttmc_unfold_dense.argtypes = [vp, vp, _u64p, C.c_int, C.c_uint64, _f64p]
+    L.hq_svd_leading.argtypes = [C.c_uint64, C.c_uint64, _f64p, C.c_uint64, _f64p]
+    L.hq_init_factors.argtypes = [vp, C.POINTER(HqConfig), vp]
+    L.hq_hooi.argtypes = [vp, C.POINTER(HqConfig), vp, vp, vp, C.POINTER(HqTrace)]
     L.hq_solver_create.argtypes = [vp, C.POINTER(HqConfig), vp, vp, pp]
     L.hq_solver_destroy.argtypes = [vp]
     L.hq_solver_run.argtypes = [vp, C.c_uint64]
@@ -446,6 +452,7 @@ class SolverConfig:
     trace_gradients: bool = False
     kernel: int = KERNEL_ELEMENTWISE
     tol_grad: float = 0.0
+    capacity_cap: int = 1 << 31  # kernels.hpp:62 (dense unfoldings of the desk-scale paths)
 
     def to_c(self, order):
         c = HqConfig()
@@ -460,6 +467,7 @@ class SolverConfig:
         c.kernel = int(self.kernel)
         c.trace_gradients = int(bool(self.trace_gradients))
         c.tol_grad = float(self.tol_grad)
+        c.capacity_cap = int(self.capacity_cap)
         return c
 
 
@@ -576,6 +584,88 @@ def hoqri(x: SparseTensor, config: SolverConfig, init_factors: Optional[Sequence
     trace = tb.to_trace(n)
     model = TuckerModel(FactorSet(fs), CoreTensor([int(k) for k in config.ranks], core), trace.data_norm_sq)
     return SolveResult(model, trace)
+
+
+def hooi(x: SparseTensor, config: SolverConfig, init_factors: Optional[Sequence[np.ndarray]] = None) -> SolveResult:
+    """tucker::hooi (solvers.hpp:82-83; solvers.cpp:93-178): desk-scale, every step on the device
+    (dense Y_(n), cuSOLVER eigen-solve of the smaller Gram side)."""
+    _check_ranks(x, config.ranks)
+    if config.max_sweeps < 1:
+        raise ShapeError("max_sweeps must be at least 1")
+    if config.tol_fit_change < 0:
+        raise ShapeError("tolerance must be nonnegative")
+    n = x.order()
+    cfg = config.to_c(n)
+    init_arr = None
+    if init_factors is not None:
+        fs0 = _factors_of(init_factors)
+        _check_factors(x, fs0)
+        cfg.init = INIT_GIVEN
+        init_arr = _ptr_array(fs0)
+    fs = [np.empty((x.dims()[v], int(config.ranks[v])), np.float64) for v in range(n)]
+    core = np.empty(int(np.prod(config.ranks)), np.float64)
+    tb = _TraceBuffers(int(config.max_sweeps), n, config.ranks)
+    _check(load_library().hq_hooi(x.handle, C.byref(cfg), init_arr, _ptr_array(fs), core.ctypes.data, C.byref(tb.c)))
+    trace = tb.to_trace(n)
+    model = TuckerModel(FactorSet(fs), CoreTensor([int(k) for k in config.ranks], core), trace.data_norm_sq)
+    return SolveResult(model, trace)
+
+
+def init_factors(x: SparseTensor, config: SolverConfig) -> FactorSet:
+    """solvers.hpp:69-70 / solvers.cpp:197-215: seeded random, or HOSVD (desk-scale) on the device."""
+    _check_ranks(x, config.ranks)
+    n = x.order()
+    fs = [np.empty((x.dims()[v], int(config.ranks[v])), np.float64) for v in range(n)]
+    cfg = config.to_c(n)
+    _check(load_library().hq_init_factors(x.handle, C.byref(cfg), _ptr_array(fs)))
+    return FactorSet(fs)
+
+
+def svd_leading(y, k: int) -> np.ndarray:
+    """dense_core.hpp:64: leading k left singular vectors (device eigen-solve; a subspace match of the
+    reference, column signs may differ)."""
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    if y.ndim != 2:
+        raise ShapeError("svd_leading: matrix expected")
+    m, p = y.shape
+    if k > min(m, p):
+        raise ShapeError("svd_leading: k exceeds min(rows, cols)")
+    u = np.zeros((m, int(k)), np.float64)
+    if k:
+        _check(load_library().hq_svd_leading(m, p, y.reshape(-1), int(k), u.reshape(-1)))
+    return u
+
+
+def densify_unfold(x: SparseTensor, mode: int, capacity_cap: int = 1 << 31) -> np.ndarray:
+    """kernels.hpp:70-71 on the device"""
+    if not 0 <= mode < x.order():
+        raise RangeError("densify_unfold: mode out of range")
+    cols = 1
+    for v, d in enumerate(x.dims()):
+        if v != mode:
+            cols *= d
+    rows = x.dims()[mode]
+    if cols and rows > capacity_cap // cols:
+        raise CapacityError(f"dense unfolding of {rows} x {cols} exceeds the capacity cap; this path is desk-scale only")
+    out = np.empty(rows * cols, np.float64)
+    _check(load_library().hq_densify_unfold(x.handle, int(mode), int(capacity_cap), out))
+    return out.reshape(rows, cols)
+
+
+def ttmc_unfold_dense(x: SparseTensor, u, mode: int, capacity_cap: int = 1 << 31) -> np.ndarray:
+    """kernels.hpp:66-67 on the device"""
+    fs = _factors_of(u)
+    _check_factors(x, fs)
+    if not 0 <= mode < x.order():
+        raise RangeError("ttmc_unfold_dense: mode out of range")
+    ranks = np.array([f.shape[1] for f in fs], np.uint64)
+    cols = int(np.prod([int(r) for v, r in enumerate(ranks) if v != mode]))
+    rows = x.dims()[mode]
+    if cols and rows > capacity_cap // cols:
+        raise CapacityError(f"dense unfolding of {rows} x {cols} exceeds the capacity cap; this path is desk-scale only")
+    out = np.empty(rows * cols, np.float64)
+    _check(load_library().hq_ttmc_unfold_dense(x.handle, _ptr_array(fs), ranks, int(mode), int(capacity_cap), out))
+    return out.reshape(rows, cols)
 
 
 def fit_error(x: SparseTensor, model: TuckerModel) -> float:

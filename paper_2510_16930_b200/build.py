@@ -35,7 +35,7 @@ def build_engine(force=False, verbose=False):
         return ENGINE
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
            "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"),
-           *cus, "-o", ENGINE]
+           *cus, "-lcublas", "-lcusolver", "-o", ENGINE]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)

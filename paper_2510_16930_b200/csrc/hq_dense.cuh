@@ -124,6 +124,21 @@ struct FillTable {
 };
 constexpr uint64_t kFillTableCap = 1ull << 28;
 std::shared_ptr<const FillTable> fill_table(uint64_t count);
+
+// tucker::Rng helpers on the host (rng.hpp): mix_seed, and `count` normals of
+// Rng(seed) (raw draws sequential, Box-Muller threaded)
+uint64_t mix_seed(uint64_t seed, uint64_t salt);
+void gaussian_stream(uint64_t seed, uint64_t count, double* out);
+
+// qr_orthonormal on the device (dense_core.cpp:127-198): CholeskyQR2 /
+// shifted CholeskyQR3 / multi-CTA Householder (with the reference's fill)
+struct QrWork {
+    DBuf<double> wpart, maxpart, w, maxv, r1inv, rinv, rc, ppart, hh;
+    DBuf<DevStatus> st;
+    void ensure(uint64_t rows, int K);
+};
+void qr_device(const double* A, uint64_t rows, int K, double* Q, QrWork& w, cudaStream_t s);
+void check_rank_limits(int K);
 // G_(n)^T (L x K_n) from the core
 void launch_gt(const double* core, const ModeShape& sh, const int* ranks, double* gt, const DevStatus* st,
                cudaStream_t s);

@@ -38,6 +38,7 @@
 #include "hq_dense.cuh"
 #include "hq_fast.cuh"
 #include "hq_tns.cuh"
+#include "hq_hooi.cuh"
 
 namespace hq {
 
@@ -68,10 +69,12 @@ int guard(F&& f) {
 
 inline cudaStream_t as_stream(void* p) { return reinterpret_cast<cudaStream_t>(p); }
 
+}  // namespace
+
 // ---- host Gaussian stream, bit-exact with tucker::Rng::normal (rng.hpp:24-35):
 // raw mt19937_64 draws are sequential; the Box-Muller transform of each pair
 // is independent, so it is spread over host threads.
-inline uint64_t mix_seed(uint64_t seed, uint64_t salt) {  // rng.hpp:57-62
+uint64_t mix_seed(uint64_t seed, uint64_t salt) {  // rng.hpp:57-62
     uint64_t z = seed + 0x9E3779B97F4A7C15ull * (salt + 1);
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
@@ -101,8 +104,6 @@ void gaussian_stream(uint64_t seed, uint64_t count, double* out) {
     for (auto& t : th) t.join();
 }
 
-}  // namespace
-
 std::shared_ptr<const FillTable> fill_table(uint64_t count) {
     if (count == 0 || count > kFillTableCap) return nullptr;
     static std::mutex mu;
@@ -124,31 +125,25 @@ std::shared_ptr<const FillTable> fill_table(uint64_t count) {
     return t;
 }
 
-namespace {
-
 // ---------------------------------------------------------------- QR -----
-struct QrWork {
-    DBuf<double> wpart, maxpart, w, maxv, r1inv, rinv, rc, ppart, hh;
-    DBuf<DevStatus> st;
-    void ensure(uint64_t rows, int K) {
-        size_t sl = dense_slots();
-        if (wpart.n < sl * K * K) wpart.alloc(sl * K * K);
-        if (ppart.n < sl * K * K) ppart.alloc(sl * K * K);
-        if (maxpart.n < sl) maxpart.alloc(sl);
-        if (w.n < (size_t)K * K) w.alloc(K * K);
-        if (r1inv.n < (size_t)K * K) r1inv.alloc(K * K);
-        if (rinv.n < (size_t)K * K) rinv.alloc(K * K);
-        if (rc.n < (size_t)K * K) rc.alloc(K * K);
-        if (!maxv.n) maxv.alloc(1);
-        const size_t hw = householder_work_doubles(rows, K);
-        if (hh.n < hw) {
-            hh.alloc(hw);
-            householder_reset(hh.get(), 0);
-            HQ_CUDA(cudaDeviceSynchronize());
-        }
-        if (!st.n) st.alloc(1);
+void QrWork::ensure(uint64_t rows, int K) {
+    size_t sl = dense_slots();
+    if (wpart.n < sl * K * K) wpart.alloc(sl * K * K);
+    if (ppart.n < sl * K * K) ppart.alloc(sl * K * K);
+    if (maxpart.n < sl) maxpart.alloc(sl);
+    if (w.n < (size_t)K * K) w.alloc(K * K);
+    if (r1inv.n < (size_t)K * K) r1inv.alloc(K * K);
+    if (rinv.n < (size_t)K * K) rinv.alloc(K * K);
+    if (rc.n < (size_t)K * K) rc.alloc(K * K);
+    if (!maxv.n) maxv.alloc(1);
+    const size_t hw = householder_work_doubles(rows, K);
+    if (hh.n < hw) {
+        hh.alloc(hw);
+        householder_reset(hh.get(), 0);
+        HQ_CUDA(cudaDeviceSynchronize());
     }
-};
+    if (!st.n) st.alloc(1);
+}
 
 // Q = qr_orthonormal(A) on the device (A, Q device, rows x K).  Returns the
 // fallback flag (1 when the Householder path ran).
@@ -181,7 +176,80 @@ void check_rank_limits(int K) {
     if (K > kMaxRank) fail(HQ_ERR_CAPACITY, "rank " + std::to_string(K) + " above the engine limit of 32");
 }
 
-}  // namespace
+// ---------------------------------------------- helpers for hq_hooi.cu ----
+void ttmc_core_dev(const DeviceTensor& T, const FactorPtrs& f, const int* ranks, double* core, cudaStream_t s) {
+    ModeShape sh = make_mode_shape(T.order, ranks, 0);
+    const ModeLayout& L = T.modes[0];
+    const int sl = pass_slots(L, sh);
+    DBuf<double> mpart, wpart, maxpart, ypart;
+    mpart.alloc((size_t)sl * sh.kn * sh.L);
+    wpart.alloc((size_t)sl * sh.kn * sh.kn);
+    maxpart.alloc(sl);
+    ypart.alloc(std::max<size_t>(1, pass_ypart_doubles(L, sh)));
+    PassOut out{nullptr, mpart.get(), wpart.get(), maxpart.get(), ypart.get()};
+    launch_pass(T, 0, sh, f, kCore, nullptr, out, nullptr, kAlways, s);
+    launch_reduce_core(mpart.get(), sl, (uint64_t)sh.kn * sh.L, core, nullptr, kAlways, s);
+    HQ_CUDA(cudaStreamSynchronize(s));
+}
+
+double subspace_distance_dev(const double* u, const double* v, uint64_t rows, int k, cudaStream_t s) {
+    DBuf<double> pp, d, obj, fit, fp;
+    DBuf<DevStatus> st;
+    pp.alloc((size_t)dense_slots() * k * k);
+    d.alloc(1);
+    obj.alloc(1);
+    fit.alloc(1);
+    fp.alloc(1);
+    st.alloc(1);
+    HQ_CUDA(cudaMemsetAsync(st.get(), 0, sizeof(DevStatus), s));
+    launch_apply(nullptr, rows, k, nullptr, const_cast<double*>(u), v, pp.get(), false, nullptr, kAlways, s);
+    SweepTrace tr{obj.get(), fit.get(), d.get(), fp.get(), nullptr, 1, 0.0, nullptr};
+    launch_drift(pp.get(), dense_slots(), k, nullptr, 0, 0.0, 1, 0, false, 0.0, 1, tr, st.get(), s);
+    double out = 0.0;
+    HQ_CUDA(cudaMemcpyAsync(&out, d.get(), 8, cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaStreamSynchronize(s));
+    return out;
+}
+
+double orthonormality_defect_dev(const double* u, uint64_t rows, int k, cudaStream_t s) {
+    DBuf<double> wp, mx;
+    wp.alloc((size_t)dense_slots() * k * k);
+    mx.alloc(1);
+    launch_defect(u, rows, k, wp.get(), mx.get(), s);
+    double out = 0.0;
+    HQ_CUDA(cudaMemcpyAsync(&out, mx.get(), 8, cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaStreamSynchronize(s));
+    return out;
+}
+
+// init_factors (solvers.cpp:182-215): 0 random (seeded Gaussian + QR), 1 HOSVD, 2 caller's factors
+void init_factors_dev(const DeviceTensor& T, const hq_config& cfg, const double* const* init_host, double* const* U,
+                      cudaStream_t s) {
+    const int N = T.order;
+    int ranks[kMaxOrder];
+    for (int v = 0; v < N; ++v) ranks[v] = (int)cfg.ranks[v];
+    if (cfg.init == 2) {
+        for (int v = 0; v < N; ++v)
+            HQ_CUDA(cudaMemcpyAsync(U[v], init_host[v], sizeof(double) * T.dims[v] * ranks[v], cudaMemcpyHostToDevice,
+                                    s));
+        HQ_CUDA(cudaStreamSynchronize(s));
+    } else if (cfg.init == 0) {
+        QrWork qw;
+        for (int v = 0; v < N; ++v) {
+            std::vector<double> g((size_t)T.dims[v] * ranks[v]);
+            gaussian_stream(mix_seed(cfg.seed, (uint64_t)v), g.size(), g.data());
+            DBuf<double> a;
+            a.alloc(std::max<size_t>(1, g.size()));
+            HQ_CUDA(cudaMemcpyAsync(a.get(), g.data(), sizeof(double) * g.size(), cudaMemcpyHostToDevice, s));
+            qr_device(a.get(), T.dims[v], ranks[v], U[v], qw, s);
+            HQ_CUDA(cudaStreamSynchronize(s));
+        }
+    } else if (cfg.init == 1) {
+        hosvd_init_dev(T, ranks, cfg.capacity_cap ? cfg.capacity_cap : (1ull << 31), U, s);
+    } else {
+        fail(HQ_ERR_SHAPE, "unknown init mode");
+    }
+}
 
 // ------------------------------------------------------------- solver ----
 struct Solver {
@@ -353,21 +421,10 @@ struct Solver {
         HQ_CUDA(cudaMemsetAsync(st.get(), 0, sizeof(DevStatus), s));
 
         // ---- initial factors (solvers.cpp:182-215)
-        if (cfg.init == 2) {
-            for (int v = 0; v < N; ++v)
-                HQ_CUDA(cudaMemcpyAsync(U[v][0].get(), init[v], sizeof(double) * dims[v] * ranks[v],
-                                        cudaMemcpyHostToDevice, s));
-        } else if (cfg.init == 0) {
-            for (int v = 0; v < N; ++v) {
-                std::vector<double> g((size_t)dims[v] * ranks[v]);
-                gaussian_stream(mix_seed(cfg.seed, (uint64_t)v), g.size(), g.data());
-                HQ_CUDA(cudaMemcpyAsync(A.get(), g.data(), sizeof(double) * g.size(), cudaMemcpyHostToDevice, s));
-                qr_device(A.get(), dims[v], ranks[v], U[v][0].get(), qw, s);
-                HQ_CUDA(cudaStreamSynchronize(s));
-            }
-        } else {
-            fail(HQ_ERR_CAPACITY, "HOSVD initialisation is desk-scale only and not part of the device engine; "
-                                  "use random init");
+        {
+            double* u0[kMaxOrder];
+            for (int v = 0; v < N; ++v) u0[v] = U[v][0].get();
+            init_factors_dev(*T, cfg, init, u0, s);
         }
         // ---- initial core (solvers.cpp:66) and objective
         compute_core(0, kAlways);
@@ -1050,6 +1107,80 @@ int hq_gen_synthetic(int order, const uint64_t* dims, uint64_t nnz, uint64_t see
     });
 }
 
+// ------------------------------------------------------------ desk-scale --
+int hq_densify_unfold(const hq_tensor* t, int mode, uint64_t capacity_cap, double* out) {
+    return guard([&] {
+        DBuf<double> d;
+        densify_unfold_dev(t->t, mode, capacity_cap, d, t->stream);
+        const uint64_t n = t->t.dims[mode] * densify_cols(t->t, mode);
+        HQ_CUDA(cudaMemcpyAsync(out, d.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, t->stream));
+        HQ_CUDA(cudaStreamSynchronize(t->stream));
+    });
+}
+
+int hq_ttmc_unfold_dense(const hq_tensor* t, const double* const* factors, const uint64_t* ranks, int mode,
+                         uint64_t capacity_cap, double* out) {
+    return guard([&] {
+        if (mode < 0 || mode >= t->t.order) fail(HQ_ERR_RANGE, "ttmc_unfold_dense: mode out of range");
+        UploadedFactors uf;
+        upload_factors(t->t, factors, ranks, uf, t->stream);
+        DBuf<double> y;
+        ttmc_unfold_dense_dev(t->t, mode, uf.f, uf.ranks, capacity_cap, y, t->stream);
+        ModeShape sh = make_mode_shape(t->t.order, uf.ranks, mode);
+        HQ_CUDA(cudaMemcpyAsync(out, y.get(), sizeof(double) * t->t.dims[mode] * sh.L, cudaMemcpyDeviceToHost,
+                                t->stream));
+        HQ_CUDA(cudaStreamSynchronize(t->stream));
+    });
+}
+
+int hq_svd_leading(uint64_t rows, uint64_t cols, const double* y, uint64_t k, double* u_out) {
+    return guard([&] {
+        if (k > std::min(rows, cols)) fail(HQ_ERR_SHAPE, "svd_leading: k exceeds min(rows, cols)");
+        if (k == 0) return;
+        check_rank_limits((int)k);
+        cudaStream_t s = nullptr;
+        DBuf<double> Y, U;
+        Y.alloc(rows * cols);
+        U.alloc(rows * k);
+        HQ_CUDA(cudaMemcpyAsync(Y.get(), y, sizeof(double) * rows * cols, cudaMemcpyHostToDevice, s));
+        svd_leading_dev(Y.get(), rows, cols, (int)k, U.get(), s);
+        HQ_CUDA(cudaMemcpyAsync(u_out, U.get(), sizeof(double) * rows * k, cudaMemcpyDeviceToHost, s));
+        HQ_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int hq_init_factors(const hq_tensor* t, const hq_config* cfg, double* const* factors_out) {
+    return guard([&] {
+        const DeviceTensor& T = t->t;
+        if (cfg->order != T.order) fail(HQ_ERR_SHAPE, "rank count does not match tensor order");
+        DBuf<double> U[kMaxOrder];
+        double* up[kMaxOrder];
+        for (int v = 0; v < T.order; ++v) {
+            if (cfg->ranks[v] < 1 || cfg->ranks[v] > T.dims[v])
+                fail(HQ_ERR_SHAPE, "rank for mode " + std::to_string(v + 1) + " must lie in [1, " +
+                                       std::to_string(T.dims[v]) + "]");
+            check_rank_limits((int)cfg->ranks[v]);
+            U[v].alloc(T.dims[v] * cfg->ranks[v]);
+            up[v] = U[v].get();
+        }
+        init_factors_dev(T, *cfg, nullptr, up, t->stream);
+        for (int v = 0; v < T.order; ++v)
+            HQ_CUDA(cudaMemcpyAsync(factors_out[v], up[v], sizeof(double) * T.dims[v] * cfg->ranks[v],
+                                    cudaMemcpyDeviceToHost, t->stream));
+        HQ_CUDA(cudaStreamSynchronize(t->stream));
+    });
+}
+
+int hq_hooi(const hq_tensor* t, const hq_config* cfg, const double* const* init_factors, double* const* factors_out,
+            double* core_out, hq_trace* trace) {
+    return guard([&] {
+        if (cfg->order != t->t.order) fail(HQ_ERR_SHAPE, "rank count does not match tensor order");
+        hq_config c = *cfg;
+        if (init_factors) c.init = 2;
+        hooi_solve(t->t, c, init_factors, factors_out, core_out, trace, t->stream);
+    });
+}
+
 int hq_qr_orthonormal(uint64_t rows, uint64_t cols, const double* a, double* q_out) {
     return guard([&] {
         if (rows < cols) fail(HQ_ERR_SHAPE, "qr_orthonormal: need rows >= cols");
@@ -1122,6 +1253,7 @@ void hq_config_default(hq_config* cfg) {
     std::memset(cfg, 0, sizeof(*cfg));
     cfg->max_sweeps = 100;
     cfg->tol_fit_change = 1e-12;
+    cfg->capacity_cap = 1ull << 31;  // kernels.hpp:62
 }
 
 int hq_solver_create(const hq_tensor* t, const hq_config* cfg, const double* const* init_factors, void* stream,

@@ -380,19 +380,67 @@ static void check_ranks(const SparseTensor& x, const std::vector<std::size_t>& r
                              std::to_string(x.dims()[n]) + "]");
 }
 
-FactorSet init_factors(const SparseTensor& x, const SolverConfig& config) {
+FactorSet init_factors(const SparseTensor& x, const SolverConfig& config) {  // solvers.cpp:202-215
     check_ranks(x, config.ranks);
-    if (config.init != InitMode::kRandom)
-        throw CapacityError("HOSVD initialisation is desk-scale only and outside the B200 engine; use random init");
-    return random_factors(x.dims(), config.ranks, config.seed);
+    if (config.init == InitMode::kRandom) return random_factors(x.dims(), config.ranks, config.seed);
+    hq_config c;
+    hq_config_default(&c);
+    c.order = static_cast<int>(x.order());
+    for (std::size_t v = 0; v < x.order(); ++v) c.ranks[v] = config.ranks[v];
+    c.init = 1;
+    c.capacity_cap = config.capacity_cap;
+    FactorSet u;
+    for (std::size_t v = 0; v < x.order(); ++v) u.factors.emplace_back(x.dims()[v], config.ranks[v]);
+    std::vector<double*> fo;
+    for (auto& m : u.factors) fo.push_back(m.data.data());
+    check(hq_init_factors(x.device(), &c, fo.data()));
+    return u;
 }
 
-static SolveResult solve_impl(const SparseTensor& x, const SolverConfig& config, const FactorSet* start) {
+Matrix svd_leading(const Matrix& y, std::size_t k) {  // dense_core.hpp:64 (device eigen-solve)
+    if (k > std::min(y.rows, y.cols)) throw ShapeError("svd_leading: k exceeds min(rows, cols)");
+    Matrix u(y.rows, k);
+    if (k) check(hq_svd_leading(y.rows, y.cols, y.data.data(), k, u.data.data()));
+    return u;
+}
+
+Matrix densify_unfold(const SparseTensor& x, std::size_t mode, std::size_t capacity_cap) {  // kernels.hpp:70-71
+    if (mode >= x.order()) throw RangeError("densify_unfold: mode out of range");
+    std::size_t cols = 1;
+    for (std::size_t v = 0; v < x.order(); ++v)
+        if (v != mode) cols *= x.dims()[v];
+    if (cols != 0 && x.dims()[mode] > capacity_cap / cols)
+        throw CapacityError("dense unfolding of " + std::to_string(x.dims()[mode]) + " x " + std::to_string(cols) +
+                            " exceeds the capacity cap; this path is desk-scale only");
+    Matrix m(x.dims()[mode], cols);
+    check(hq_densify_unfold(x.device(), static_cast<int>(mode), capacity_cap, m.data.data()));
+    return m;
+}
+
+Matrix ttmc_unfold_dense(const SparseTensor& x, const FactorSet& u, std::size_t mode,
+                         std::size_t capacity_cap) {  // kernels.hpp:66-67
+    check_factors(x, u);
+    if (mode >= x.order()) throw RangeError("ttmc_unfold_dense: mode out of range");
+    std::size_t cols = 1;
+    std::vector<uint64_t> r;
+    for (std::size_t v = 0; v < x.order(); ++v) {
+        r.push_back(u.factors[v].cols);
+        if (v != mode) cols *= u.factors[v].cols;
+    }
+    if (cols != 0 && x.dims()[mode] > capacity_cap / cols)
+        throw CapacityError("dense unfolding of " + std::to_string(x.dims()[mode]) + " x " + std::to_string(cols) +
+                            " exceeds the capacity cap; this path is desk-scale only");
+    Matrix y(x.dims()[mode], cols);
+    auto p = ptrs(u);
+    check(hq_ttmc_unfold_dense(x.device(), p.data(), r.data(), static_cast<int>(mode), capacity_cap, y.data.data()));
+    return y;
+}
+
+static SolveResult solve_impl(const SparseTensor& x, const SolverConfig& config, const FactorSet* start,
+                              bool hooi_alg = false) {
     check_ranks(x, config.ranks);
     if (config.max_sweeps < 1) throw ShapeError("max_sweeps must be at least 1");
     if (config.tol_fit_change < 0.0) throw ShapeError("tolerance must be nonnegative");
-    if (!start && config.init != InitMode::kRandom)
-        throw CapacityError("HOSVD initialisation is desk-scale only and outside the B200 engine; use random init");
     const std::size_t n = x.order();
     hq_config c;
     hq_config_default(&c);
@@ -404,6 +452,8 @@ static SolveResult solve_impl(const SparseTensor& x, const SolverConfig& config,
     c.kernel = config.kernel == KernelVariant::kMatrix ? 1 : 0;
     c.trace_gradients = config.trace_gradients ? 1 : 0;
     c.tol_grad = config.tol_grad;
+    c.init = config.init == InitMode::kHosvd ? 1 : 0;
+    c.capacity_cap = config.capacity_cap;
     std::vector<const double*> init;
     if (start) {
         if (start->order() != n) throw ShapeError("factor count does not match tensor order");
@@ -432,7 +482,10 @@ static SolveResult solve_impl(const SparseTensor& x, const SolverConfig& config,
     tr.upd_sigma = sig.data();
     tr.upd_lambda = lam.data();
     tr.sigma_stride = ks;
-    check(hq_hoqri(x.device(), &c, start ? init.data() : nullptr, fo.data(), res.model.core.data.data(), &tr));
+    if (hooi_alg)
+        check(hq_hooi(x.device(), &c, start ? init.data() : nullptr, fo.data(), res.model.core.data.data(), &tr));
+    else
+        check(hq_hoqri(x.device(), &c, start ? init.data() : nullptr, fo.data(), res.model.core.data.data(), &tr));
     res.model.data_norm_sq = tr.data_norm_sq;
     res.trace.data_norm_sq = tr.data_norm_sq;
     res.trace.initial_objective = tr.initial_objective;
@@ -463,6 +516,10 @@ static SolveResult solve_impl(const SparseTensor& x, const SolverConfig& config,
 }
 
 SolveResult hoqri(const SparseTensor& x, const SolverConfig& config) { return solve_impl(x, config, nullptr); }
+
+SolveResult hooi(const SparseTensor& x, const SolverConfig& config) {  // solvers.hpp:82-83, on the device
+    return solve_impl(x, config, nullptr, true);
+}
 
 SolveResult hoqri_from(const SparseTensor& x, const SolverConfig& config, const FactorSet& start) {
     return solve_impl(x, config, &start);
@@ -770,17 +827,11 @@ TraceFile read_trace_json(std::istream& in) {
     return t;
 }
 
-SolveResult hooi(const SparseTensor&, const SolverConfig&) {
-    throw CapacityError("hooi is outside the B200 engine (the HOQRI hot path); use the reference library for HOOI");
-}
-
-ExperimentResult run_experiment(const ExperimentSpec& spec) {  // harness.cpp:241-345, HOQRI on the device
+ExperimentResult run_experiment(const ExperimentSpec& spec) {  // harness.cpp:241-345, solves on the device
     if (spec.repetitions < 1) throw ShapeError("repetitions must be at least 1");
     if (spec.input_path.has_value() == spec.synthetic.has_value())
         throw ShapeError("specify exactly one input source (file or synthetic)");
     if (spec.out_dir.empty()) throw ShapeError("output directory required");
-    if (spec.solver != SolverChoice::kHoqri)
-        throw CapacityError("hooi is outside the B200 engine (the HOQRI hot path); run_experiment supports kHoqri");
     SparseTensor x;
     if (spec.input_path) {
         x = load_tns_file(*spec.input_path, spec.dims_override);
@@ -789,47 +840,67 @@ ExperimentResult run_experiment(const ExperimentSpec& spec) {  // harness.cpp:24
         x = gen_synthetic(syn.dims, syn.nnz, syn.seed);
     }
     std::filesystem::create_directories(spec.out_dir);
+    std::vector<std::pair<const char*, bool>> chosen;  // (name, is_hooi)
+    if (spec.solver != SolverChoice::kHooi) chosen.push_back({"hoqri", false});
+    if (spec.solver != SolverChoice::kHoqri) chosen.push_back({"hooi", true});
     ExperimentResult result;
-    std::string runs;
-    double mean_total = 0.0;
-    for (std::size_t rep = 0; rep < spec.repetitions; ++rep) {
-        SolverConfig cfg = spec.config;
-        cfg.seed = spec.config.seed + rep;
-        SolveResult res = hoqri(x, cfg);
-        TraceFile t = make_trace_file("hoqri", cfg, x, res.trace);
-        const std::string base = (std::filesystem::path(spec.out_dir) / ("hoqri_rep" + std::to_string(rep))).string();
-        {
-            std::ofstream csv(base + ".trace.csv");
-            write_trace_csv(csv, t);
-            std::ofstream js(base + ".trace.json");
-            write_trace_json(js, t);
+    std::string sections;
+    for (const auto& [name, is_hooi] : chosen) {
+        std::string runs;
+        double mean_total = 0.0;
+        for (std::size_t rep = 0; rep < spec.repetitions; ++rep) {  // repetitions share the GPU: in order
+            SolverConfig cfg = spec.config;
+            cfg.seed = spec.config.seed + rep;
+            SolveResult res = is_hooi ? hooi(x, cfg) : hoqri(x, cfg);
+            TraceFile t = make_trace_file(name, cfg, x, res.trace);
+            const std::string base =
+                (std::filesystem::path(spec.out_dir) / (std::string(name) + "_rep" + std::to_string(rep))).string();
+            {
+                std::ofstream csv(base + ".trace.csv");
+                write_trace_csv(csv, t);
+                std::ofstream js(base + ".trace.json");
+                write_trace_json(js, t);
+            }
+            const std::size_t sweeps = res.trace.sweeps.size();
+            double mean_sweep = 0.0, fobj = 0.0, ffit = 0.0;
+            if (sweeps) {
+                mean_sweep = res.trace.sweeps.back().elapsed_s / static_cast<double>(sweeps);
+                fobj = res.trace.sweeps.back().objective;
+                ffit = res.trace.sweeps.back().fit;
+            }
+            mean_total += mean_sweep;
+            result.trace_paths.push_back(base + ".trace.csv");
+            runs += std::string(rep ? "," : "") + "\n      {\n        \"final_fit\": " + json_number(ffit) +
+                    ",\n        \"final_objective\": " + json_number(fobj) + ",\n        \"mean_sweep_s\": " +
+                    json_number(mean_sweep) + ",\n        \"rep\": " + std::to_string(rep) +
+                    ",\n        \"sweeps\": " + std::to_string(sweeps) + ",\n        \"trace\": " +
+                    json_string(base + ".trace.csv") + "\n      }";
         }
-        const std::size_t sweeps = res.trace.sweeps.size();
-        double mean_sweep = 0.0, fobj = 0.0, ffit = 0.0;
-        if (sweeps) {
-            mean_sweep = res.trace.sweeps.back().elapsed_s / static_cast<double>(sweeps);
-            fobj = res.trace.sweeps.back().objective;
-            ffit = res.trace.sweeps.back().fit;
-        }
-        mean_total += mean_sweep;
-        result.trace_paths.push_back(base + ".trace.csv");
-        runs += std::string(rep ? "," : "") + "\n      {\n        \"final_fit\": " + json_number(ffit) +
-                ",\n        \"final_objective\": " + json_number(fobj) + ",\n        \"mean_sweep_s\": " +
-                json_number(mean_sweep) + ",\n        \"rep\": " + std::to_string(rep) + ",\n        \"sweeps\": " +
-                std::to_string(sweeps) + ",\n        \"trace\": " + json_string(base + ".trace.csv") + "\n      }";
+        sections += ",\n  " + json_string(name) + ": {\n    \"mean_sweep_s\": " +
+                    json_number(mean_total / static_cast<double>(spec.repetitions)) + ",\n    \"runs\": [" + runs +
+                    "\n    ]\n  }";
     }
     auto arr = [](const std::vector<std::size_t>& v) {
-        std::string s = "[";
-        for (std::size_t i = 0; i < v.size(); ++i) s += (i ? ", " : "") + std::to_string(v[i]);
-        return s + "]";
+        std::string s2 = "[";
+        for (std::size_t i2 = 0; i2 < v.size(); ++i2) s2 += (i2 ? ", " : "") + std::to_string(v[i2]);
+        return s2 + "]";
     };
     const std::string sp = (std::filesystem::path(spec.out_dir) / "summary.json").string();
     std::ofstream out(sp);
-    out << "{\n  \"dims\": " << arr(x.dims()) << ",\n  \"hoqri\": {\n    \"mean_sweep_s\": "
-        << json_number(mean_total / static_cast<double>(spec.repetitions)) << ",\n    \"runs\": [" << runs
-        << "\n    ]\n  },\n  \"nnz\": " << x.nnz() << ",\n  \"ranks\": " << arr(spec.config.ranks)
-        << ",\n  \"repetitions\": " << spec.repetitions << ",\n  \"tool_version\": " << json_string(kToolVersion)
-        << "\n}\n";
+    // keys in sorted order like the reference's json dump: dims, hooi, hoqri, nnz, ranks, repetitions, tool_version
+    std::string hooi_sec, hoqri_sec;
+    {
+        const std::size_t cut = sections.find(",\n  \"hooi\"");
+        hoqri_sec = cut == std::string::npos ? sections : sections.substr(0, cut);
+        hooi_sec = cut == std::string::npos ? std::string() : sections.substr(cut);
+        if (spec.solver == SolverChoice::kHooi) {
+            hooi_sec = sections;
+            hoqri_sec.clear();
+        }
+    }
+    out << "{\n  \"dims\": " << arr(x.dims()) << hooi_sec << hoqri_sec << ",\n  \"nnz\": " << x.nnz()
+        << ",\n  \"ranks\": " << arr(spec.config.ranks) << ",\n  \"repetitions\": " << spec.repetitions
+        << ",\n  \"tool_version\": " << json_string(kToolVersion) << "\n}\n";
     result.summary_path = sp;
     return result;
 }

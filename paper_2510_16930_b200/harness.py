@@ -7,8 +7,7 @@ grad_norm_sq, drift_1..drift_N``, ``%.17g`` cells), same file layout
 the same exceptions, so plots and tests written for the reference consume GPU
 runs unchanged.  What differs is the clock: ``elapsed_s`` is device time of
 the solve, and :func:`bench_kernel` times each TTMcTC call with CUDA events on
-a resident state (harness.cpp:350-381 times host calls).  HOOI is outside the
-engine: selecting it raises :class:`CapacityError`.
+a resident state (harness.cpp:350-381 times host calls).
 """
 from __future__ import annotations
 
@@ -22,7 +21,7 @@ from typing import Dict, List, Optional, Sequence
 import numpy as np
 
 from . import (CapacityError, InfeasibleError, IterationTrace, ParseError, SolverConfig, ShapeError, SparseTensor,
-               _check, _factors_of, _check_factors, _ptr_array, gen_synthetic, hoqri, load_library, load_tns)
+               _check, _factors_of, _check_factors, _ptr_array, gen_synthetic, hooi, hoqri, load_library, load_tns)
 
 K_TOOL_VERSION = "0.1.0"  # harness.hpp:15-16
 K_TRACE_VERSION = 1
@@ -151,11 +150,6 @@ class ExperimentResult:
     summary_path: str
 
 
-def hooi(x, config):
-    """solvers.hpp:82-83 -- outside the B200 engine."""
-    raise CapacityError("hooi is outside the B200 engine (the HOQRI hot path); use the reference library for HOOI")
-
-
 def run_experiment(spec: ExperimentSpec) -> ExperimentResult:
     """harness.cpp:241-345, HOQRI on the device."""
     if spec.repetitions < 1:
@@ -164,8 +158,8 @@ def run_experiment(spec: ExperimentSpec) -> ExperimentResult:
         raise ShapeError("specify exactly one input source (file or synthetic)")
     if not spec.out_dir:
         raise ShapeError("output directory required")
-    if spec.solver != SOLVER_HOQRI:
-        raise CapacityError("hooi is outside the B200 engine (the HOQRI hot path); run_experiment supports hoqri")
+    if spec.solver not in (SOLVER_HOQRI, SOLVER_HOOI, SOLVER_BOTH):
+        raise ShapeError(f"unknown solver choice {spec.solver!r}")
     if spec.input_path is not None:
         x = load_tns(spec.input_path, spec.dims_override)
     else:
@@ -177,25 +171,29 @@ def run_experiment(spec: ExperimentSpec) -> ExperimentResult:
             raise InfeasibleError("synthetic nnz exceeds the number of cells")
         x = gen_synthetic(s.dims, s.nnz, s.seed)
     os.makedirs(spec.out_dir, exist_ok=True)
-    runs, paths = [], []
-    for rep in range(spec.repetitions):
-        cfg = dataclasses.replace(spec.config, seed=int(spec.config.seed) + rep)
-        res = hoqri(x, cfg)
-        t = make_trace_file("hoqri", cfg, x, res.trace)
-        base = os.path.join(spec.out_dir, f"hoqri_rep{rep}")
-        with open(base + ".trace.csv", "w") as f:
-            write_trace_csv(f, t)
-        with open(base + ".trace.json", "w") as f:
-            write_trace_json(f, t)
-        sw = res.trace.sweeps
-        last = sw[-1] if sw else None
-        runs.append({"rep": rep, "trace": base + ".trace.csv", "sweeps": len(sw),
-                     "mean_sweep_s": last.elapsed_s / len(sw) if sw else 0.0,
-                     "final_objective": last.objective if sw else 0.0, "final_fit": last.fit if sw else 0.0})
-        paths.append(base + ".trace.csv")
+    chosen = [("hoqri", hoqri)] if spec.solver == SOLVER_HOQRI else [("hooi", hooi)] if spec.solver == SOLVER_HOOI \
+        else [("hoqri", hoqri), ("hooi", hooi)]
+    paths = []
     summary = {"tool_version": K_TOOL_VERSION, "dims": [int(d) for d in x.dims()], "nnz": int(x.nnz()),
-               "ranks": [int(k) for k in spec.config.ranks], "repetitions": spec.repetitions,
-               "hoqri": {"runs": runs, "mean_sweep_s": sum(r["mean_sweep_s"] for r in runs) / len(runs)}}
+               "ranks": [int(k) for k in spec.config.ranks], "repetitions": spec.repetitions}
+    for name, solve in chosen:
+        runs = []
+        for rep in range(spec.repetitions):  # repetitions share the GPU: in order
+            cfg = dataclasses.replace(spec.config, seed=int(spec.config.seed) + rep)
+            res = solve(x, cfg)
+            t = make_trace_file(name, cfg, x, res.trace)
+            base = os.path.join(spec.out_dir, f"{name}_rep{rep}")
+            with open(base + ".trace.csv", "w") as f:
+                write_trace_csv(f, t)
+            with open(base + ".trace.json", "w") as f:
+                write_trace_json(f, t)
+            sw = res.trace.sweeps
+            last = sw[-1] if sw else None
+            runs.append({"rep": rep, "trace": base + ".trace.csv", "sweeps": len(sw),
+                         "mean_sweep_s": last.elapsed_s / len(sw) if sw else 0.0,
+                         "final_objective": last.objective if sw else 0.0, "final_fit": last.fit if sw else 0.0})
+            paths.append(base + ".trace.csv")
+        summary[name] = {"runs": runs, "mean_sweep_s": sum(r["mean_sweep_s"] for r in runs) / len(runs)}
     sp = os.path.join(spec.out_dir, "summary.json")
     with open(sp, "w") as f:
         f.write(json.dumps(summary, indent=2, sort_keys=True) + "\n")

@@ -189,10 +189,32 @@ int main() {
         CHECK(tc.header["solver"] == "hoqri" && tc.header["seed"] == "5" && tc.header["dims"] == "20,18,16");
         for (std::size_t i = 1; i < tc.rows.size(); ++i) CHECK(tc.rows[i][1] >= tc.rows[i - 1][1]);  // elapsed
         spec.solver = SolverChoice::kBoth;
-        CHECK_THROWS_AS(run_experiment(spec), CapacityError);
+        spec.repetitions = 1;
+        ExperimentResult eb = run_experiment(spec);
+        CHECK(eb.trace_paths.size() == 2);
+        CHECK(eb.trace_paths[1].find("hooi_rep0.trace.csv") != std::string::npos);
+        // HOOI and HOSVD init on the device (solvers_test.cpp:71-79, 158-170)
         SolverConfig hc;
         hc.ranks = {3, 3, 3};
-        CHECK_THROWS_AS(hooi(x, hc), CapacityError);
+        hc.max_sweeps = 10;
+        hc.tol_fit_change = 0.0;
+        hc.init = InitMode::kHosvd;
+        SolveResult ra = hoqri(x, hc), rb = hooi(x, hc);
+        CHECK(rb.trace.sweeps.size() == 10);
+        double prev = rb.trace.initial_objective;
+        for (const SweepRecord& sw : rb.trace.sweeps) {
+            CHECK(sw.objective >= prev - 1e-9 * std::max(prev, 1.0));
+            prev = sw.objective;
+        }
+        CHECK(rb.model.factors.orthonormality_defect() <= 1e-10);
+        FactorSet hs = init_factors(x, hc);
+        CHECK(hs.factors.size() == 3 && hs.orthonormality_defect() <= 1e-10);
+        Matrix yd = densify_unfold(x, 0);
+        CHECK(yd.rows == 20 && yd.cols == 18 * 16);
+        Matrix ul = svd_leading(yd, 3);
+        CHECK(ul.rows == 20 && ul.cols == 3);
+        hc.capacity_cap = 100;
+        CHECK_THROWS_AS(init_factors(x, hc), CapacityError);
         FactorSet u = random_factors(x.dims(), {3, 3, 3}, 7);
         BenchStats bs = bench_kernel(x, u, 1, KernelVariant::kElementwise, 5);
         CHECK(bs.repetitions == 5 && bs.min_s > 0.0 && bs.min_s <= bs.median_s && bs.median_s <= bs.max_s);

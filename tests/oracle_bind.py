@@ -258,6 +258,12 @@ class RefLib:
                                 C.POINTER(C.c_uint64), C.POINTER(C.c_double), f64p, f64p, f64p, f64p]
         L.ref_hoqri_replay.argtypes = [vp, u64p, f64p, C.c_uint64, f64p, f64p, f64p]
         L.ref_tensor_dims.argtypes = [vp, u64p]
+        L.ref_densify_unfold.argtypes = [vp, C.c_int, C.c_uint64, f64p]
+        L.ref_ttmc_unfold_dense.argtypes = [vp, u64p, f64p, C.c_int, C.c_uint64, f64p]
+        L.ref_svd_leading.argtypes = [C.c_uint64, C.c_uint64, f64p, C.c_uint64, f64p]
+        L.ref_init_factors.argtypes = [vp, u64p, C.c_uint64, C.c_int, C.c_uint64, f64p]
+        L.ref_solve.argtypes = [vp, C.c_int, u64p, C.c_uint64, C.c_double, C.c_uint64, C.c_int, C.c_int, f64p, f64p,
+                                C.POINTER(C.c_uint64), C.POINTER(C.c_double), f64p, f64p, f64p, f64p]
         L.ref_tns_parse.argtypes = [C.c_char_p, C.c_uint64, C.c_int, C.c_void_p, C.POINTER(vp)]
         L.ref_last_message.restype = C.c_char_p
         L.ref_trace_files.argtypes = [vp, u64p, C.c_uint64, C.c_uint64, C.c_char_p, C.c_char_p, C.c_uint64]
@@ -272,6 +278,15 @@ class RefLib:
         L.ref_slices_time.restype = C.c_double
         L.ref_time_qr.argtypes = [C.c_uint64, C.c_uint64, f64p, C.c_int]
         L.ref_time_qr.restype = C.c_double
+
+
+def ref_svd_leading(lib, y, k):
+    y = _f64(y)
+    out = np.empty(y.shape[0] * k, np.float64)
+    st = lib.L.ref_svd_leading(y.shape[0], y.shape[1], y.reshape(-1), k, out)
+    if st:
+        raise RuntimeError(f"ref svd_leading status {st}")
+    return out.reshape(y.shape[0], k)
 
 
 def ref_load_tns(lib, text: bytes, dims_override=None):
@@ -368,6 +383,42 @@ class RefTensor:
         return dict(status=st, payload=int(self.lib.L.ref_last_payload()), sweeps=s, initial_objective=f0.value,
                     objective=obj[:s], fit=fit[:s], drift=drift[: s * N].reshape(s, N), elapsed=el[:s],
                     factors=_split(f, self.dims, ranks), core=core.reshape(tuple(int(r) for r in ranks)))
+
+    def densify(self, mode, cap=1 << 31):
+        cols = int(np.prod([d for v, d in enumerate(self.dims) if v != mode]))
+        out = np.empty(self.dims[mode] * cols, np.float64)
+        st = self.lib.L.ref_densify_unfold(self.h, mode, cap, out)
+        return st, (out.reshape(self.dims[mode], cols) if not st else None)
+
+    def unfold_dense(self, ranks, factors, mode, cap=1 << 31):
+        ranks = _u64(ranks)
+        f = _f64(np.concatenate([np.asarray(u).reshape(-1) for u in factors]))
+        cols = int(np.prod([int(r) for v, r in enumerate(ranks) if v != mode]))
+        out = np.empty(self.dims[mode] * cols, np.float64)
+        st = self.lib.L.ref_ttmc_unfold_dense(self.h, ranks, f, mode, cap, out)
+        return st, (out.reshape(self.dims[mode], cols) if not st else None)
+
+    def init_factors(self, ranks, seed, hosvd, cap=1 << 31):
+        ranks = _u64(ranks)
+        out = np.empty(sum(d * int(k) for d, k in zip(self.dims, ranks)), np.float64)
+        st = self.lib.L.ref_init_factors(self.h, ranks, seed, int(hosvd), cap, out)
+        msg = self.lib.L.ref_last_message().decode() if st else ""
+        return st, msg, (_split(out, self.dims, ranks) if not st else None)
+
+    def solve(self, hooi, ranks, sweeps, tol, seed, hosvd, trace_gradients=False):
+        ranks = _u64(ranks)
+        n = len(self.dims)
+        fs = np.empty(sum(d * int(k) for d, k in zip(self.dims, ranks)), np.float64)
+        core = np.empty(int(np.prod(ranks)), np.float64)
+        sw, f0 = C.c_uint64(0), C.c_double(0)
+        obj, fit = np.zeros(sweeps), np.zeros(sweeps)
+        drift, grad = np.zeros(sweeps * n), np.zeros(sweeps * n)
+        st = self.lib.L.ref_solve(self.h, int(hooi), ranks, sweeps, tol, seed, int(hosvd), int(trace_gradients), fs,
+                                  core, C.byref(sw), C.byref(f0), obj, fit, drift, grad)
+        s_ = int(sw.value)
+        return dict(status=st, sweeps=s_, initial_objective=f0.value, objective=obj[:s_], fit=fit[:s_],
+                    drift=drift[:s_ * n], grad=grad[:s_ * n], core=core,
+                    factors=_split(fs, self.dims, ranks) if not st else None)
 
     def trace_files(self, ranks, sweeps, seed, cap=1 << 20):
         """make_trace_file + write_trace_csv / write_trace_json of a reference hoqri run."""

@@ -57,12 +57,16 @@ def test_bench_kernel_device_timing():
 
 def test_harness_errors(tmp_path):
     cfg = hq.SolverConfig(ranks=[2, 2])
-    with pytest.raises(hq.CapacityError):
+    res = harness.run_experiment(harness.ExperimentSpec(hq.SolverConfig(ranks=[2, 2], max_sweeps=3), str(tmp_path),
+                                                        synthetic=harness.SyntheticSpec([5, 5], 12, 1),
+                                                        solver=harness.SOLVER_BOTH))
+    assert [p.rsplit("/", 1)[-1] for p in res.trace_paths] == ["hoqri_rep0.trace.csv", "hooi_rep0.trace.csv"]
+    s = json.load(open(res.summary_path))
+    assert "hoqri" in s and "hooi" in s
+    with pytest.raises(hq.ShapeError):
         harness.run_experiment(harness.ExperimentSpec(cfg, str(tmp_path), synthetic=harness.SyntheticSpec([5, 5], 5, 1),
-                                                      solver=harness.SOLVER_BOTH))
+                                                      solver="svd"))
     with pytest.raises(hq.ShapeError):
         harness.run_experiment(harness.ExperimentSpec(cfg, str(tmp_path)))
     with pytest.raises(hq.InfeasibleError):
         harness.run_experiment(harness.ExperimentSpec(cfg, str(tmp_path), synthetic=harness.SyntheticSpec([2, 2], 9, 1)))
-    with pytest.raises(hq.CapacityError):
-        harness.hooi(None, cfg)

@@ -310,24 +310,25 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
     // both factor rows of records [0, cn) -> sF with cp.async, piece-major: consecutive lanes copy
-    // consecutive 16-byte pieces of one row.  (Register-staged LDG.128 would double the gather rate but
-    // needs ~100 registers per thread for a whole tile: measured, spills.)
+    // consecutive 16-byte pieces of one record's rows.  (Register-staged LDG.128 needs ~100 registers per
+    // thread for a whole tile: measured, spills; record-per-thread issue measured 15% slower.)
     constexpr int PA = KA / 2, PP = (KA + KB) / 2;
-    constexpr int ESTEP = C::THREADS / PP, PSTEP = C::THREADS % PP;
     auto gathers_issue = [&](int rb, int cn) {
         const Rec* rec = sRecB + rb * C::CAP;
-        int e = tid / PP, pc = tid % PP;
-        for (; e < cn;) {
-            const Rec& r = rec[e];
-            const double* src = (pc < PA) ? Ua + (size_t)r.j * KA + 2 * pc : Ub + (size_t)r.k * KB + 2 * (pc - PA);
-            double* dst = sF + (size_t)e * C::FW + ((pc < PA) ? 2 * pc : KA + 2 * (pc - PA));
-            cp16(dst, src, (pc < PA) ? pol_a : pol_b);
-            e += ESTEP;
-            pc += PSTEP;
-            if (pc >= PP) {
-                pc -= PP;
-                ++e;
-            }
+        // each of the first (THREADS / PP) * PP threads owns one fixed piece slot of every record it copies:
+        // no per-piece slot arithmetic, one record index load per piece
+        constexpr int RPI = C::THREADS / PP;  // records per iteration
+        if (tid < RPI * PP) {
+            const int pc = tid % PP;
+            const bool isa = pc < PA;
+            const double* base = isa ? Ua + 2 * pc : Ub + 2 * (pc - PA);
+            const int kk = isa ? KA : KB;
+            const int off = isa ? 2 * pc : KA + 2 * (pc - PA);
+            const uint64_t pol = isa ? pol_a : pol_b;
+            const uint32_t* idxp = isa ? &rec[0].j : &rec[0].k;
+            constexpr int RS = sizeof(Rec) / sizeof(uint32_t);
+            for (int e = tid / PP; e < cn; e += RPI)
+                cp16(sF + (size_t)e * C::FW + off, base + (size_t)idxp[e * RS] * kk, pol);
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };

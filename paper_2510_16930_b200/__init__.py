@@ -754,10 +754,10 @@ class Solver:
 
     def status(self):
         """Device status word: sweeps done, Householder fallbacks, abort code, degenerate mode, shifted CholeskyQR3 updates."""
-        out = (C.c_int64 * 5)()
+        out = (C.c_int64 * 6)()
         _check(load_library().hq_solver_status(self._h, out))
         return {"sweeps": out[0], "fallbacks": out[1], "abort": out[2], "degenerate_mode": out[3],
-                "shifted": out[4]}
+                "shifted": out[4], "deficient_kept": out[5]}
 
     def launch_mode_pass(self, mode):
         _check(load_library().hq_solver_launch_mode_pass(self._h, mode))

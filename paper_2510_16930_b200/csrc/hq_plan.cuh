@@ -43,6 +43,7 @@ struct DevStatus {
     unsigned int shifted_count;
     int diag_code;         // abort 5/6 detail: 1 negative gradient, 2 interlacing, 3 not PSD
     int diag_k;            // 1-based index for interlacing
+    unsigned int deficient_count;  // multi-GPU: rank-deficient updates kept on the shifted basis
 };
 
 enum RunIf { kAlways = 0, kOnlyFallback = 1, kOnlyCholQR = 2, kOnlyShifted = 3, kFallbackOrShifted = 4 };

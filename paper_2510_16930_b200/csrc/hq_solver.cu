@@ -329,7 +329,7 @@ struct Solver {
     void setup(const DeviceTensor* t, const hq_config* c, const double* const* init, cudaStream_t stream,
                const Comm* cm = nullptr) {
         T = t;
-        comm = (cm && cm->world > 1) ? cm : nullptr;
+        comm = cm;  // a one-rank communicator runs the distributed path with identity collectives
         s = stream;
         cfg = *c;
         N = t->order;
@@ -1338,6 +1338,7 @@ int hq_solver_status(hq_solver* s, int64_t* out) {
         out[2] = h.abort;
         out[3] = h.degenerate_mode;
         out[4] = h.shifted_count;
+        out[5] = h.deficient_count;
     });
 }
 

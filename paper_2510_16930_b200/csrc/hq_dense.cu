@@ -412,6 +412,37 @@ __global__ void k_reduce_core(const double* __restrict__ mpart, int nslots, uint
     }
 }
 
+// the same reduction for a pass over mode n != 0: G_(n) (K_n x L) refolded into the core layout
+__global__ void k_reduce_core_refold(const double* __restrict__ mpart, int nslots, ModeShape sh, double* core_out,
+                                     const DevStatus* st, int run_if) {
+    if (skip_kernel(st, run_if)) return;
+    int gstride[kMaxOrder];
+    {
+        int ks[kMaxOrder];
+        int j = 0;
+        for (int v = 0; v < sh.order; ++v) ks[v] = (v == sh.n) ? sh.kn : sh.ko[j++];
+        int acc = 1;
+        for (int v = sh.order - 1; v >= 0; --v) {
+            gstride[v] = acc;
+            acc *= ks[v];
+        }
+    }
+    const uint64_t size = (uint64_t)sh.kn * sh.L;
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < size; q += (uint64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int c = 0; c < nslots; ++c) acc += mpart[(size_t)c * size + q];
+        const int r = (int)(q / sh.L), l = (int)(q - (uint64_t)r * sh.L);
+        size_t lin = (size_t)r * gstride[sh.n];
+        int j = 0;
+        for (int v = 0; v < sh.order; ++v) {
+            if (v == sh.n) continue;
+            lin += (size_t)((l / sh.cstride[j]) % sh.ko[j]) * gstride[v];
+            ++j;
+        }
+        core_out[lin] = acc;
+    }
+}
+
 __global__ void k_normsq_one(const double* __restrict__ core, uint64_t size, double* out) {
     __shared__ double red[33];
     double part = 0.0;
@@ -570,6 +601,18 @@ void launch_reduce_core(const double* mpart, int nslots, uint64_t size, double* 
                         int run_if, cudaStream_t s) {
     int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>((size + 255) / 256, (uint64_t)num_sms() * 4));
     k_reduce_core<<<blocks, 256, 0, s>>>(mpart, nslots, size, core_out, st, run_if);
+    HQ_CHECK_LAUNCH();
+}
+
+void launch_reduce_core_mode(const double* mpart, int nslots, const ModeShape& sh, double* core_out,
+                             const DevStatus* st, int run_if, cudaStream_t s) {
+    const uint64_t size = (uint64_t)sh.kn * sh.L;
+    if (sh.n == 0) {
+        launch_reduce_core(mpart, nslots, size, core_out, st, run_if, s);
+        return;
+    }
+    int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>((size + 255) / 256, (uint64_t)num_sms() * 4));
+    k_reduce_core_refold<<<blocks, 256, 0, s>>>(mpart, nslots, sh, core_out, st, run_if);
     HQ_CHECK_LAUNCH();
 }
 

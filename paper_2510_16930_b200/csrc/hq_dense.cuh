@@ -145,6 +145,9 @@ void launch_gt(const double* core, const ModeShape& sh, const int* ranks, double
 // core_out = reduce of M partials (mode 0 unfolding == core layout)
 void launch_reduce_core(const double* mpart, int nslots, uint64_t size, double* core_out, const DevStatus* st,
                         int run_if, cudaStream_t s);
+// core = reduce of the M partials of a kCore pass over mode sh.n, refolded into the core layout
+void launch_reduce_core_mode(const double* mpart, int nslots, const ModeShape& sh, double* core_out,
+                             const DevStatus* st, int run_if, cudaStream_t s);
 // ||G||^2 into *out (deterministic)
 void launch_core_normsq(const double* core, uint64_t size, double* out, cudaStream_t s);
 // max_ij |U^T U - I| over all modes' final factors

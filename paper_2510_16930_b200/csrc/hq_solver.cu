@@ -445,6 +445,15 @@ struct Solver {
     // carry the Gram matrix's conditioning into the core).  Multi-GPU: the
     // all-reduce runs unconditionally in the captured graph, so a conditional
     // recompute goes through core_alt and is copied into place only when it ran.
+    // the mode whose kCore pass is cheapest: the longest rows (fewest non-empty rows) run on the
+    // DMMA long-row path; ties keep the lowest mode
+    int core_mode() const {
+        int best = 0;
+        for (int v = 1; v < N; ++v)
+            if (T->modes[v].nonempty_rows < T->modes[best].nonempty_rows) best = v;
+        return best;
+    }
+
     void compute_core(int p, int run_if, int updated_mode = -1) {
         FactorPtrs f{};
         for (int v = 0; v < N; ++v) {
@@ -452,14 +461,15 @@ struct Solver {
             f.u[v] = U[v][q].get();
             f.k[v] = ranks[v];
         }
-        launch_pass(*T, 0, sh[0], f, kCore, nullptr, pass_out(nullptr), st.get(), run_if, s, rb(0), re(0));
-        const int slots = pass_slots(T->modes[0], sh[0]);
+        const int cm = core_mode();
+        launch_pass(*T, cm, sh[cm], f, kCore, nullptr, pass_out(nullptr), st.get(), run_if, s, rb(cm), re(cm));
+        const int slots = pass_slots(T->modes[cm], sh[cm]);
         if (comm && run_if != kAlways) {
-            launch_reduce_core(mpart.get(), slots, core_size, core_alt.get(), st.get(), run_if, s);
+            launch_reduce_core_mode(mpart.get(), slots, sh[cm], core_alt.get(), st.get(), run_if, s);
             comm->allreduce_sum(core_alt.get(), core_size, s);
             launch_reduce_core(core_alt.get(), 1, core_size, core.get(), st.get(), run_if, s);
         } else {
-            launch_reduce_core(mpart.get(), slots, core_size, core.get(), st.get(), run_if, s);
+            launch_reduce_core_mode(mpart.get(), slots, sh[cm], core.get(), st.get(), run_if, s);
             if (comm) comm->allreduce_sum(core.get(), core_size, s);
         }
     }
@@ -557,7 +567,7 @@ struct Solver {
 
     int launches_per_sweep() const {
         int c = 0;
-        const int core_pass = pass_launch_count(T->modes[0], sh[0]);
+        const int core_pass = pass_launch_count(T->modes[core_mode()], sh[core_mode()]);
         for (int n = 0; n < N; ++n) {
             const int pass = pass_launch_count(T->modes[n], sh[n]);
             if (tracing) c += 1;  // update diagnostics

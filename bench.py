@@ -307,6 +307,8 @@ def run_engine(args, ws, rank, local):
         uid = [hq.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = hq.Comm(ws, rank, uid[0])
+    elif os.environ.get("HQ_BENCH_DIST_PATH") == "1":  # test hook: the distributed path on one rank
+        comm = hq.Comm(1, 0, hq.nccl_unique_id())
     c, coords, vals = workload(args.config)
     dims, ranks = list(c["dims"]), list(c["ranks"])
     N = len(dims)

@@ -15,6 +15,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -90,17 +91,17 @@ Comm::~Comm() {
 }
 
 void Comm::allreduce_sum(double* buf, size_t count, cudaStream_t s) const {
-    if (world == 1 || !count) return;
+    if (!comm || !count) return;  // one rank without NCCL: identity
     HQ_NCCL(nccl().AllReduce(buf, buf, count, ncclFloat64, ncclSum, static_cast<ncclComm_t>(comm), s));
 }
 
 void Comm::allreduce_max(double* buf, size_t count, cudaStream_t s) const {
-    if (world == 1 || !count) return;
+    if (!comm || !count) return;
     HQ_NCCL(nccl().AllReduce(buf, buf, count, ncclFloat64, ncclMax, static_cast<ncclComm_t>(comm), s));
 }
 
 void Comm::allgather_rows(double* buf, const uint64_t* bounds, size_t row_elems, cudaStream_t s) const {
-    if (world == 1) return;
+    if (!comm) return;
     HQ_NCCL(nccl().GroupStart());
     for (int r = 0; r < world; ++r) {
         const size_t off = bounds[r] * row_elems, cnt = (bounds[r + 1] - bounds[r]) * row_elems;
@@ -120,7 +121,10 @@ Comm* comm_create(int world, int rank, const uint8_t* id128) {
     auto* c = new Comm();
     c->world = world;
     c->rank = rank;
-    if (world > 1) {
+    // a one-rank communicator needs no NCCL; HQ_NCCL_ONE_RANK=1 builds a real one-rank NCCL communicator
+    // anyway (exercises the NCCL calls inside the captured sweep on one GPU)
+    const char* force = std::getenv("HQ_NCCL_ONE_RANK");
+    if (world > 1 || (force && force[0] == '1')) {
         ncclUniqueId id;
         std::memcpy(id.internal, id128, NCCL_UNIQUE_ID_BYTES);
         ncclComm_t nc = nullptr;

@@ -22,15 +22,24 @@ def _solve(x, ranks, sweeps, u, comm):
     return sol.download(), sol.status()
 
 
+@pytest.fixture(params=["identity", "nccl"])
+def one_rank(request, monkeypatch):
+    """a one-rank communicator: identity collectives, or a real one-rank NCCL
+    communicator (HQ_NCCL_ONE_RANK=1) so the NCCL calls run inside the captured sweep"""
+    if request.param == "nccl":
+        monkeypatch.setenv("HQ_NCCL_ONE_RANK", "1")
+    return lambda: hq.Comm(1, 0, hq.nccl_unique_id())
+
+
 @pytest.mark.parametrize("name", ["h3", "h4"])
-def test_dist_path_matches_oracle(oracle, name):
+def test_dist_path_matches_oracle(oracle, name, one_rank):
     g = golden("hoqri.npz")
     dims = [int(d) for d in g[f"{name}_dims"]]
     ranks = [int(r) for r in g[f"{name}_ranks"]]
     coords, vals = g[f"{name}_coords"], g[f"{name}_vals"]
     u0 = [g[f"{name}_U0_{m}"] for m in range(len(dims))]
     x = hq.SparseTensor(dims, coords, vals)
-    r, st = _solve(x, ranks, 6, u0, hq.Comm(1, 0))
+    r, st = _solve(x, ranks, 6, u0, one_rank())
     ref = oracle.hoqri(dims, ranks, coords, vals, u0, 6)
     np.testing.assert_allclose([s.objective for s in r.trace.sweeps], ref["objective"], rtol=1e-9)
     for m in range(len(dims)):
@@ -38,19 +47,19 @@ def test_dist_path_matches_oracle(oracle, name):
         assert np.sqrt(2) * np.linalg.norm(ug - ur @ (ur.T @ ug)) <= 1e-8
 
 
-def test_dist_path_shifted_matches_single_gpu():
+def test_dist_path_shifted_matches_single_gpu(one_rank):
     dims, k = [5000, 5000, 5000], 10
     coords, vals = uniform_coo(dims, 50000, 3)
     x = hq.SparseTensor(dims, coords, vals)
     u = hq.random_factors(dims, [k] * 3, 4).factors
     r1, s1 = _solve(x, [k] * 3, 20, u, None)
-    r2, s2 = _solve(x, [k] * 3, 20, u, hq.Comm(1, 0))
+    r2, s2 = _solve(x, [k] * 3, 20, u, one_rank())
     assert s1["shifted"] > 0 and s2["shifted"] == s1["shifted"]
     np.testing.assert_allclose([s.objective for s in r2.trace.sweeps], [s.objective for s in r1.trace.sweeps],
                                rtol=1e-9)
 
 
-def test_dist_path_rank_deficient_keeps_going():
+def test_dist_path_rank_deficient_keeps_going(one_rank):
     """BASELINE config 2's later sweeps need the seeded fill on one GPU; the
     distributed path completes on the shifted basis (counted), never aborts."""
     coords, vals = config_coo(2)
@@ -58,7 +67,7 @@ def test_dist_path_rank_deficient_keeps_going():
     x = hq.SparseTensor(dims, coords, vals)
     u = hq.random_factors(dims, [k] * 3, 1).factors
     r1, s1 = _solve(x, [k] * 3, 20, u, None)
-    r2, s2 = _solve(x, [k] * 3, 20, u, hq.Comm(1, 0))
+    r2, s2 = _solve(x, [k] * 3, 20, u, one_rank())
     assert s1["fallbacks"] > 0 and s2["fallbacks"] == 0 and s2["deficient_kept"] > 0
     assert len(r2.trace.sweeps) == 20
     o1 = np.array([s.objective for s in r1.trace.sweeps])

@@ -264,7 +264,7 @@ struct Solver {
     double initial_objective = 0.0;
 
     DBuf<double> U[kMaxOrder][2];
-    DBuf<double> core, gt, A, mpart, wpart, maxpart, ypart, mred, wred, maxv, r1inv, rinv, rc, w2part, hh;
+    DBuf<double> core, gt, A, mpart, wpart, maxpart, ypart, red3, r1inv, rinv, rc, w2part, hh;
     DBuf<double> ppart[kMaxOrder];  // per-mode drift products (their drift kernels run on the side stream)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork[kMaxOrder] = {nullptr};
@@ -367,9 +367,10 @@ struct Solver {
         wpart.alloc(maxslots * kmax * kmax);
         maxpart.alloc(maxslots);
         ypart.alloc(std::max<size_t>(maxy, 1));
-        mred.alloc(maxLK);
-        wred.alloc(kmax * kmax);
-        maxv.alloc(1);
+        // M, W and max|A| of a mode update in one buffer (per mode: M at 0, W at K_n L, max after W) so
+        // the distributed path all-reduces them in one call (max|A| >= 0 per rank: its sum is zero
+        // exactly when every rank's is, which is all the degeneracy test reads)
+        red3.alloc(maxLK + (size_t)kmax * kmax + 1);
         r1inv.alloc(kmax * kmax);
         rinv.alloc(kmax * kmax);
         rc.alloc(kmax * kmax);
@@ -485,19 +486,20 @@ struct Solver {
         launch_pass(*T, n, m, f, kTTMcTC, gt.get(), pass_out(A.get()), S, kAlways, s, r0, r1);
         mark("pass");
         const int slots = pass_slots(T->modes[n], m);
-        launch_reduce_pass(mpart.get(), m.kn * m.L, wpart.get(), K * K, maxpart.get(), slots, mred.get(), wred.get(),
-                           maxv.get(), S, kAlways, s);
+        double* mred = red3.get();
+        double* wred = mred + (size_t)m.kn * m.L;
+        double* maxv = wred + (size_t)K * K;
+        launch_reduce_pass(mpart.get(), m.kn * m.L, wpart.get(), K * K, maxpart.get(), slots, mred, wred, maxv, S,
+                           kAlways, s);
         mark("reduce");
         if (comm) {  // M, W, max|A| over all ranks' rows
-            comm->allreduce_sum(mred.get(), (size_t)m.kn * m.L, s);
-            comm->allreduce_sum(wred.get(), (size_t)K * K, s);
-            comm->allreduce_max(maxv.get(), 1, s);
+            comm->allreduce_sum(mred, (size_t)m.kn * m.L + (size_t)K * K + 1, s);
         }
         if (tracing) {  // pre-update diagnostics (solvers.cpp:126-137): W = A^T A and G_(n) at hand
             UpdTrace ut{tr_grad.get(), tr_fb.get(), tr_sig.get(), tr_lam.get(), tr_t.get(), kmax_};
-            launch_update_diag(wred.get(), gt.get(), K, m.L, n, N, ut, S, s);
+            launch_update_diag(wred, gt.get(), K, m.L, n, N, ut, S, s);
         }
-        launch_chol1(wred.get(), maxv.get(), K, r1inv.get(), S, n + 1, dims[n], s, comm != nullptr);
+        launch_chol1(wred, maxv, K, r1inv.get(), S, n + 1, dims[n], s, comm != nullptr);
         mark("chol1");
         const double* a_loc = A.get() + r0 * K;
         double* unew = U[n][1 - p].get();
@@ -507,12 +509,12 @@ struct Solver {
         if (!comm) {
             launch_gram2(a_loc, lrows, K, r1inv.get(), unew, w2part.get(), S, s);  // U_new <- Q1
             mark("gram2");
-            launch_chol2(w2part.get(), dense_slots(), K, r1inv.get(), rinv.get(), rc.get(), mred.get(), &m, core.get(),
+            launch_chol2(w2part.get(), dense_slots(), K, r1inv.get(), rinv.get(), rc.get(), mred, &m, core.get(),
                          S, s);
             mark("chol2");
             // shifted CholeskyQR3 branch (device flag): U_new <- Q2, R3
             launch_gram3(unew, lrows, K, rinv.get(), w2part.get(), S, s);
-            launch_chol3(w2part.get(), dense_slots(), K, rc.get(), rinv.get(), wred.get(), S, s);
+            launch_chol3(w2part.get(), dense_slots(), K, rc.get(), rinv.get(), wred, S, s);
             mark("cholqr3(no-op)");
             launch_apply(unew, lrows, K, rinv.get(), unew, uold, pp, true, S, kOnlyCholQR, s);
             mark("apply");
@@ -528,13 +530,13 @@ struct Solver {
             launch_reduce_pass(nullptr, 0, w2part.get(), K * K, nullptr, dense_slots(), nullptr, w2red.get(), nullptr, S,
                                kOnlyCholQR, s);
             comm->allreduce_sum(w2red.get(), (size_t)K * K, s);
-            launch_chol2(w2red.get(), 1, K, r1inv.get(), rinv.get(), rc.get(), mred.get(), &m, core.get(), S, s, true);
+            launch_chol2(w2red.get(), 1, K, r1inv.get(), rinv.get(), rc.get(), mred, &m, core.get(), S, s, true);
             // shifted CholeskyQR3 (device flag; the all-reduce always runs, on stale data when skipped)
             launch_gram3(uloc, lrows, K, rinv.get(), w2part.get(), S, s);
             launch_reduce_pass(nullptr, 0, w2part.get(), K * K, nullptr, dense_slots(), nullptr, w2red.get(), nullptr, S,
                                kOnlyShifted, s);
             comm->allreduce_sum(w2red.get(), (size_t)K * K, s);
-            launch_chol3(w2red.get(), 1, K, rc.get(), rinv.get(), wred.get(), S, s, true);
+            launch_chol3(w2red.get(), 1, K, rc.get(), rinv.get(), wred, S, s, true);
             launch_apply(uloc, lrows, K, rinv.get(), uloc, uold + r0 * K, pp, true, S, kOnlyCholQR, s);
             launch_reduce_pass(nullptr, 0, pp, K * K, nullptr, dense_slots(), nullptr, pred.get(), nullptr, S, kAlways,
                                s);

@@ -196,6 +196,11 @@ int hq_densify_unfold(const hq_tensor* t, int mode, uint64_t capacity_cap, doubl
 int hq_ttmc_unfold_dense(const hq_tensor* t, const double* const* factors, const uint64_t* ranks, int mode,
                          uint64_t capacity_cap, double* out);
 int hq_svd_leading(uint64_t rows, uint64_t cols, const double* y, uint64_t k, double* u_out);
+/* jacobi_eig_sym (dense_core.hpp:85-90): eigenpairs of the symmetrised n x n
+ * host matrix, values descending, eigenvector j in column j of the row-major
+ * `vectors` (may be NULL); cuSOLVER syevd on the device, so vector signs may
+ * differ from the reference's Jacobi rotations */
+int hq_sym_eig(uint64_t n, const double* m, double* values_desc, double* vectors);
 int hq_init_factors(const hq_tensor* t, const hq_config* cfg, double* const* factors_out);
 int hq_hooi(const hq_tensor* t, const hq_config* cfg, const double* const* init_factors,
             double* const* factors_out, double* core_out, hq_trace* trace);

@@ -94,6 +94,13 @@ Matrix qr_orthonormal(const Matrix& a);                          // dense_core.h
 Matrix unfold_core(const CoreTensor& g, std::size_t mode);       // dense_core.hpp:72
 std::vector<std::size_t> unfold_col_strides(const std::vector<std::size_t>& dims,
                                             std::size_t mode);   // dense_core.hpp:77-78
+double nuclear_norm(const Matrix& m);                             // dense_core.hpp:67 (device eigen-solve)
+std::vector<double> gram_eigvals_desc(const Matrix& m);          // dense_core.hpp:82 (device eigen-solve)
+struct EigResult {                                               // dense_core.hpp:86-89
+    std::vector<double> values;
+    Matrix vectors;
+};
+EigResult jacobi_eig_sym(Matrix m);  // dense_core.hpp:90: same pairs (device syevd; vector signs may differ)
 
 // -------------------------------------------------- sparse_tensor.hpp ----
 using index_t = std::uint32_t;
@@ -170,7 +177,21 @@ Matrix ttmctc_matrix(const SparseTensor& x, const FactorSet& u, std::size_t mode
 constexpr std::size_t kDefaultCapacityCap = std::size_t{1} << 31;
 
 // ---------------------------------------------------------- manifold.hpp --
+struct GradientReport {  // manifold.hpp:14-19
+    std::vector<double> per_mode_norm_sq;
+    double total_norm_sq = 0.0;
+    std::vector<std::vector<double>> sigma;
+    std::vector<std::vector<double>> lambda;
+};
+Matrix project_tangent(const Matrix& u, const Matrix& a);                  // manifold.hpp:23
+Matrix riemannian_grad(const Matrix& u, const Matrix& a, const Matrix& gn);  // manifold.hpp:27
+double grad_norm_sq(const Matrix& a, const Matrix& gn);                    // manifold.hpp:31
 double subspace_distance(const Matrix& u, const Matrix& v);  // manifold.hpp:34-36 (device)
+struct InterlacingResult {  // manifold.hpp:38-42
+    std::vector<double> sigma, lambda;
+    double min_margin = 0.0;
+};
+InterlacingResult interlacing_check(const Matrix& a, const Matrix& gn);     // manifold.hpp:46
 
 // ----------------------------------------------------------- solvers.hpp --
 enum class InitMode { kRandom, kHosvd };
@@ -231,5 +252,12 @@ SolveResult hoqri(const SparseTensor& x, const SolverConfig& config);        // 
 // B200 extension: start from caller-supplied factors (init_factors result)
 SolveResult hoqri_from(const SparseTensor& x, const SolverConfig& config, const FactorSet& start);
 double fit_error(const SparseTensor& x, const TuckerModel& model);           // solvers.hpp:87
+GradientReport gradient_report(const SparseTensor& x, const FactorSet& u);   // solvers.hpp:91 (device TTMcTC)
+struct DescentCheck {                                                       // solvers.hpp:93-98
+    bool ok = true;
+    std::size_t checked = 0, violations = 0;
+    double worst_violation = 0.0;
+};
+DescentCheck check_descent_inequality(const IterationTrace& trace, double data_norm_sq);  // solvers.hpp:102-103
 
 }  // namespace tucker

@@ -122,6 +122,7 @@ EXPORTED_SYMBOLS = [
     "hq_solver_create_dist", "hq_bench_ttmctc", "hq_gen_synthetic",
     "hq_tns_parse", "hq_tns_parse_file", "hq_tns_info", "hq_tns_copy", "hq_tns_tensor", "hq_tns_destroy",
     "hq_densify_unfold", "hq_ttmc_unfold_dense", "hq_svd_leading", "hq_init_factors", "hq_hooi",
+    "hq_sym_eig",
 ]
 
 _lib = None
@@ -170,6 +171,7 @@ def load_library(path: str = None) -> C.CDLL:
     L.hq_ttmc_unfold_dense.argtypes = [vp, vp, _u64p, C.c_int, C.c_uint64, _f64p]
     L.hq_svd_leading.argtypes = [C.c_uint64, C.c_uint64, _f64p, C.c_uint64, _f64p]
     L.hq_init_factors.argtypes = [vp, C.POINTER(HqConfig), vp]
+    L.hq_sym_eig.argtypes = [C.c_uint64, _f64p, _f64p, vp]
     L.hq_hooi.argtypes = [vp, C.POINTER(HqConfig), vp, vp, vp, C.POINTER(HqTrace)]
     L.hq_solver_create.argtypes = [vp, C.POINTER(HqConfig), vp, vp, pp]
     L.hq_solver_destroy.argtypes = [vp]
@@ -634,6 +636,19 @@ def svd_leading(y, k: int) -> np.ndarray:
     if k:
         _check(load_library().hq_svd_leading(m, p, y.reshape(-1), int(k), u.reshape(-1)))
     return u
+
+
+def jacobi_eig_sym(m):
+    """dense_core.hpp:85-90: eigenpairs of the symmetrised matrix, values descending, vectors in columns
+    (device eigen-solve; vector signs may differ from the reference's Jacobi rotations)."""
+    m = np.ascontiguousarray(m, dtype=np.float64)
+    if m.ndim != 2 or m.shape[0] != m.shape[1]:
+        raise ShapeError("jacobi_eig_sym: square matrix required")
+    n = m.shape[0]
+    vals, vecs = np.zeros(n, np.float64), np.zeros((n, n), np.float64)
+    if n:
+        _check(load_library().hq_sym_eig(n, m.reshape(-1), vals, vecs.ctypes.data))
+    return vals, vecs
 
 
 def densify_unfold(x: SparseTensor, mode: int, capacity_cap: int = 1 << 31) -> np.ndarray:

@@ -108,6 +108,17 @@ __global__ void k_scale_col(double* u, uint64_t m, int k, int j, double inv) {
         u[i * k + j] *= inv;
 }
 
+// jacobi_eig_sym symmetrises its input first (dense_core.cpp:204-210)
+__global__ void k_symmetrize(double* m, uint64_t n) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n * n; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = t / n, j = t % n;
+        if (j <= i) continue;
+        const double avg = 0.5 * (m[i * n + j] + m[j * n + i]);
+        m[i * n + j] = avg;
+        m[j * n + i] = avg;
+    }
+}
+
 __global__ void k_max_abs(const double* __restrict__ v, uint64_t n, double* out) {
     __shared__ double red[32];
     double m = 0.0;
@@ -271,6 +282,43 @@ void svd_leading_dev(const double* y, uint64_t m, uint64_t p, int k, double* u_o
     }
     QrWork qw;
     qr_device(uu.get(), m, k, u_out, qw, s);
+}
+
+void sym_eig_host(uint64_t n, const double* m, double* values_desc, double* vectors, cudaStream_t s) {
+    if (n == 0) return;
+    if (n > 46340) fail(HQ_ERR_CAPACITY, "sym_eig: matrix above the dense eigen-solver limit");
+    DenseLib& d = dense_lib(s);
+    DBuf<double> g, w;
+    g.alloc(n * n);
+    w.alloc(n);
+    HQ_CUDA(cudaMemcpyAsync(g.get(), m, sizeof(double) * n * n, cudaMemcpyHostToDevice, s));
+    k_symmetrize<<<grid_for(n * n), 256, 0, s>>>(g.get(), n);
+    HQ_CHECK_LAUNCH();
+    int lwork = 0;
+    if (cusolverDnDsyevd_bufferSize(d.sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)n, g.get(), (int)n,
+                                    w.get(), &lwork) != CUSOLVER_STATUS_SUCCESS)
+        fail(HQ_ERR_CUDA, "cusolverDnDsyevd_bufferSize failed");
+    DBuf<double> work;
+    work.alloc(std::max(1, lwork));
+    DBuf<int> info;
+    info.alloc(1);
+    if (cusolverDnDsyevd(d.sol, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, (int)n, g.get(), (int)n, w.get(),
+                         work.get(), lwork, info.get()) != CUSOLVER_STATUS_SUCCESS)
+        fail(HQ_ERR_CUDA, "cusolverDnDsyevd failed");
+    std::vector<double> lam(n), vec(n * n);
+    int hinfo = 0;
+    HQ_CUDA(cudaMemcpyAsync(&hinfo, info.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaMemcpyAsync(lam.data(), w.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaMemcpyAsync(vec.data(), g.get(), sizeof(double) * n * n, cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaStreamSynchronize(s));
+    if (hinfo != 0) fail(HQ_ERR_DIAGNOSTIC, "sym_eig: the symmetric eigen-solver did not converge");
+    // ascending pairs, vector j = column j (column-major) -> descending, vectors as row-major columns
+    for (uint64_t j = 0; j < n; ++j) {
+        const uint64_t src = n - 1 - j;
+        values_desc[j] = lam[src];
+        if (vectors)
+            for (uint64_t i = 0; i < n; ++i) vectors[i * n + j] = vec[src * n + i];
+    }
 }
 
 void hosvd_init_dev(const DeviceTensor& T, const int* ranks, uint64_t cap, double* const* U, cudaStream_t s) {

@@ -13,6 +13,8 @@ void ttmc_unfold_dense_dev(const DeviceTensor& T, int mode, const FactorPtrs& f,
                            DBuf<double>& y, cudaStream_t s);
 // u_out: m x k device, y: m x p device
 void svd_leading_dev(const double* y, uint64_t m, uint64_t p, int k, double* u_out, cudaStream_t s);
+// symmetric eigenpairs of a host n x n matrix (descending; vectors row-major, may be null)
+void sym_eig_host(uint64_t n, const double* m, double* values_desc, double* vectors, cudaStream_t s);
 // HOSVD (solvers.cpp:202-215) into device factor buffers U[v] (I_v x K_v)
 void hosvd_init_dev(const DeviceTensor& T, const int* ranks, uint64_t cap, double* const* U, cudaStream_t s);
 // the HOOI solve (solvers.cpp:50-178 with Algorithm::kHooi)

@@ -147,7 +147,10 @@ struct Cfg {
     static constexpr int TR = TP * TQ;           // lanes per row
     static constexpr int BP = KA / TP;
     static constexpr int BQ = KB / TQ;
-    static constexpr int WARPS = 4;
+#ifndef HQ_WARPS
+#define HQ_WARPS 4
+#endif
+    static constexpr int WARPS = HQ_WARPS;
     static constexpr int THREADS = 32 * WARPS;
     static constexpr int R = THREADS / TR;       // rows per tile
     static constexpr int RPW = 32 / TR;          // rows per warp

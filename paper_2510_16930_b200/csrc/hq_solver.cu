@@ -1161,6 +1161,10 @@ int hq_svd_leading(uint64_t rows, uint64_t cols, const double* y, uint64_t k, do
     });
 }
 
+int hq_sym_eig(uint64_t n, const double* m, double* values_desc, double* vectors) {
+    return guard([&] { sym_eig_host(n, m, values_desc, vectors, nullptr); });
+}
+
 int hq_init_factors(const hq_tensor* t, const hq_config* cfg, double* const* factors_out) {
     return guard([&] {
         const DeviceTensor& T = t->t;

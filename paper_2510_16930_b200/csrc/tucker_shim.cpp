@@ -171,6 +171,41 @@ Matrix qr_orthonormal(const Matrix& a) {
     return q;
 }
 
+EigResult jacobi_eig_sym(Matrix m) {  // dense_core.cpp:200-262 contract; eigen-solve on the device
+    if (m.rows != m.cols) throw ShapeError("jacobi_eig_sym: square matrix required");
+    EigResult r;
+    r.values.resize(m.rows);
+    r.vectors = Matrix(m.rows, m.rows);
+    check(hq_sym_eig(m.rows, m.data.data(), r.values.data(), r.vectors.data.data()));
+    return r;
+}
+
+std::vector<double> gram_eigvals_desc(const Matrix& m) {  // dense_core.cpp:371-386
+    if (m.rows != m.cols) throw ShapeError("gram_eigvals_desc: square matrix required");
+    const double scale = std::max(1.0, std::sqrt(frob_norm_sq(m)));
+    for (std::size_t i = 0; i < m.rows; ++i)
+        for (std::size_t j = i + 1; j < m.cols; ++j)
+            if (std::fabs(m(i, j) - m(j, i)) > 1e-10 * scale)
+                throw ContractError("gram_eigvals_desc: matrix is not symmetric");
+    std::vector<double> ev(m.rows);
+    check(hq_sym_eig(m.rows, m.data.data(), ev.data(), nullptr));
+    for (double& v : ev) {
+        if (v < -1e-10 * scale) throw ContractError("gram_eigvals_desc: matrix is not PSD");
+        v = std::max(v, 0.0);
+    }
+    return ev;
+}
+
+double nuclear_norm(const Matrix& m) {  // dense_core.cpp:329-335: sum of sqrt(eig(M^T M))
+    if (m.rows != m.cols) throw ShapeError("nuclear_norm: square matrix required");
+    const Matrix mtm = matmul_tn(m, m);
+    std::vector<double> ev(m.rows);
+    check(hq_sym_eig(m.rows, mtm.data.data(), ev.data(), nullptr));
+    double s = 0.0;
+    for (double v : ev) s += std::sqrt(std::max(v, 0.0));
+    return s;
+}
+
 std::vector<std::size_t> unfold_col_strides(const std::vector<std::size_t>& dims, std::size_t mode) {
     if (mode >= dims.size()) throw RangeError("unfold: mode out of range");
     std::vector<std::size_t> st(dims.size(), 0);
@@ -352,6 +387,56 @@ Matrix ttmctc_matrix(const SparseTensor& x, const FactorSet& u, std::size_t mode
     return ttmctc_common(x, u, mode, nullptr, 1, ws);
 }
 
+// -------------------------------------------------------------- manifold --
+Matrix project_tangent(const Matrix& u, const Matrix& a) {  // manifold.cpp:10-22: A - U sym(U^T A)
+    if (u.rows != a.rows || u.cols != a.cols)
+        throw ShapeError("project_tangent: U and A must have the same shape");
+    Matrix s = matmul_tn(u, a);
+    for (std::size_t i = 0; i < s.rows; ++i)
+        for (std::size_t j = i + 1; j < s.cols; ++j) s(i, j) = s(j, i) = 0.5 * (s(i, j) + s(j, i));
+    const Matrix us = matmul(u, s);
+    Matrix out = a;
+    for (std::size_t i = 0; i < out.data.size(); ++i) out.data[i] -= us.data[i];
+    return out;
+}
+
+Matrix riemannian_grad(const Matrix& u, const Matrix& a, const Matrix& gn) {  // manifold.cpp:24-35
+    if (u.rows != a.rows || u.cols != a.cols)
+        throw ShapeError("riemannian_grad: U and A must have the same shape");
+    if (gn.rows != u.cols) throw ShapeError("riemannian_grad: core unfolding does not match the mode rank");
+    const Matrix ugg = matmul(u, matmul_nt(gn, gn));
+    Matrix out(a.rows, a.cols);
+    for (std::size_t i = 0; i < out.data.size(); ++i) out.data[i] = 2.0 * (a.data[i] - ugg.data[i]);
+    return out;
+}
+
+double grad_norm_sq(const Matrix& a, const Matrix& gn) {  // manifold.cpp:37-53: 4(||A||^2 - ||G G^T||^2)
+    if (gn.rows != a.cols) throw ShapeError("grad_norm_sq: core unfolding does not match the mode rank");
+    const double a_sq = frob_norm_sq(a);
+    const double r = 4.0 * (a_sq - frob_norm_sq(matmul_nt(gn, gn)));
+    if (r < -1e-8 * std::max(1.0, 4.0 * a_sq))
+        throw DiagnosticError("grad_norm_sq is negative beyond rounding; orthonormality is broken upstream");
+    if (std::fabs(r) <= 1e-10) return 0.0;
+    return std::max(r, 0.0);
+}
+
+InterlacingResult interlacing_check(const Matrix& a, const Matrix& gn) {  // manifold.cpp:62-84
+    if (gn.rows != a.cols) throw ShapeError("interlacing_check: core unfolding does not match the mode rank");
+    InterlacingResult r;
+    r.sigma = gram_eigvals_desc(matmul_tn(a, a));
+    for (double& v : r.sigma) v = std::sqrt(v);
+    r.lambda = gram_eigvals_desc(matmul_nt(gn, gn));
+    const double scale = std::max(1.0, r.sigma.empty() ? 0.0 : r.sigma[0]);
+    for (std::size_t k = 0; k < r.sigma.size(); ++k) {
+        const double margin = r.sigma[k] - r.lambda[k];
+        if (k == 0 || margin < r.min_margin) r.min_margin = margin;
+        if (margin < -1e-9 * scale)
+            throw DiagnosticError("interlacing violated at k=" + std::to_string(k + 1) +
+                                  "; upstream state is numerically corrupted");
+    }
+    return r;
+}
+
 double subspace_distance(const Matrix& u, const Matrix& v) {
     if (u.rows != v.rows || u.cols != v.cols) throw ShapeError("subspace_distance: shapes differ");
     double d = 0.0;
@@ -523,6 +608,36 @@ SolveResult hooi(const SparseTensor& x, const SolverConfig& config) {  // solver
 
 SolveResult hoqri_from(const SparseTensor& x, const SolverConfig& config, const FactorSet& start) {
     return solve_impl(x, config, &start);
+}
+
+GradientReport gradient_report(const SparseTensor& x, const FactorSet& u) {  // solvers.cpp:238-252
+    const CoreTensor core = ttmc_core(x, u);
+    GradientReport rep;
+    for (std::size_t n = 0; n < x.order(); ++n) {
+        const Matrix a = ttmctc_elementwise(x, u, n, &core);
+        const Matrix gn = unfold_core(core, n);
+        rep.per_mode_norm_sq.push_back(grad_norm_sq(a, gn));
+        InterlacingResult il = interlacing_check(a, gn);
+        rep.sigma.push_back(std::move(il.sigma));
+        rep.lambda.push_back(std::move(il.lambda));
+        rep.total_norm_sq += rep.per_mode_norm_sq.back();
+    }
+    return rep;
+}
+
+DescentCheck check_descent_inequality(const IterationTrace& trace, double data_norm_sq) {  // solvers.cpp:254-270
+    DescentCheck out;
+    const double slack = 1e-8 * data_norm_sq * data_norm_sq;
+    for (const ModeUpdateRecord& up : trace.updates) {
+        ++out.checked;
+        const double excess = up.grad_norm_sq - (4.0 * data_norm_sq * (up.f_after - up.f_before) + slack);
+        if (excess > 0.0) {
+            ++out.violations;
+            out.ok = false;
+        }
+        out.worst_violation = std::max(out.worst_violation, excess);
+    }
+    return out;
 }
 
 double fit_error(const SparseTensor& x, const TuckerModel& model) {

@@ -97,3 +97,19 @@ def test_hooi_degenerate():
     with pytest.raises(hq.DegenerateStateError) as e:
         hq.hooi(x, hq.SolverConfig(ranks=[1, 1, 1], max_sweeps=5))
     assert e.value.mode == 1
+
+
+@pytest.mark.parametrize("n", [1, 3, 10, 40])
+def test_sym_eig(n):
+    """jacobi_eig_sym contract (dense_core.cpp:200-262): the symmetrised input's eigenpairs, descending."""
+    rng = np.random.default_rng(n)
+    b = rng.standard_normal((n, n))
+    m = b @ b.T + 1e-13 * rng.standard_normal((n, n))  # slightly asymmetric: the call symmetrises
+    vals, vecs = hq.jacobi_eig_sym(m)
+    ms = 0.5 * (m + m.T)
+    ref = np.linalg.eigvalsh(ms)[::-1]
+    scale = max(1.0, float(np.abs(ref).max()))
+    assert np.all(np.diff(vals) <= 0)
+    assert np.abs(vals - ref).max() <= 1e-12 * scale
+    assert np.abs(ms @ vecs - vecs * vals).max() <= 1e-11 * scale
+    assert np.abs(vecs.T @ vecs - np.eye(n)).max() <= 1e-12

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cstdlib>
 
 #include <cstdint>
 #include <stdexcept>
@@ -47,7 +48,10 @@ inline void device_pool_init() {
         cudaGetDevice(&dev);
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = 64ull << 30;
+            // freed blocks stay mapped in the pool (like a caching allocator): re-mapping
+            // tens of GB between solves costs 100+ ms.  HQ_POOL_RELEASE_GB caps what is kept.
+            uint64_t thr = ~0ull;
+            if (const char* e = std::getenv("HQ_POOL_RELEASE_GB")) thr = std::strtoull(e, nullptr, 10) << 30;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }
         return 0;

@@ -15,7 +15,10 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "hq_internal.cuh"
@@ -90,17 +93,52 @@ __global__ void k_run_starts(const uint32_t* __restrict__ head, const uint32_t* 
         if (head[i]) start[runid[i]] = (uint32_t)i;
 }
 
-// sparse_tensor.cpp:58-68: each run's values summed in sorted (= input) order
+// sparse_tensor.cpp:58-68: each run's values summed in sorted (= input) order.
+// Runs longer than kLongRun (hot cells of skewed inputs: 10^5 duplicates are
+// common under Zipf draws) would serialise one thread on a chain of dependent
+// gathers; they are queued for k_merge_long instead.
+constexpr uint64_t kLongRun = 128;
+
 __global__ void k_merge(const uint32_t* __restrict__ coords, const double* __restrict__ vals,
                         const uint32_t* __restrict__ perm, const uint32_t* __restrict__ start, uint64_t nruns,
-                        uint64_t n, int order, uint32_t* __restrict__ out_coords, double* __restrict__ out_vals) {
+                        uint64_t n, int order, uint32_t* __restrict__ out_coords, double* __restrict__ out_vals,
+                        uint32_t* __restrict__ long_runs, unsigned int* __restrict__ n_long) {
     for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < nruns; u += (uint64_t)gridDim.x * blockDim.x) {
         uint64_t s = start[u], e = (u + 1 < nruns) ? start[u + 1] : n;
         uint32_t p0 = perm[s];
+        for (int m = 0; m < order; ++m) out_coords[u * order + m] = coords[(uint64_t)p0 * order + m];
+        if (e - s > kLongRun) {
+            long_runs[atomicAdd(n_long, 1u)] = (uint32_t)u;
+            continue;
+        }
         double acc = vals[p0];
         for (uint64_t p = s + 1; p < e; ++p) acc += vals[perm[p]];
         out_vals[u] = acc;
-        for (int m = 0; m < order; ++m) out_coords[u * order + m] = coords[(uint64_t)p0 * order + m];
+    }
+}
+
+// one block per long run: thread-strided partial sums in input order, then a
+// fixed reduction tree, so the merged value does not depend on scheduling
+__global__ void __launch_bounds__(256) k_merge_long(const double* __restrict__ vals, const uint32_t* __restrict__ perm,
+                                                    const uint32_t* __restrict__ start, uint64_t nruns, uint64_t n,
+                                                    const uint32_t* __restrict__ long_runs,
+                                                    const unsigned int* __restrict__ n_long,
+                                                    double* __restrict__ out_vals) {
+    __shared__ double red[256];
+    const unsigned int cnt = *n_long;
+    for (unsigned int i = blockIdx.x; i < cnt; i += gridDim.x) {
+        const uint32_t u = long_runs[i];
+        const uint64_t s = start[u], e = (u + 1 < nruns) ? start[u + 1] : n;
+        double acc = 0.0;
+        for (uint64_t p = s + threadIdx.x; p < e; p += blockDim.x) acc += vals[perm[p]];
+        red[threadIdx.x] = acc;
+        __syncthreads();
+        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+            if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) out_vals[u] = red[0];
+        __syncthreads();
     }
 }
 
@@ -193,6 +231,27 @@ int bit_width(uint64_t extent) {
     return b;
 }
 
+// HQ_PROFILE_BUILD=1: per-phase wall times of the layout build (stream-synchronised; diagnostics only)
+struct PhaseClock {
+    cudaStream_t s;
+    bool on;
+    std::chrono::steady_clock::time_point t;
+    explicit PhaseClock(cudaStream_t st) : s(st), on(std::getenv("HQ_PROFILE_BUILD") != nullptr) {
+        if (on) {
+            cudaStreamSynchronize(s);
+            t = std::chrono::steady_clock::now();
+        }
+    }
+    void mark(const char* what, int mode = -1) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[build] %-14s%s%d %8.2f ms\n", what, mode >= 0 ? " mode " : "", mode >= 0 ? mode : 0,
+                     std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
 }  // namespace
 
 double device_sum_sq(const double* v, uint64_t n, cudaStream_t s) {
@@ -219,6 +278,7 @@ void build_tensor(DeviceTensor& T, int order, const uint64_t* dims, uint64_t nnz
         if (dims[m] > 0x100000000ull) fail(HQ_ERR_CAPACITY, "extent above 2^32");
     T.order = order;
     for (int m = 0; m < order; ++m) T.dims[m] = dims[m];
+    PhaseClock clk(s);
 
     // ---- validation (sparse_tensor.cpp:29-38)
     if (nnz) {
@@ -245,6 +305,7 @@ void build_tensor(DeviceTensor& T, int order, const uint64_t* dims, uint64_t nnz
             fail(HQ_ERR_VALUE, "non-finite value at entry " + std::to_string(hb));
         }
     }
+    clk.mark("validate");
 
     // ---- lexicographic sort (sparse_tensor.cpp:43-53)
     KeySpec ks{};
@@ -283,6 +344,7 @@ void build_tensor(DeviceTensor& T, int order, const uint64_t* dims, uint64_t nnz
             std::swap(p0, p1);
         }
         perm = std::move(p0);
+        clk.mark("lexsort");
 
         // ---- run heads and merge (sparse_tensor.cpp:54-70)
         DBuf<uint32_t> head, runid;
@@ -303,10 +365,18 @@ void build_tensor(DeviceTensor& T, int order, const uint64_t* dims, uint64_t nnz
         k_run_starts<<<grid_for(nnz), 256, 0, s>>>(head.get(), runid.get(), nnz, start.get());
         T.coords.alloc(nruns * order);
         T.vals.alloc(nruns);
+        DBuf<uint32_t> long_runs;
+        long_runs.alloc(std::max<uint64_t>(1, std::min<uint64_t>(nruns, nnz / (kLongRun + 1))));
+        DBuf<unsigned int> n_long;
+        n_long.alloc(1);
+        HQ_CUDA(cudaMemsetAsync(n_long.get(), 0, sizeof(unsigned int), s));
         k_merge<<<grid_for(nruns), 256, 0, s>>>(coords_in, vals_in, perm.get(), start.get(), nruns, nnz, order,
-                                               T.coords.get(), T.vals.get());
+                                               T.coords.get(), T.vals.get(), long_runs.get(), n_long.get());
+        k_merge_long<<<num_sms() * 4, 256, 0, s>>>(vals_in, perm.get(), start.get(), nruns, nnz, long_runs.get(),
+                                                  n_long.get(), T.vals.get());
         HQ_CHECK_LAUNCH();
     }
+    clk.mark("merge");
     T.nnz = nruns;
     const uint64_t n = nruns;
     T.norm_sq = n ? device_sum_sq(T.vals.get(), n, s) : 0.0;
@@ -335,6 +405,7 @@ void build_tensor(DeviceTensor& T, int order, const uint64_t* dims, uint64_t nnz
             radix_sort_pairs(key.get(), skey.get(), io.get(), L.entries.get(), n, std::max(1, ks.bits[m]), s);
             sorted_keys = skey.get();
         }
+        clk.mark("mode sort", m);
         k_rowptr<<<grid_for(n + 1), 256, 0, s>>>(sorted_keys, n, dims[m], L.rowptr.get());
         if (n) {
             uint32_t* o[7] = {nullptr};
@@ -352,7 +423,9 @@ void build_tensor(DeviceTensor& T, int order, const uint64_t* dims, uint64_t nnz
         HQ_CUDA(cudaMemcpyAsync(&hc, cnt.get(), 8, cudaMemcpyDeviceToHost, s));
         HQ_CUDA(cudaStreamSynchronize(s));
         L.nonempty_rows = hc;
+        clk.mark("mode streams", m);
         plan_mode(L, n, s);
+        clk.mark("mode plan", m);
     }
     HQ_CUDA(cudaStreamSynchronize(s));
 }

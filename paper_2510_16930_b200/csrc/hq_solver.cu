@@ -810,6 +810,12 @@ static int tensor_create_impl(int order, const uint64_t* dims, uint64_t nnz, con
             v.alloc(nnz);
             HQ_CUDA(cudaMemcpyAsync(c.get(), coords, sizeof(uint32_t) * nnz * order, cudaMemcpyHostToDevice, s));
             HQ_CUDA(cudaMemcpyAsync(v.get(), values, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+            if (std::getenv("HQ_PROFILE_BUILD")) {
+                const auto t0 = std::chrono::steady_clock::now();
+                HQ_CUDA(cudaStreamSynchronize(s));
+                std::fprintf(stderr, "[build] upload wait     %8.2f ms\n",
+                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+            }
             build_tensor(h->t, order, dims, nnz, c.get(), v.get(), s);
         }
         *out = h.release();

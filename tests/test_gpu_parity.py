@@ -33,6 +33,27 @@ def subspace_gap(ug, ur):
 
 
 # ------------------------------------------------------------------ layout --
+def test_long_duplicate_runs():
+    """Hot cells (runs far above the one-thread merge length) merge to the per-cell sum, deterministically,
+    next to ordinary short runs; coordinates / order are the reference's (sorted, unique)."""
+    rng = np.random.default_rng(5)
+    dims = [50, 40, 30]
+    hot = np.array([[3, 4, 5]] * 20000 + [[7, 1, 2]] * 300 + [[0, 0, 0]] * 129, np.uint32)
+    rest = np.stack([rng.integers(0, d, 10000) for d in dims], 1).astype(np.uint32)
+    coords = np.concatenate([hot, rest])
+    perm = rng.permutation(len(coords))
+    coords = coords[perm]
+    vals = rng.standard_normal(len(coords))
+    x = hq.SparseTensor(dims, coords, vals)
+    uc, inv = np.unique(coords, axis=0, return_inverse=True)
+    sums = np.zeros(len(uc))
+    np.add.at(sums, inv.reshape(-1), vals)
+    assert (x.coords() == uc).all()
+    np.testing.assert_allclose(x.values(), sums, rtol=1e-12, atol=1e-12)
+    y = hq.SparseTensor(dims, coords, vals)
+    assert sha(y.values()) == sha(x.values())
+
+
 @pytest.mark.parametrize("name", ["hand", "gs4", "gs2", "gs3", "dups"])
 def test_layout_bit_exact(name):
     g = golden("tensors.npz")

@@ -138,7 +138,8 @@ __global__ void __launch_bounds__(kRgWarps * 32)
                 const double av = sx[(4 * ks + tig) * C::LD + 8 * mt + gid];
 #pragma unroll
                 for (int nt = 0; nt < C::NT; ++nt)
-                    dmma884(acc[mt][nt][0], acc[mt][nt][1], av, y[(4 * ks + tig) * C::LD + 8 * nt + gid]);
+                    if (other || nt >= mt)  // a Gram is symmetric: its lower tiles are mirrored at the end
+                        dmma884(acc[mt][nt][0], acc[mt][nt][1], av, y[(4 * ks + tig) * C::LD + 8 * nt + gid]);
             }
         __syncwarp();
     };
@@ -174,7 +175,8 @@ __global__ void __launch_bounds__(kRgWarps * 32)
     if (part)
         for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
             const int p = e / K, q = e - p * K;
-            part[(size_t)blockIdx.x * K * K + e] = sRed[p * C::KP + q];
+            const bool mirror = !other && (p >> 3) > (q >> 3);
+            part[(size_t)blockIdx.x * K * K + e] = mirror ? sRed[q * C::KP + p] : sRed[p * C::KP + q];
         }
     if (maxpart && threadIdx.x == 0) {
         double m = 0.0;

@@ -30,7 +30,7 @@ def _newer(target, sources):
 def build_engine(force=False, verbose=False):
     os.makedirs(LIB, exist_ok=True)
     cus = sorted(glob.glob(os.path.join(CSRC, "hq_*.cu")))
-    deps = cus + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "hoqri_b200.h")]
+    deps = cus + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.inc")) + [os.path.join(ROOT, "include", "hoqri_b200.h")]
     if not force and not _newer(ENGINE, deps):
         return ENGINE
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",

@@ -15,12 +15,16 @@
 // 329-335), evaluated on the device by one thread (K x K).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 
 #include "hq_dense.cuh"
 
 namespace hq {
 
-int dense_slots() { return num_sms() * 4; }
+#ifndef HQ_RG_CTAS
+#define HQ_RG_CTAS 1
+#endif
+int dense_slots() { return num_sms() * HQ_RG_CTAS; }  // = the tall-skinny pass's grid (one CTA per SM, hq_rowgemm.cu)
 
 namespace {
 
@@ -128,7 +132,15 @@ __device__ __forceinline__ void hh_grid_sync(HhCtl* ctl, unsigned int& gen) {
             __threadfence();
             atomicExch(&ctl->bar_gen, gen + 1);
         } else {
-            while (atomicAdd(&ctl->bar_gen, 0u) == gen) __nanosleep(64);
+            const long long t0 = clock64();
+            while (atomicAdd(&ctl->bar_gen, 0u) == gen) {
+                __nanosleep(64);
+                if (clock64() - t0 > (1ll << 33)) {  // ~4 s: a lost arrival -- fail loudly instead of hanging
+                    printf("hq: householder grid barrier timeout: cta %d gen %u count %u grid %d\n", (int)blockIdx.x,
+                           gen, atomicAdd(&ctl->bar_count, 0u), (int)gridDim.x);
+                    __trap();
+                }
+            }
         }
         __threadfence();
         gen = gen + 1;

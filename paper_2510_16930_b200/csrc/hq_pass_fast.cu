@@ -230,9 +230,12 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
     double macc[C::MBW][2];
 #pragma unroll
     for (int b = 0; b < C::MBW; ++b) macc[b][0] = macc[b][1] = 0.0;
-    double wacc[C::WQ];
-#pragma unroll
-    for (int b = 0; b < C::WQ; ++b) wacc[b] = 0.0;
+    // W = A^T A on DMMA: warp w < NT (NT + 1) / 2 owns the upper block (wmA, wmB) of W; its A fragments are
+    // the M-GEMM's (same operand layout), so W costs NT (NT + 1) / 2 DMMAs per k-step and no extra loads
+    constexpr int NWB = C::NT * (C::NT + 1) / 2;
+    static_assert(NWB <= C::WARPS, "one W block per warp");
+    const int wmA = (C::NT == 1 || warp < 2) ? 0 : 1, wmB = (C::NT == 1 || warp == 0) ? 0 : 1;
+    double wfr0 = 0.0, wfr1 = 0.0;
     double mx = 0.0;
 
     const double* __restrict__ Ua = a.ua;
@@ -462,7 +465,11 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
             const int row = q / KN, r = q - row * KN;
             const double v = sA[row * C::ALD + r];
             if (row < nr && ln[row] >= 0) {
+#ifdef HQ_A_STCS
+                if (a.A) __stcs(&a.A[(r0 + row) * KN + r], v);
+#else
                 if (a.A) a.A[(r0 + row) * KN + r] = v;
+#endif
                 mx = fmax(mx, fabs(v));
             } else {
                 sA[row * C::ALD + r] = 0.0;  // long / absent rows contribute nothing
@@ -483,14 +490,11 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
                     dmma884(macc[bi][0], macc[bi][1], av, yv);
                 }
             }
+        if (warp < NWB) {
 #pragma unroll
-        for (int wi = 0; wi < C::WQ; ++wi) {
-            const int q = tid + wi * C::THREADS;
-            if (q < KN * KN) {
-                const int r1 = q / KN, r2 = q - r1 * KN;
-                double s = wacc[wi];
-                for (int row = 0; row < C::R; ++row) s = fma(sA[row * C::ALD + r1], sA[row * C::ALD + r2], s);
-                wacc[wi] = s;
+            for (int ks = 0; ks < C::R / 4; ++ks) {
+                const double* ar = sA + (size_t)(ks * 4 + (lane & 3)) * C::ALD + (lane >> 2);
+                dmma884(wfr0, wfr1, ar[wmA * 8], ar[wmB * 8]);
             }
         }
         __syncthreads();
@@ -518,10 +522,19 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
             }
         }
     }
+    if (warp < NWB) {  // C fragment: W[8 wmA + gid][8 wmB + 2 tig + {0, 1}], mirrored below the diagonal blocks
+        double* wp = a.wpart + (size_t)slot * KN * KN;
+        const int r = wmA * 8 + (lane >> 2);
+        const int c0 = wmB * 8 + 2 * (lane & 3);
+        const double v[2] = {wfr0, wfr1};
 #pragma unroll
-    for (int wi = 0; wi < C::WQ; ++wi) {
-        const int q = tid + wi * C::THREADS;
-        if (q < KN * KN) a.wpart[(size_t)slot * KN * KN + q] = wacc[wi];
+        for (int e = 0; e < 2; ++e) {
+            const int cc = c0 + e;
+            if (r < KN && cc < KN) {
+                wp[r * KN + cc] = v[e];
+                if (wmA != wmB) wp[cc * KN + r] = v[e];
+            }
+        }
     }
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
     if (lane == 0) red[warp] = mx;

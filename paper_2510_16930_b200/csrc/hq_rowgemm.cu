@@ -14,6 +14,8 @@
 // stay in registers; warps are combined in fixed order into one partial slot
 // per CTA (deterministic).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "hq_dense.cuh"
 
@@ -185,10 +187,270 @@ __global__ void __launch_bounds__(kRgWarps * 32)
     }
 }
 
+// ============================================================================
+// Bulk-copy pipelined variant (the default; one CTA per SM, grid = dense_slots()).
+//
+// The pass streams A (and `other`) once, so it is an HBM pass whose speed is
+// set by how many bytes are in flight.  A CTA owns a contiguous range of
+// 8*CW-row chunks; a producer warp moves each chunk (contiguous rows*K
+// doubles) into a kTStages-deep shared-memory ring with cp.async.bulk (TMA
+// engine, completion counted in bytes on a per-stage mbarrier), so 3-4 chunks
+// per SM are always in flight without holding registers.  CW consumer warps
+// each take one 8-row group of a chunk, with the same DMMA m8n8k4 products as
+// above (X = A T, X^T Y), write X coalesced, and release the stage.
+
+__device__ __forceinline__ uint32_t s_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mb_init(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_addr(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+    asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(s_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mb_arrive_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}" ::"r"(s_addr(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mb_try(uint64_t* b, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(s_addr(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// bounded wait: a lost arrival traps (a CUDA error the host reports) instead of hanging the device
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+    if (mb_try(b, parity)) return;
+    const long long t0 = clock64();
+    while (!mb_try(b, parity)) {
+        if (clock64() - t0 > (1ll << 33)) {
+            printf("hq: rowgemm pipeline barrier timeout: cta %d thread %d\n", (int)blockIdx.x, (int)threadIdx.x);
+            __trap();
+        }
+    }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     s_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(s_addr(b))
+                 : "memory");
+}
+__device__ __forceinline__ void cbar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+template <int K>
+struct RT {
+#ifndef HQ_RG_CTAS
+#define HQ_RG_CTAS 1
+#endif
+    static constexpr int CW = (K <= 16 && HQ_RG_CTAS == 1) ? 16 : 8;  // consumer warps (K > 16: register budget)
+    static constexpr int ROWS = 8 * CW;           // rows per chunk
+    static constexpr int NT = (K + 7) / 8;
+    static constexpr int KP = NT * 8;
+    static constexpr int KS = (K + 3) / 4;
+    static constexpr int LD = KP + 4;
+    static constexpr int CHD = ROWS * K;  // doubles per chunk per array
+    // ring of chunk buffers: S2 stages of (A, other) pairs, or 2 S2 stages of A alone -- as many bytes in
+    // flight as ~190 KB of shared memory holds (the pass is bound by bytes in flight x latency)
+    static constexpr int SB = (190 / HQ_RG_CTAS) * 1024;
+    static constexpr int S2 = SB / (2 * CHD * 8) < 8 ? SB / (2 * CHD * 8) : 8;
+    static_assert(S2 >= 2, "chunk ring");
+    static constexpr int MAXS = 2 * S2;
+    static constexpr size_t smem = (size_t)2 * S2 * CHD * 8 + (size_t)CW * 8 * LD * 8 + (size_t)KP * KP * 8 +
+                                   CW * 8 + 2 * MAXS * 8 + 64;
+};
+
+template <int K>
+__global__ void __launch_bounds__((RT<K>::CW + 1) * 32, HQ_RG_CTAS)
+    k_rowgemm_tma(const double* A, uint64_t rows, const double* __restrict__ T, double* out,
+                  const double* __restrict__ other, double* __restrict__ part, double* __restrict__ maxpart,
+                  const DevStatus* st, int run_if) {
+    using C = RT<K>;
+    constexpr int kTcW = C::CW, kTRows = C::ROWS;
+    if (skip_kernel(st, run_if)) return;
+    extern __shared__ __align__(128) double rsm[];
+    const int NS = other ? C::S2 : C::MAXS;                   // stages
+    double* sA = rsm;                                         // NS x CHD
+    double* sO = sA + (size_t)NS * C::CHD;                    // NS x CHD (other)
+    double* sXall = rsm + (size_t)2 * C::S2 * C::CHD;         // kTcW x 8 x LD
+    double* sRed = sXall + (size_t)kTcW * 8 * C::LD;          // KP x KP
+    double* sMax = sRed + C::KP * C::KP;                      // kTcW
+    uint64_t* full = reinterpret_cast<uint64_t*>(sMax + kTcW);
+    uint64_t* empty = full + C::MAXS;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gid = lane >> 2, tig = lane & 3;
+
+    const uint64_t nch = (rows + kTRows - 1) / kTRows;
+    const uint64_t cb = nch * blockIdx.x / gridDim.x, ce = nch * (blockIdx.x + 1) / gridDim.x;
+    const int my = (int)(ce - cb);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mb_init(&full[s], 1);
+            mb_init(&empty[s], kTcW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == kTcW) {  // ---------------- producer
+        if (lane == 0) {
+            for (int j = 0; j < my; ++j) {
+                const int s = j % NS;
+                if (j >= NS) mb_wait(&empty[s], ((j / NS) - 1) & 1);
+                const uint64_t r0 = (cb + j) * kTRows;
+                const uint64_t nr = min((uint64_t)kTRows, rows - r0);
+                const uint32_t n = (uint32_t)(nr * K);  // doubles
+                const uint32_t n2 = n & ~1u;            // bulk copies move whole 16-byte units
+                if (n2 != n) {                          // odd tail: the last double by hand, before the arrive
+                    sA[(size_t)s * C::CHD + n - 1] = A[r0 * K + n - 1];
+                    if (other) sO[(size_t)s * C::CHD + n - 1] = other[r0 * K + n - 1];
+                }
+                mb_arrive_tx(&full[s], n2 * 8 * (other ? 2 : 1));
+                if (n2) {
+                    bulk_g2s(sA + (size_t)s * C::CHD, A + r0 * K, n2 * 8, &full[s]);
+                    if (other) bulk_g2s(sO + (size_t)s * C::CHD, other + r0 * K, n2 * 8, &full[s]);
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers: warp w owns rows [8w, 8w + 8) of every chunk
+    double tf[C::KS][C::NT];
+#pragma unroll
+    for (int ks = 0; ks < C::KS; ++ks)
+#pragma unroll
+        for (int nt = 0; nt < C::NT; ++nt) {
+            const int k = 4 * ks + tig, n = 8 * nt + gid;
+            double v = 0.0;
+            if (k < K && n < K) v = T ? T[k * K + n] : (k == n ? 1.0 : 0.0);
+            tf[ks][nt] = v;
+        }
+    double acc[C::NT][C::NT][2];
+#pragma unroll
+    for (int i = 0; i < C::NT; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    double* sx = sXall + (size_t)warp * 8 * C::LD;
+    for (int q = lane; q < 8 * C::LD; q += 32) sx[q] = 0.0;
+    __syncwarp();
+    double mx = 0.0;
+    const int grow = 8 * warp + gid;  // this lane's row within a chunk (A fragments)
+
+    for (int j = 0; j < my; ++j) {
+        const int s = j % NS;
+        const uint64_t r0 = (cb + j) * kTRows;
+        const int nr = (int)min((uint64_t)kTRows, rows - r0);
+        mb_wait(&full[s], (j / NS) & 1);
+        const double* ca = sA + (size_t)s * C::CHD;
+        const double* co = sO + (size_t)s * C::CHD;
+        double a[C::KS];
+#pragma unroll
+        for (int ks = 0; ks < C::KS; ++ks) {
+            const int col = 4 * ks + tig;
+            a[ks] = (grow < nr && col < K) ? ca[grow * K + col] : 0.0;
+            mx = fmax(mx, fabs(a[ks]));
+        }
+        // X = A T (C fragment: row gid, cols 8nt + 2 tig + {0,1}) -> sx
+#pragma unroll
+        for (int nt = 0; nt < C::NT; ++nt) {
+            double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < C::KS; ++ks) dmma884(c0, c1, a[ks], tf[ks][nt]);
+            const int col = 8 * nt + 2 * tig;
+            sx[gid * C::LD + col] = c0;
+            sx[gid * C::LD + col + 1] = c1;
+        }
+        __syncwarp();
+        const int gr0 = 8 * warp;
+        if (out) {
+            const int lim = max(0, min(8, nr - gr0)) * K;
+            double* og = out + (r0 + gr0) * K;
+            for (int q = lane; q < lim; q += 32) {
+                const int r = q / K, cc = q - r * K;
+                og[q] = sx[r * C::LD + cc];
+            }
+        }
+        // X^T Y: k = the group's rows.  Rows past the chunk end are zero in sx (A fragments were zeroed).
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+            const int rr = 4 * ks + tig;  // row within the group
+#pragma unroll
+            for (int mt = 0; mt < C::NT; ++mt) {
+                const double av = sx[rr * C::LD + 8 * mt + gid];
+#pragma unroll
+                for (int nt = 0; nt < C::NT; ++nt) {
+                    if (other) {
+                        const int col = 8 * nt + gid;
+                        const double yv = (gr0 + rr < nr && col < K) ? co[(gr0 + rr) * K + col] : 0.0;
+                        dmma884(acc[mt][nt][0], acc[mt][nt][1], av, yv);
+                    } else if (nt >= mt) {  // a Gram is symmetric: its lower tiles are mirrored at the end
+                        dmma884(acc[mt][nt][0], acc[mt][nt][1], av, sx[rr * C::LD + 8 * nt + gid]);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mb_arrive(&empty[s]);
+    }
+
+    // fixed-order combination of the consumer warps' fragments
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+    if (lane == 0) sMax[warp] = mx;
+    constexpr int CT = kTcW * 32;
+    for (int ww = 0; ww < kTcW; ++ww) {
+        if (warp == ww) {
+#pragma unroll
+            for (int mt = 0; mt < C::NT; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < C::NT; ++nt) {
+                    const int p = 8 * mt + gid, q = 8 * nt + 2 * tig;
+                    double* d = sRed + p * C::KP + q;
+                    d[0] = (ww == 0 ? 0.0 : d[0]) + acc[mt][nt][0];
+                    d[1] = (ww == 0 ? 0.0 : d[1]) + acc[mt][nt][1];
+                }
+        }
+        cbar(1, CT);
+    }
+    if (part)
+        for (int e = threadIdx.x; e < K * K; e += CT) {
+            const int p = e / K, q = e - p * K;
+            const bool mirror = !other && (p >> 3) > (q >> 3);
+            part[(size_t)blockIdx.x * K * K + e] = mirror ? sRed[q * C::KP + p] : sRed[p * C::KP + q];
+        }
+    if (maxpart && threadIdx.x == 0) {
+        double m = 0.0;
+        for (int ww = 0; ww < kTcW; ++ww) m = fmax(m, sMax[ww]);
+        maxpart[blockIdx.x] = m;
+    }
+}
+
 template <int K>
 void launch_rg(const double* A, uint64_t rows, const double* T, double* out, const double* other, double* part,
                double* maxpart, const DevStatus* st, int run_if, cudaStream_t s) {
-    k_rowgemm<K><<<dense_slots(), kRgWarps * 32, 0, s>>>(A, rows, T, out, other, part, maxpart, st, run_if);  // dense_slots() = 4 CTAs/SM
+    // bulk copies need 16-byte aligned sources (a row-range slice of A in the multi-GPU path may start
+    // mid-unit): those take the register-staged kernel
+    static const bool force_ld = [] {
+        const char* e = std::getenv("HQ_RG_LD");
+        return e && e[0] == '1';
+    }();
+    const bool aligned = !force_ld && (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
+                         (!other || reinterpret_cast<uintptr_t>(other) % 16 == 0);
+    if (aligned) {
+        using C = RT<K>;
+        static bool attr = false;
+        if (!attr) {
+            HQ_CUDA(cudaFuncSetAttribute(k_rowgemm_tma<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem));
+            attr = true;
+        }
+        k_rowgemm_tma<K><<<dense_slots(), (C::CW + 1) * 32, C::smem, s>>>(A, rows, T, out, other, part, maxpart, st,
+                                                                        run_if);
+    } else {
+        k_rowgemm<K><<<dense_slots(), kRgWarps * 32, 0, s>>>(A, rows, T, out, other, part, maxpart, st, run_if);
+    }
     HQ_CHECK_LAUNCH();
 }
 

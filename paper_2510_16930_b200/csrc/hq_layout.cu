@@ -390,8 +390,10 @@ void build_tensor(DeviceTensor& T, int order, const uint64_t* dims, uint64_t nnz
         int j = 0;
         for (int v = 0; v < order; ++v)
             if (v != m) L.others[j++] = v;
-        L.val.alloc(n);
-        for (int q = 0; q < order - 1; ++q) L.idx[q].alloc(n);
+        // 16 bytes of tail padding: the pass stages a tile's contiguous stream slice with 16-byte copies from its
+        // aligned base, which may read up to one 16-byte unit past the last nonzero
+        L.val.alloc(n + 2);
+        for (int q = 0; q < order - 1; ++q) L.idx[q].alloc(n + 4);
         DBuf<uint32_t> key, skey;
         key.alloc(n);
         if (n) k_extract_mode<<<grid_for(n), 256, 0, s>>>(T.coords.get(), n, order, m, key.get());

@@ -174,7 +174,11 @@ struct Cfg {
     static_assert(R % 8 == 0, "m-tiles of 8 rows");
     // shared memory: gather buffer, Y tile, two record buffers, A tile, three row-meta slots
     static constexpr size_t META = (size_t)R * (8 + 4 + 4 + 4) + 16;  // start, len, off, perm, total
-    static constexpr size_t smem_bytes = (size_t)CAP * FW * 8 + (size_t)R * LDY * 8 + 2 * (size_t)CAP * sizeof(Rec) +
+    // a record buffer: x[CAP + 2] (f64), j[CAP + 4], k[CAP + 4] (u32) -- SoA, so a tile whose records are one
+    // contiguous stream slice is staged with 16-byte copies at the slice's 16-byte-aligned base
+    static constexpr size_t RECB = (size_t)(CAP + 2) * 8 + 2 * (size_t)(CAP + 4) * 4;
+    static_assert(RECB % 16 == 0, "record buffer alignment");
+    static constexpr size_t smem_bytes = (size_t)CAP * FW * 8 + (size_t)R * LDY * 8 + 2 * RECB +
                                          (size_t)R * ALD * 8 + 3 * META + 64;
 };
 
@@ -189,8 +193,11 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
     extern __shared__ __align__(16) double sm[];
     double* sF = sm;                                          // CAP x FW gathered factor rows
     double* sY = sF + (size_t)C::CAP * C::FW;                 // R x LDY Kronecker rows
-    Rec* sRecB = reinterpret_cast<Rec*>(sY + (size_t)C::R * C::LDY);  // 2 x CAP records
-    double* sA = reinterpret_cast<double*>(sRecB + 2 * C::CAP);       // R x ALD a_i rows
+    char* sRecB = reinterpret_cast<char*>(sY + (size_t)C::R * C::LDY);  // 2 record buffers (SoA)
+    double* sA = reinterpret_cast<double*>(sRecB + 2 * C::RECB);       // R x ALD a_i rows
+    auto rx = [&](int rb) { return reinterpret_cast<double*>(sRecB + rb * C::RECB); };
+    auto rj = [&](int rb) { return reinterpret_cast<uint32_t*>(sRecB + rb * C::RECB + (C::CAP + 2) * 8); };
+    auto rk = [&](int rb) { return rj(rb) + C::CAP + 4; };
     char* sMetaB = reinterpret_cast<char*>(sA + (size_t)C::R * C::ALD);
     // row meta of a tile: start position, length (-1: long row), virtual offset, lane slot -> row, total
     auto m_start = [&](int mb) { return reinterpret_cast<int64_t*>(sMetaB + mb * C::META); };
@@ -273,7 +280,7 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
             m_len(mb)[tid] = len;
             m_start(mb)[tid] = st_lo;
         }
-        __syncthreads();
+        const int any_long = __syncthreads_or(tid < C::R && tid < nr && st_hi - st_lo > kShortMax);
         if (tid < C::R) {
             const int* ln = m_len(mb);
             const int me = max(ln[tid], 0);
@@ -285,7 +292,11 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
             }
             m_perm(mb)[rank] = tid;
             m_off(mb)[tid] = off;
-            if (tid == C::R - 1) m_tot(mb)[0] = off + me;
+            if (tid == C::R - 1) {
+                m_tot(mb)[0] = off + me;
+                // contiguous: the tile's records are the stream slice [start of row 0, + total)
+                m_tot(mb)[1] = !any_long && off + me <= C::CAP;
+            }
         }
         __syncthreads();
     };
@@ -301,26 +312,39 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
     };
     // records of virtual positions [cv, cv + CAP) of tile (meta mb) -> record buffer rb (per row lanes)
     auto records_issue = [&](int mb, int rb, int cv) {
-        const int lr = m_perm(mb)[rslot];
-        const int len = max(m_len(mb)[lr], 0);
-        const int voff = m_off(mb)[lr];
-        const int64_t pbase = m_start(mb)[lr] - voff;
-        Rec* rec = sRecB + rb * C::CAP;
-        const int lo = max(voff, cv), hi = min(voff + len, cv + C::CAP);
-        for (int v = lo + sub; v < hi; v += C::TR) {
-            const int64_t pz = pbase + v;
-            cp8(&rec[v - cv].x, a.val + pz, pol_stream);
-            cp4(&rec[v - cv].j, a.ia + pz, pol_stream);
-            cp4(&rec[v - cv].k, a.ib + pz, pol_stream);
+        if (cv == 0 && m_tot(mb)[1]) {  // one contiguous slice: 16-byte copies from its aligned base
+            const int64_t p0 = m_start(mb)[0];
+            const int tot = m_tot(mb)[0];
+            const int64_t bx = p0 & ~(int64_t)1, bj = p0 & ~(int64_t)3;
+            const int nx = (int)((p0 + tot - bx + 1) >> 1), nj = (int)((p0 + tot - bj + 3) >> 2);
+            for (int q = tid; q < nx; q += C::THREADS) cp16(rx(rb) + 2 * q, a.val + bx + 2 * q, pol_stream);
+            for (int q = tid; q < nj; q += C::THREADS) {
+                cp16(rj(rb) + 4 * q, a.ia + bj + 4 * q, pol_stream);
+                cp16(rk(rb) + 4 * q, a.ib + bj + 4 * q, pol_stream);
+            }
+        } else {
+            const int lr = m_perm(mb)[rslot];
+            const int len = max(m_len(mb)[lr], 0);
+            const int voff = m_off(mb)[lr];
+            const int64_t pbase = m_start(mb)[lr] - voff;
+            const int lo = max(voff, cv), hi = min(voff + len, cv + C::CAP);
+            for (int v = lo + sub; v < hi; v += C::TR) {
+                const int64_t pz = pbase + v;
+                cp8(rx(rb) + (v - cv), a.val + pz, pol_stream);
+                cp4(rj(rb) + (v - cv), a.ia + pz, pol_stream);
+                cp4(rk(rb) + (v - cv), a.ib + pz, pol_stream);
+            }
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
+    // element offsets of record 0 in a record buffer (non-zero only for a contiguous slice)
+    auto rec_ox = [&](int mb, int cv) { return (cv == 0 && m_tot(mb)[1]) ? (int)(m_start(mb)[0] & 1) : 0; };
+    auto rec_oj = [&](int mb, int cv) { return (cv == 0 && m_tot(mb)[1]) ? (int)(m_start(mb)[0] & 3) : 0; };
     // both factor rows of records [0, cn) -> sF with cp.async, piece-major: consecutive lanes copy
     // consecutive 16-byte pieces of one record's rows.  (Register-staged LDG.128 needs ~100 registers per
     // thread for a whole tile: measured, spills; record-per-thread issue measured 15% slower.)
     constexpr int PA = KA / 2, PP = (KA + KB) / 2;
-    auto gathers_issue = [&](int rb, int cn) {
-        const Rec* rec = sRecB + rb * C::CAP;
+    auto gathers_issue = [&](int rb, int cn, int oj) {
         // each of the first (THREADS / PP) * PP threads owns one fixed piece slot of every record it copies:
         // no per-piece slot arithmetic, one record index load per piece
         constexpr int RPI = C::THREADS / PP;  // records per iteration
@@ -331,10 +355,9 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
             const int kk = isa ? KA : KB;
             const int off = isa ? 2 * pc : KA + 2 * (pc - PA);
             const uint64_t pol = isa ? pol_a : pol_b;
-            const uint32_t* idxp = isa ? &rec[0].j : &rec[0].k;
-            constexpr int RS = sizeof(Rec) / sizeof(uint32_t);
+            const uint32_t* idxp = (isa ? rj(rb) : rk(rb)) + oj;
             for (int e = tid / PP; e < cn; e += RPI)
-                cp16(sF + (size_t)e * C::FW + off, base + (size_t)idxp[e * RS] * kk, pol);
+                cp16(sF + (size_t)e * C::FW + off, base + (size_t)idxp[e] * kk, pol);
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
@@ -347,7 +370,7 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
         records_issue(0, 0, 0);
         cp_wait_all();
         __syncthreads();
-        gathers_issue(0, min(C::CAP, m_tot(0)[0]));
+        gathers_issue(0, min(C::CAP, m_tot(0)[0]), rec_oj(0, 0));
         if (t0 + 1 < t1) {
             load_starts(t0 + 1, lo, hi);
             meta_from(t0 + 1, 1, lo, hi);
@@ -368,7 +391,7 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
         const int lr = m_perm(mb)[rslot];
         const int len = max(m_len(mb)[lr], 0);
         const int voff = m_off(mb)[lr];
-        const Rec* rec = sRecB + rb * C::CAP;
+        const double* recx = rx(rb) + rec_ox(mb, 0);
 
         double acc[C::BP][C::BQ];
 #pragma unroll
@@ -378,7 +401,7 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
         auto kron = [&](int e0, int e1) {
 #pragma unroll 2
             for (int e = e0; e < e1; ++e) {
-                const double x = rec[e].x;
+                const double x = recx[e];
                 const double* f = sF + (size_t)e * C::FW;
                 double sa[C::BP], vb[C::BQ];
                 lds_block<C::BP>(f, p0, sa);
@@ -397,7 +420,7 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
             records_issue(mb, rb, cv);
             cp_wait_all();
             __syncthreads();
-            gathers_issue(rb, min(C::CAP, total - cv));
+            gathers_issue(rb, min(C::CAP, total - cv), 0);
             cp_wait_all();
             __syncthreads();
             kron(max(voff, cv) - cv, min(voff + len, cv + C::CAP) - cv);
@@ -415,7 +438,7 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
         }
         __syncthreads();  // sF and this tile's record buffer are free
         HQ_PHASE(2);
-        if (t + 1 < t1) gathers_issue(rb ^ 1, min(C::CAP, m_tot((mb + 1) % 3)[0]));
+        if (t + 1 < t1) gathers_issue(rb ^ 1, min(C::CAP, m_tot((mb + 1) % 3)[0]), rec_oj((mb + 1) % 3, 0));
         HQ_PHASE(3);
         const int* ln = m_len(mb);
         if (a.kind == kTTMcTC) {
@@ -442,6 +465,8 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
                         dmma884(c[bi][ks & 1][0], c[bi][ks & 1][1], yv, gv);
                     }
                 }
+            // epilogue straight from the fragments: long / absent rows zeroed, A written (16-byte stores),
+            // max|A|, and the A tile for the M / W products
 #pragma unroll
             for (int bi = 0; bi < C::ABW; ++bi) {
                 const int b = warp + bi * C::WARPS;
@@ -449,18 +474,34 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
                     const int mt = b / C::NT;
                     const int row = mt * 8 + (lane >> 2);
                     const int col = nt * 8 + 2 * (lane & 3);
-                    sA[row * C::ALD + col] = c[bi][0][0] + c[bi][1][0];
-                    sA[row * C::ALD + col + 1] = c[bi][0][1] + c[bi][1][1];
+                    const bool valid = row < nr && ln[row] >= 0;
+                    const double v0 = valid ? c[bi][0][0] + c[bi][1][0] : 0.0;
+                    const double v1 = valid ? c[bi][0][1] + c[bi][1][1] : 0.0;
+                    sA[row * C::ALD + col] = v0;
+                    sA[row * C::ALD + col + 1] = v1;
+                    mx = fmax(mx, fmax(fabs(v0), fabs(v1)));  // padding columns are exactly 0
+                    if (valid && a.A && col < KN) {
+                        double* dst = a.A + (r0 + row) * KN + col;
+                        if constexpr (KN % 2 == 0)
+                            *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+                        else {
+                            dst[0] = v0;
+                            if (col + 1 < KN) dst[1] = v1;
+                        }
+                    }
                 }
             }
+            __syncthreads();
+            HQ_PHASE(4);
         } else {
             for (int q = tid; q < C::R * KN; q += C::THREADS) {
                 const int row = q / KN, r = q - row * KN;
                 sA[row * C::ALD + r] = (row < nr && ln[row] >= 0) ? a.un[(r0 + row) * KN + r] : 0.0;
             }
+            __syncthreads();
+            HQ_PHASE(4);
         }
-        __syncthreads();
-        HQ_PHASE(4);
+        if (a.kind != kTTMcTC) {
         for (int q = tid; q < C::R * KN; q += C::THREADS) {
             const int row = q / KN, r = q - row * KN;
             const double v = sA[row * C::ALD + r];
@@ -476,6 +517,7 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
             }
         }
         __syncthreads();
+        }
         HQ_PHASE(5);
         // M += A_tile^T Y_tile (DMMA), W += A^T A (DFMA)
 #pragma unroll

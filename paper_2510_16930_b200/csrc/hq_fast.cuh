@@ -28,6 +28,7 @@ struct FastArgs {
     // the launch when l2_bytes > 0 (cudaLaunchAttributeAccessPolicyWindow)
     size_t l2_bytes;
     float l2_hit;
+    int l1_a, l1_b;       // L1-allocating gathers for a hot (skewed) factor (ModeLayout::hot)
 };
 
 // Sets the device's persisting-L2 carve-out to its maximum once and returns

@@ -119,6 +119,10 @@ struct ModeLayout {
     DBuf<uint32_t> idx[kMaxOrder - 1];  // nnz each: index of the j-th other mode (ascending v != n)
     int others[kMaxOrder - 1] = {0};
     uint64_t nonempty_rows = 0;        // R_n
+    // skewed: rows longer than 32x the mean hold >= 5% of the nonzeros.  Row i of this mode's unfolding is
+    // how often U_n[i] is gathered by the other modes' passes, so a skewed mode's factor has hot rows that
+    // pile onto single L2 slices: its gathers are made L1-allocating (cp.async.ca) to absorb the repeats.
+    bool hot = false;
     // work plan (see hq_pass.cu)
     uint64_t long_rows = 0;
     DBuf<uint32_t> long_row_ids;       // rows with more than kShortMax nonzeros

@@ -33,6 +33,10 @@ __device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cv
 __device__ __forceinline__ void cpa16(void* d, const void* s) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr(d)), "l"(s));
 }
+// L1-allocating variant for the rows of a hot factor (repeats served by L1, not one L2 slice)
+__device__ __forceinline__ void cpa16_l1(void* d, const void* s) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(saddr(d)), "l"(s));
+}
 __device__ __forceinline__ void cpa8(void* d, const void* s) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(saddr(d)), "l"(s));
 }
@@ -132,8 +136,12 @@ __device__ __forceinline__ void kstep(const double* f, int ks, int n, int gid, i
 // consecutive lanes copy one row; full chunks run a fixed-trip loop.
 template <int KM, int OFF, class S>
 __device__ __forceinline__ void gather_mode(const double* __restrict__ u, const uint32_t* r, double* dst, int n,
-                                            int tid) {
+                                            int tid, int l1) {
     constexpr int PM = KM / 2;
+    auto cp = [&](void* d, const void* src) {
+        if (l1) cpa16_l1(d, src);
+        else cpa16(d, src);
+    };
     if (n == S::CH) {
         constexpr int TOT = S::CH * PM, IT = (TOT + S::THREADS - 1) / S::THREADS;
 #pragma unroll
@@ -141,13 +149,13 @@ __device__ __forceinline__ void gather_mode(const double* __restrict__ u, const 
             const int q = tid + it * S::THREADS;
             if (TOT % S::THREADS == 0 || q < TOT) {
                 const int e = q / PM, p = q - e * PM;
-                cpa16(dst + (size_t)e * S::FW + OFF + 2 * p, u + (size_t)r[e] * KM + 2 * p);
+                cp(dst + (size_t)e * S::FW + OFF + 2 * p, u + (size_t)r[e] * KM + 2 * p);
             }
         }
     } else {
         for (int q = tid; q < n * PM; q += S::THREADS) {
             const int e = q / PM, p = q - e * PM;
-            cpa16(dst + (size_t)e * S::FW + OFF + 2 * p, u + (size_t)r[e] * KM + 2 * p);
+            cp(dst + (size_t)e * S::FW + OFF + 2 * p, u + (size_t)r[e] * KM + 2 * p);
         }
     }
 }
@@ -195,9 +203,9 @@ __global__ void __launch_bounds__(256) k_longseg_mma(LongArgs a) {
             const int n = cg.n(S::CH);
             const uint32_t* r = rec + (size_t)rslot * S::rec_words;
             double* dst = rowbuf + (size_t)bslot * S::row_doubles;
-            gather_mode<K0, 0, S>(a.u0, r, dst, n, tid);
-            gather_mode<K1, K0, S>(a.u1, r + S::CH, dst, n, tid);
-            if constexpr (K2 != 0) gather_mode<K2, K0 + K1, S>(a.u2, r + 2 * S::CH, dst, n, tid);
+            gather_mode<K0, 0, S>(a.u0, r, dst, n, tid, a.l1_0);
+            gather_mode<K1, K0, S>(a.u1, r + S::CH, dst, n, tid, a.l1_1);
+            if constexpr (K2 != 0) gather_mode<K2, K0 + K1, S>(a.u2, r + 2 * S::CH, dst, n, tid, a.l1_2);
             if (tid < n) cpa8(dst + (size_t)tid * S::FW + S::RW, a.val + cg.z0 + tid);
             cg.advance(a, rend, S::CH);
         }

@@ -31,6 +31,7 @@ struct LongArgs {
     int slot0;
     const DevStatus* st;
     int run_if;
+    int l1_0, l1_1, l1_2;            // L1-allocating gathers for hot (skewed) factors (ModeLayout::hot)
 };
 
 bool long_fast_supported(const ModeShape& sh);

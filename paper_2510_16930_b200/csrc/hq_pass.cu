@@ -46,12 +46,13 @@ ModeShape make_mode_shape(int order, const int* ranks, int n) {
 namespace {
 
 __global__ void k_long_flags(const int64_t* __restrict__ rowptr, uint64_t rows, uint32_t* __restrict__ flag,
-                             uint32_t* __restrict__ nseg) {
+                             uint32_t* __restrict__ nseg, int64_t hot_len, unsigned long long* __restrict__ hot_nnz) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < rows; i += (uint64_t)gridDim.x * blockDim.x) {
         int64_t len = rowptr[i + 1] - rowptr[i];
         bool lng = len > kShortMax;
         flag[i] = lng;
         nseg[i] = lng ? (uint32_t)((len + kSegLen - 1) / kSegLen) : 0u;
+        if (len > hot_len) atomicAdd(hot_nnz, (unsigned long long)len);  // integer: order-independent
     }
 }
 
@@ -96,15 +97,20 @@ inline int grid_for(uint64_t n, int threads = 256) {
 }  // namespace
 
 void plan_mode(ModeLayout& L, uint64_t nnz, cudaStream_t s) {
-    (void)nnz;
     const uint64_t rows = L.rows;
     DBuf<uint32_t> flag, nseg, pos, segpos;
+    DBuf<unsigned long long> hot;
     flag.alloc(rows);
     nseg.alloc(rows);
     pos.alloc(rows);
     segpos.alloc(rows);
-    k_long_flags<<<grid_for(rows), 256, 0, s>>>(L.rowptr.get(), rows, flag.get(), nseg.get());
+    hot.alloc(1);
+    HQ_CUDA(cudaMemsetAsync(hot.get(), 0, sizeof(unsigned long long), s));
+    const int64_t hot_len = std::max<int64_t>(64, (int64_t)(32 * (nnz / std::max<uint64_t>(rows, 1))));
+    k_long_flags<<<grid_for(rows), 256, 0, s>>>(L.rowptr.get(), rows, flag.get(), nseg.get(), hot_len, hot.get());
     HQ_CHECK_LAUNCH();
+    unsigned long long hot_nnz = 0;
+    HQ_CUDA(cudaMemcpyAsync(&hot_nnz, hot.get(), sizeof(hot_nnz), cudaMemcpyDeviceToHost, s));
     exclusive_scan(flag.get(), pos.get(), rows, s);
     exclusive_scan(nseg.get(), segpos.get(), rows, s);
     uint32_t lp = 0, lf = 0, sp = 0, sn = 0;
@@ -113,6 +119,7 @@ void plan_mode(ModeLayout& L, uint64_t nnz, cudaStream_t s) {
     HQ_CUDA(cudaMemcpyAsync(&sp, segpos.get() + rows - 1, 4, cudaMemcpyDeviceToHost, s));
     HQ_CUDA(cudaMemcpyAsync(&sn, nseg.get() + rows - 1, 4, cudaMemcpyDeviceToHost, s));
     HQ_CUDA(cudaStreamSynchronize(s));
+    L.hot = nnz > 0 && (double)hot_nnz >= 0.05 * (double)nnz;
     L.long_rows = (uint64_t)lp + lf;
     L.long_segments = (uint64_t)sp + sn;
     if (L.long_rows) {
@@ -444,6 +451,8 @@ void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const Fac
         const size_t budget = l2_window_enabled() ? l2_persist_budget() : 0;
         fa.l2_bytes = budget ? fbytes : 0;
         fa.l2_hit = budget ? (float)std::min(1.0, (double)budget / (double)fbytes) : 0.f;
+        fa.l1_a = T.modes[L.others[0]].hot;
+        fa.l1_b = T.modes[L.others[1]].hot;
         launch_fast(fa, sh, tile_grid(sh), s);
     } else {
         size_t smem = sizeof(double) * ((size_t)a.R * sh.L + (size_t)a.R * sh.kn);
@@ -463,6 +472,9 @@ void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const Fac
         la.u0 = a.uo[0];
         la.u1 = a.uo[1];
         la.u2 = sh.nothers > 2 ? a.uo[2] : nullptr;
+        la.l1_0 = T.modes[L.others[0]].hot;
+        la.l1_1 = T.modes[L.others[1]].hot;
+        la.l1_2 = sh.nothers > 2 && T.modes[L.others[2]].hot;
         la.un = a.un;
         la.gt = gt;
         la.long_ids = a.long_ids;

@@ -97,6 +97,11 @@ __device__ __forceinline__ void cp16(void* dst, const void* src, uint64_t pol) {
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
                  "l"(pol));
 }
+// L1-allocating variant for the rows of a hot (skewed) factor: repeats are served by L1 instead of one L2 slice
+__device__ __forceinline__ void cp16_l1(void* dst, const void* src, uint64_t pol) {
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
+                 "l"(pol));
+}
 __device__ __forceinline__ void cp8(void* dst, const void* src, uint64_t pol) {
     asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(smem_addr(dst)), "l"(src),
                  "l"(pol));
@@ -356,8 +361,13 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
             const int off = isa ? 2 * pc : KA + 2 * (pc - PA);
             const uint64_t pol = isa ? pol_a : pol_b;
             const uint32_t* idxp = (isa ? rj(rb) : rk(rb)) + oj;
-            for (int e = tid / PP; e < cn; e += RPI)
-                cp16(sF + (size_t)e * C::FW + off, base + (size_t)idxp[e] * kk, pol);
+            if (isa ? a.l1_a : a.l1_b) {
+                for (int e = tid / PP; e < cn; e += RPI)
+                    cp16_l1(sF + (size_t)e * C::FW + off, base + (size_t)idxp[e] * kk, pol);
+            } else {
+                for (int e = tid / PP; e < cn; e += RPI)
+                    cp16(sF + (size_t)e * C::FW + off, base + (size_t)idxp[e] * kk, pol);
+            }
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };

@@ -11,7 +11,10 @@ namespace hq {
 // partial Kronecker row, and the partials of a row are summed in segment
 // order (deterministic).  All other rows are processed whole by the tile
 // kernels.
-constexpr int64_t kShortMax = 256;
+#ifndef HQ_SHORT_MAX
+#define HQ_SHORT_MAX 256
+#endif
+constexpr int64_t kShortMax = HQ_SHORT_MAX;
 constexpr int64_t kSegLen = 4096;
 
 void plan_mode(ModeLayout& L, uint64_t nnz, cudaStream_t s);

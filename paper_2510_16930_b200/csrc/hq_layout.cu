@@ -35,8 +35,9 @@ __global__ void k_validate(const uint32_t* __restrict__ coords, const double* __
                            unsigned long long* first_bad) {
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz;
          e += (uint64_t)gridDim.x * blockDim.x) {
-        bool bad = !isfinite(vals[e]);
-        for (int m = 0; m < order; ++m) bad |= (uint64_t)coords[e * order + m] >= dims[m];
+        bool bad = vals && !isfinite(vals[e]);  // vals == nullptr: coordinates only
+        if (coords)
+            for (int m = 0; m < order; ++m) bad |= (uint64_t)coords[e * order + m] >= dims[m];
         if (bad) atomicMin(first_bad, (unsigned long long)e);
     }
 }
@@ -269,7 +270,7 @@ double device_sum_sq(const double* v, uint64_t n, cudaStream_t s) {
 }
 
 void build_tensor(DeviceTensor& T, int order, const uint64_t* dims, uint64_t nnz, const uint32_t* coords_in,
-                  const double* vals_in, cudaStream_t s) {
+                  const double* vals_in, cudaStream_t s, cudaEvent_t vals_ready) {
     if (order <= 0) fail(HQ_ERR_SHAPE, "sparse tensor needs at least one mode");
     if (order > kMaxOrder) fail(HQ_ERR_SHAPE, "tensor order above the engine limit of 8");
     for (int m = 0; m < order; ++m)
@@ -280,16 +281,13 @@ void build_tensor(DeviceTensor& T, int order, const uint64_t* dims, uint64_t nnz
     for (int m = 0; m < order; ++m) T.dims[m] = dims[m];
     PhaseClock clk(s);
 
-    // ---- validation (sparse_tensor.cpp:29-38)
-    if (nnz) {
-        DBuf<uint64_t> ddims;
-        ddims.alloc(order);
-        HQ_CUDA(cudaMemcpyAsync(ddims.get(), dims, sizeof(uint64_t) * order, cudaMemcpyHostToDevice, s));
-        DBuf<unsigned long long> bad;
-        bad.alloc(1);
-        HQ_CUDA(cudaMemsetAsync(bad.get(), 0xff, sizeof(unsigned long long), s));
-        k_validate<<<grid_for(nnz), 256, 0, s>>>(coords_in, vals_in, nnz, order, ddims.get(), bad.get());
-        HQ_CHECK_LAUNCH();
+    // ---- validation (sparse_tensor.cpp:29-38): the first bad entry in entry order decides the error (its
+    // coordinates are checked before its value).  With vals_ready the coordinate check runs now and the value
+    // check after the lexicographic sort (the values' upload overlaps the sort); the sort never indexes
+    // memory by coordinate, so a bad coordinate is harmless until the check below.
+    DBuf<uint64_t> ddims;
+    DBuf<unsigned long long> bad;
+    auto check_entries = [&]() {
         unsigned long long hb = 0;
         HQ_CUDA(cudaMemcpyAsync(&hb, bad.get(), sizeof(hb), cudaMemcpyDeviceToHost, s));
         HQ_CUDA(cudaStreamSynchronize(s));
@@ -304,6 +302,16 @@ void build_tensor(DeviceTensor& T, int order, const uint64_t* dims, uint64_t nnz
                                            std::to_string(m + 1) + " (extent " + std::to_string(dims[m]) + ")");
             fail(HQ_ERR_VALUE, "non-finite value at entry " + std::to_string(hb));
         }
+    };
+    if (nnz) {
+        ddims.alloc(order);
+        HQ_CUDA(cudaMemcpyAsync(ddims.get(), dims, sizeof(uint64_t) * order, cudaMemcpyHostToDevice, s));
+        bad.alloc(1);
+        HQ_CUDA(cudaMemsetAsync(bad.get(), 0xff, sizeof(unsigned long long), s));
+        k_validate<<<grid_for(nnz), 256, 0, s>>>(coords_in, vals_ready ? nullptr : vals_in, nnz, order, ddims.get(),
+                                                 bad.get());
+        HQ_CHECK_LAUNCH();
+        if (!vals_ready) check_entries();
     }
     clk.mark("validate");
 
@@ -344,6 +352,12 @@ void build_tensor(DeviceTensor& T, int order, const uint64_t* dims, uint64_t nnz
             std::swap(p0, p1);
         }
         perm = std::move(p0);
+        if (vals_ready) {  // the values have landed: their check, then the first bad entry (if any) is reported
+            HQ_CUDA(cudaStreamWaitEvent(s, vals_ready, 0));
+            k_validate<<<grid_for(nnz), 256, 0, s>>>(nullptr, vals_in, nnz, order, ddims.get(), bad.get());
+            HQ_CHECK_LAUNCH();
+            check_entries();
+        }
         clk.mark("lexsort");
 
         // ---- run heads and merge (sparse_tensor.cpp:54-70)

@@ -20,8 +20,10 @@ constexpr int64_t kSegLen = 4096;
 void plan_mode(ModeLayout& L, uint64_t nnz, cudaStream_t s);
 
 double device_sum_sq(const double* v, uint64_t n, cudaStream_t s);
+// vals_ready (optional): the values are still arriving (an H2D copy on another stream that records this
+// event); the coordinate-only work (range checks, key packing, lexicographic sort) runs before s waits on it
 void build_tensor(DeviceTensor& T, int order, const uint64_t* dims, uint64_t nnz, const uint32_t* coords_dev,
-                  const double* vals_dev, cudaStream_t s);
+                  const double* vals_dev, cudaStream_t s, cudaEvent_t vals_ready = nullptr);
 void export_buckets(const DeviceTensor& T, int mode, uint64_t* offsets, uint64_t* entries, cudaStream_t s);
 }  // namespace hq
 struct hq_tns;

@@ -808,15 +808,35 @@ static int tensor_create_impl(int order, const uint64_t* dims, uint64_t nnz, con
             DBuf<double> v;
             c.alloc(nnz * order);
             v.alloc(nnz);
+            // coordinates first at full link bandwidth; the values follow on a second stream while the
+            // coordinate-only part of the build (range check, key packing, lexicographic sort) runs
+            cudaStream_t s2 = nullptr;
+            cudaEvent_t ev_c = nullptr, ev_v = nullptr;
+            HQ_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+            HQ_CUDA(cudaEventCreateWithFlags(&ev_c, cudaEventDisableTiming));
+            HQ_CUDA(cudaEventCreateWithFlags(&ev_v, cudaEventDisableTiming));
+            struct Cleanup {
+                cudaStream_t s2;
+                cudaEvent_t a, b;
+                ~Cleanup() {
+                    cudaStreamSynchronize(s2);
+                    cudaEventDestroy(a);
+                    cudaEventDestroy(b);
+                    cudaStreamDestroy(s2);
+                }
+            } cleanup{s2, ev_c, ev_v};
             HQ_CUDA(cudaMemcpyAsync(c.get(), coords, sizeof(uint32_t) * nnz * order, cudaMemcpyHostToDevice, s));
-            HQ_CUDA(cudaMemcpyAsync(v.get(), values, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+            HQ_CUDA(cudaEventRecord(ev_c, s));
+            HQ_CUDA(cudaStreamWaitEvent(s2, ev_c, 0));
+            HQ_CUDA(cudaMemcpyAsync(v.get(), values, sizeof(double) * nnz, cudaMemcpyHostToDevice, s2));
+            HQ_CUDA(cudaEventRecord(ev_v, s2));
             if (std::getenv("HQ_PROFILE_BUILD")) {
                 const auto t0 = std::chrono::steady_clock::now();
                 HQ_CUDA(cudaStreamSynchronize(s));
-                std::fprintf(stderr, "[build] upload wait     %8.2f ms\n",
+                std::fprintf(stderr, "[build] upload wait     %8.2f ms (coordinates)\n",
                              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
             }
-            build_tensor(h->t, order, dims, nnz, c.get(), v.get(), s);
+            build_tensor(h->t, order, dims, nnz, c.get(), v.get(), s, ev_v);
         }
         *out = h.release();
     });

@@ -21,10 +21,7 @@
 
 namespace hq {
 
-#ifndef HQ_RG_CTAS
-#define HQ_RG_CTAS 1
-#endif
-int dense_slots() { return num_sms() * HQ_RG_CTAS; }  // = the tall-skinny pass's grid (one CTA per SM, hq_rowgemm.cu)
+int dense_slots() { return num_sms(); }  // = the tall-skinny pass's grid (one CTA per SM, hq_rowgemm.cu)
 
 namespace {
 

@@ -243,10 +243,7 @@ __device__ __forceinline__ void cbar(int id, int n) { asm volatile("bar.sync %0,
 
 template <int K>
 struct RT {
-#ifndef HQ_RG_CTAS
-#define HQ_RG_CTAS 1
-#endif
-    static constexpr int CW = (K <= 16 && HQ_RG_CTAS == 1) ? 16 : 8;  // consumer warps (K > 16: register budget)
+    static constexpr int CW = K <= 16 ? 16 : 8;  // consumer warps (K > 16: register budget of the K x K fragments)
     static constexpr int ROWS = 8 * CW;           // rows per chunk
     static constexpr int NT = (K + 7) / 8;
     static constexpr int KP = NT * 8;
@@ -255,7 +252,7 @@ struct RT {
     static constexpr int CHD = ROWS * K;  // doubles per chunk per array
     // ring of chunk buffers: S2 stages of (A, other) pairs, or 2 S2 stages of A alone -- as many bytes in
     // flight as ~190 KB of shared memory holds (the pass is bound by bytes in flight x latency)
-    static constexpr int SB = (190 / HQ_RG_CTAS) * 1024;
+    static constexpr int SB = 190 * 1024;
     static constexpr int S2 = SB / (2 * CHD * 8) < 8 ? SB / (2 * CHD * 8) : 8;
     static_assert(S2 >= 2, "chunk ring");
     static constexpr int MAXS = 2 * S2;
@@ -264,7 +261,7 @@ struct RT {
 };
 
 template <int K>
-__global__ void __launch_bounds__((RT<K>::CW + 1) * 32, HQ_RG_CTAS)
+__global__ void __launch_bounds__((RT<K>::CW + 1) * 32, 1)
     k_rowgemm_tma(const double* A, uint64_t rows, const double* __restrict__ T, double* out,
                   const double* __restrict__ other, double* __restrict__ part, double* __restrict__ maxpart,
                   const DevStatus* st, int run_if) {

@@ -1,0 +1,62 @@
+"""GPU: skewed (Zipf) tensors -- the shape of BASELINE config 3 at test scale.
+
+Every mode of a Zipf tensor is "hot" (rows longer than 32x the mean hold >= 5 %
+of the nonzeros), so the passes gather those factors L1-allocating
+(cp.async.ca) and the heavy rows run through the segmented long-row kernels.
+Results must match the oracle (restatement of the reference's kernels.cpp /
+solvers.cpp) exactly as for uniform tensors, and be bitwise repeatable."""
+import numpy as np
+import pytest
+
+import paper_2510_16930_b200 as hq
+from paper_2510_16930_b200.workloads import uniform_coo, zipf_coo
+
+pytestmark = pytest.mark.gpu
+
+DIMS = [20000, 4000, 400]
+K = 10
+
+
+@pytest.fixture(scope="module")
+def zipf_tensor():
+    coords, vals = zipf_coo(DIMS, 300000, 3)
+    return hq.SparseTensor(DIMS, coords, vals)
+
+
+def test_mode_plan_marks_skewed_modes_hot(zipf_tensor):
+    for m in range(3):
+        p = zipf_tensor.mode_plan(m)
+        assert p["rows"] == DIMS[m]
+        assert p["hot"], (m, p)
+        assert p["long_rows"] > 0 and p["long_segments"] >= p["long_rows"]
+    coords, vals = uniform_coo([3000, 2500, 2000], 60000, 5)
+    u = hq.SparseTensor([3000, 2500, 2000], coords, vals)
+    assert not any(u.mode_plan(m)["hot"] for m in range(3))
+    with pytest.raises(hq.RangeError):
+        u.mode_plan(3)
+
+
+def test_zipf_kernels_match_oracle(oracle, zipf_tensor):
+    x = zipf_tensor
+    u = hq.random_factors(DIMS, [K] * 3, 21)
+    core = hq.ttmc_core(x, u)
+    oc = oracle.ttmc_core(DIMS, [K] * 3, x.coords(), x.values(), u.factors).reshape(-1)
+    scale = max(1.0, np.abs(oc).max())
+    assert np.abs(core.data - oc).max() <= 1e-11 * scale
+    for m in range(3):
+        a = hq.ttmctc_elementwise(x, u, m, core)
+        ao = oracle.ttmctc(DIMS, [K] * 3, x.coords(), x.values(), u.factors, m, core.data)
+        assert np.abs(a - ao).max() <= 1e-11 * max(1.0, np.abs(ao).max()), m
+        assert (a == hq.ttmctc_elementwise(x, u, m, core)).all()  # bitwise repeatable
+
+
+def test_zipf_hoqri_matches_oracle(oracle, zipf_tensor):
+    x = zipf_tensor
+    sweeps = 4
+    u0 = oracle.random_factors(DIMS, [K] * 3, 13)
+    r = hq.hoqri(x, hq.SolverConfig(ranks=[K] * 3, max_sweeps=sweeps, tol_fit_change=0.0), init_factors=u0)
+    ro = oracle.hoqri(DIMS, [K] * 3, x.coords(), x.values(), u0, sweeps)
+    rel = np.linalg.norm(r.model.core.data - ro["core"].reshape(-1)) / np.linalg.norm(ro["core"])
+    assert rel <= 1e-9, rel
+    obj = np.array([s.objective for s in r.trace.sweeps])
+    np.testing.assert_allclose(obj, ro["objective"], rtol=1e-9, atol=0)

@@ -8,11 +8,14 @@
 //   part[c] += X^T Y over the CTA's rows, Y = X (Gram) or another matrix
 //              (U_old, for the drift product P = U_new^T U_old)
 //   max|A|         (optional)
-// Each warp walks groups of 8 rows: A fragments come straight from HBM, the
-// X = A T product and the X^T Y accumulation are DMMA m8n8k4 (f64), X is
-// re-laid out through a per-warp shared-memory tile.  The K x K accumulators
-// stay in registers; warps are combined in fixed order into one partial slot
-// per CTA (deterministic).
+// Each warp walks groups of 8 rows: the X = A T product and the X^T Y
+// accumulation are DMMA m8n8k4 (f64), X is re-laid out through a per-warp
+// shared-memory tile.  The K x K accumulators stay in registers; warps are
+// combined in fixed order into one partial slot per CTA (deterministic).
+// Two kernels share that structure: k_rowgemm_tma (default) stages chunks of
+// contiguous rows in a shared-memory ring filled by a producer warp with
+// cp.async.bulk; k_rowgemm loads row groups through registers and is kept for
+// sources that are not 16-byte aligned (a multi-GPU row slice of A).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>

@@ -259,7 +259,7 @@ def run_reference(args, ws, rank):
     model, ncpu = host_desc()
     line = {"impl": "reference", "metric": METRIC.format(cfg=args.config), "value": value, "unit": "iter/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": sweep_s * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",  # same fixed workload as the engine arm
             "data": "synthetic (BASELINE config %d, seeded PCG64)" % args.config,
             "config": {"workload": c["name"], "dims": list(c["dims"]), "ranks": list(c["ranks"]),
                        "nnz_merged": int(ov.size)},

@@ -112,7 +112,9 @@ struct HhCtl {
     unsigned int bar_count;
     unsigned int bar_gen;
     unsigned int rng_seeded;
-    unsigned int pad;
+    unsigned int started;  // diagnostics for the barrier watchdog: CTAs that entered / left the kernel
+    unsigned int exited;
+    unsigned int pad[3];
     DevRng rng;
 };
 
@@ -120,6 +122,10 @@ __host__ __device__ inline size_t hh_part_doubles(int G) { return (size_t)2 * G 
 constexpr size_t kHhCtlDoubles = (sizeof(HhCtl) + 15) / 16 * 2;
 
 __device__ __forceinline__ void hh_grid_sync(HhCtl* ctl, unsigned int& gen) {
+    // every thread's global writes of this phase (partial slots, w, reflectors, q) are made visible at GPU
+    // scope before thread 0 signals arrival: a fence by thread 0 alone orders only its own stores, and a CTA
+    // reading another CTA's partial slot early derives different pivots -> diverging barrier counts (hang)
+    __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
@@ -133,8 +139,9 @@ __device__ __forceinline__ void hh_grid_sync(HhCtl* ctl, unsigned int& gen) {
             while (atomicAdd(&ctl->bar_gen, 0u) == gen) {
                 __nanosleep(64);
                 if (clock64() - t0 > (1ll << 33)) {  // ~4 s: a lost arrival -- fail loudly instead of hanging
-                    printf("hq: householder grid barrier timeout: cta %d gen %u count %u grid %d\n", (int)blockIdx.x,
-                           gen, atomicAdd(&ctl->bar_count, 0u), (int)gridDim.x);
+                    printf("hq: householder grid barrier timeout: cta %d gen %u count %u grid %d started %u exited %u\n",
+                           (int)blockIdx.x, gen, atomicAdd(&ctl->bar_count, 0u), (int)gridDim.x,
+                           atomicAdd(&ctl->started, 0u), atomicAdd(&ctl->exited, 0u));
                     __trap();
                 }
             }
@@ -167,7 +174,7 @@ __device__ __forceinline__ void hh_cta_partials(const double (&acc)[KM + 1], int
 __device__ __forceinline__ void hh_reduce_all(const double* part, int cnt, double* T) {
     for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
         double t = 0.0;
-        for (unsigned c = 0; c < gridDim.x; ++c) t += part[(size_t)c * kHhSlot + j];
+        for (unsigned c = 0; c < gridDim.x; ++c) t += __ldcg(part + (size_t)c * kHhSlot + j);  // L2: other CTAs' slots
         T[j] = t;
     }
     __syncthreads();
@@ -203,7 +210,10 @@ __global__ void __launch_bounds__(kHhThreads) k_householder_mc(const double* __r
     double* refl = w + m * (uint64_t)n;  // rows >= k of reflector k used
     const uint64_t r0 = m * c / G, r1 = m * (c + 1) / G;
     unsigned int gen = 0;
-    if (tid == 0) gen = atomicAdd(&ctl->bar_gen, 0u);
+    if (tid == 0) {
+        gen = atomicAdd(&ctl->bar_gen, 0u);
+        atomicAdd(&ctl->started, 1u);
+    }
     if (c == 0 && tid == 0) ctl->rng_seeded = 0;  // each QR starts the fill stream afresh (read after a barrier)
     int par = 0;
     uint64_t pos = 0;  // fill-stream position (identical in every CTA)
@@ -236,13 +246,17 @@ __global__ void __launch_bounds__(kHhThreads) k_householder_mc(const double* __r
         if (k == 0) ptol = 1e-12 * sqrt(T[KM]);
         double normx;
         {
-            const double x0 = w[(uint64_t)k * n + k];
+            const double x0 = __ldcg(w + (uint64_t)k * n + k);  // pivot row: another CTA's
             normx = sqrt(T[k] + x0 * x0);
         }
         // rank-deficient column: rows >= k replaced by the next normals of the
         // fill stream (dense_core.cpp:146-157), redrawn while the norm is zero
         bool need = normx <= ptol;
         while (need) {
+            // every CTA has read the pivot w[k][k] and taken the same decision before the owner of row k
+            // overwrites it with the fill: without this barrier a late CTA could read the filled pivot, skip
+            // the fill, and run two grid barriers fewer than the others (the kernel then hangs)
+            hh_grid_sync(ctl, gen);
             const uint64_t cnt = m - (uint64_t)k;
             if (table && pos + cnt <= table_len) {
                 for (uint64_t i = (r0 > (uint64_t)k ? r0 : (uint64_t)k) + tid; i < r1; i += nt)
@@ -272,13 +286,13 @@ __global__ void __launch_bounds__(kHhThreads) k_householder_mc(const double* __r
             }
             hh_grid_sync(ctl, gen);
             hh_reduce_all(slots(par), n, T);
-            const double x0 = w[(uint64_t)k * n + k];
+            const double x0 = __ldcg(w + (uint64_t)k * n + k);  // pivot row: another CTA's
             normx = sqrt(T[k] + x0 * x0);
             need = normx == 0.0;
         }
         // reflector (every CTA derives the same values)
         if (tid == 0) {
-            const double x0 = w[(uint64_t)k * n + k];
+            const double x0 = __ldcg(w + (uint64_t)k * n + k);  // pivot row: another CTA's
             const double alpha = (x0 >= 0.0) ? -normx : normx;
             const double vk = x0 - alpha;
             const double vn2 = T[k] + vk * vk;
@@ -287,7 +301,7 @@ __global__ void __launch_bounds__(kHhThreads) k_householder_mc(const double* __r
             flip[k] = alpha < 0.0;
         }
         __syncthreads();
-        for (int j = k + 1 + (int)tid; j < n; j += nt) dots[j] = betas[k] * (sc[2] * w[(uint64_t)k * n + j] + T[j]);
+        for (int j = k + 1 + (int)tid; j < n; j += nt) dots[j] = betas[k] * (sc[2] * __ldcg(w + (uint64_t)k * n + j) + T[j]);
         __syncthreads();
         // apply to columns > k over rows >= k; partial T for column k+1 (rows > k+1)
         {
@@ -381,6 +395,7 @@ __global__ void __launch_bounds__(kHhThreads) k_householder_mc(const double* __r
     for (uint64_t i = r0 + tid; i < r1; i += nt)
         for (int j = 0; j < n; ++j)
             if (flip[j]) q[i * n + j] = -q[i * n + j];
+    if (tid == 0) atomicAdd(&ctl->exited, 1u);
 }
 
 __global__ void k_gt(const double* __restrict__ core, ModeShape sh, int order, const int* __restrict__ dranks_unused,

@@ -107,6 +107,8 @@ __device__ double rng_normal(DevRng* r) {
 // else CTA 0 draws them with the device MT19937-64.
 constexpr int kHhThreads = 256;
 constexpr int kHhSlot = 36;  // partial-slot stride (K <= 32 sums + ||A||^2)
+constexpr int kHhGramSlot = 32 * 33 / 2;  // per-CTA partial of V^T V (upper triangle, K <= 32)
+constexpr int kHhGramRows = 64;           // rows of V staged per Gram tile
 
 struct HhCtl {
     unsigned int bar_count;
@@ -336,60 +338,106 @@ __global__ void __launch_bounds__(kHhThreads) k_householder_mc(const double* __r
         }
         hh_grid_sync(ctl, gen);
     }
-    // ---- Q = H_0 ... H_{n-1} [I; 0] by backward accumulation; the pass
-    // applying reflector kk also forms the partial dots v_{kk-1}^T Q
+    // ---- Q = H_0 ... H_{n-1} [I; 0] in compact WY form (LAPACK dlarft):
+    // H_0 ... H_{n-1} = I - V Tw V^T with V = [v_0 ... v_{n-1}] (v_k zero above row k) and Tw upper
+    // triangular, Tw[k][k] = beta_k, Tw[0:k, k] = -beta_k Tw[0:k, 0:k] (V[:, 0:k]^T v_k).  Then
+    // Q [i, :] = e_i - v(i) C with C = Tw V_top^T (V_top = the first n rows of V), so the whole product is
+    // one Gram pass (V^T V, partial per CTA), one barrier, and one pass writing Q -- equal in exact
+    // arithmetic to the reference's backward accumulation (dense_core.cpp:183-196).
     {
-        double acc[KM + 1];
+        constexpr int NP = KM * (KM + 1) / 2;  // upper-triangle pairs of V^T V
+        double* gpart = refl + (uint64_t)n * m;  // [G][kHhGramSlot]
+        __shared__ double sV[kHhGramRows][KM + 1];
+        __shared__ double sG[KM][KM];
+        __shared__ double sTw[KM][KM];
+        __shared__ double sC[KM][KM];
+        const int np = n * (n + 1) / 2;
+        double gacc[(NP + kHhThreads - 1) / kHhThreads];
 #pragma unroll
-        for (int j = 0; j <= KM; ++j) acc[j] = 0.0;
-        const int kk = n - 1;
+        for (int u = 0; u < (NP + kHhThreads - 1) / kHhThreads; ++u) gacc[u] = 0.0;
+        for (uint64_t t0 = r0; t0 < r1; t0 += kHhGramRows) {
+            const int tr = (int)min((uint64_t)kHhGramRows, r1 - t0);
+            __syncthreads();
+            for (int e = tid; e < kHhGramRows * n; e += nt) {  // reflector-major: coalesced along rows
+                const int k = e / kHhGramRows, r = e - k * kHhGramRows;
+                const uint64_t i = t0 + r;
+                sV[r][k] = (r < tr && i >= (uint64_t)k) ? refl[(uint64_t)k * m + i] : 0.0;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < (NP + kHhThreads - 1) / kHhThreads; ++u) {
+                const int pi = (int)tid + u * kHhThreads;
+                if (pi < np) {
+                    int k = 0, rem = pi;  // pair pi -> (k, l), l >= k, row-major upper triangle
+                    while (rem >= n - k) {
+                        rem -= n - k;
+                        ++k;
+                    }
+                    const int l = k + rem;
+                    double sacc = gacc[u];
+                    for (int r = 0; r < tr; ++r) sacc = fma(sV[r][k], sV[r][l], sacc);
+                    gacc[u] = sacc;
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < (NP + kHhThreads - 1) / kHhThreads; ++u) {
+            const int pi = (int)tid + u * kHhThreads;
+            if (pi < np) gpart[(size_t)c * kHhGramSlot + pi] = gacc[u];
+        }
+        hh_grid_sync(ctl, gen);
+        // V^T V (every CTA, fixed order over the CTAs), then Tw and C on one warp
+        for (int pi = tid; pi < np; pi += nt) {
+            double v = 0.0;
+            for (unsigned cc = 0; cc < G; ++cc) v += __ldcg(gpart + (size_t)cc * kHhGramSlot + pi);
+            int k = 0, rem = pi;
+            while (rem >= n - k) {
+                rem -= n - k;
+                ++k;
+            }
+            sG[k][k + rem] = v;
+            sG[k + rem][k] = v;
+        }
+        // V_top: the first n rows of V (another CTA's rows: read through L2)
+        for (int e = tid; e < n * n; e += nt) {
+            const int j = e / n, l = e - j * n;  // v_l[j]
+            sV[j][l] = ((uint64_t)j < m && j >= l) ? __ldcg(refl + (uint64_t)l * m + j) : 0.0;
+        }
+        __syncthreads();
+        if (tid < 32) {
+            const int lane = tid;
+            for (int k = 0; k < n; ++k) {
+                // Tw[0:k, k] = -beta_k Tw[0:k, 0:k] G[0:k, k]  (lane l computes row l < k)
+                double z = 0.0;
+                if (lane < k)
+                    for (int j = lane; j < k; ++j) z += sTw[lane][j] * sG[j][k];
+                __syncwarp();
+                if (lane < n) sTw[lane][k] = lane < k ? -betas[k] * z : (lane == k ? betas[k] : 0.0);
+                __syncwarp();
+            }
+            // C = Tw V_top^T: C[k][j] = sum_{l >= k} Tw[k][l] v_l[j]
+            for (int e = lane; e < n * n; e += 32) {
+                const int k = e / n, j = e - k * n;
+                double v = 0.0;
+                for (int l = k; l < n; ++l) v += sTw[k][l] * sV[j][l];
+                sC[k][j] = v;
+            }
+        }
+        __syncthreads();
         for (uint64_t i = r0 + tid; i < r1; i += nt) {
-            const double vi = (i >= (uint64_t)kk) ? refl[(uint64_t)kk * m + i] : 0.0;
+            double vi[KM];
+#pragma unroll
+            for (int k = 0; k < KM; ++k) vi[k] = (k < n && i >= (uint64_t)k) ? refl[(uint64_t)k * m + i] : 0.0;
 #pragma unroll
             for (int j = 0; j < KM; ++j)
                 if (j < n) {
-                    const double e = (i == (uint64_t)j) ? 1.0 : 0.0;
-                    q[i * n + j] = e;
-                    if (j >= kk) acc[j] += vi * e;
+                    double v = (i == (uint64_t)j) ? 1.0 : 0.0;
+#pragma unroll
+                    for (int k = 0; k < KM; ++k)
+                        if (k < n) v -= vi[k] * sC[k][j];
+                    q[i * n + j] = v;
                 }
         }
-        par ^= 1;
-        hh_cta_partials<KM>(acc, n, red_w, slot(par));
-    }
-    hh_grid_sync(ctl, gen);
-    for (int kk = n - 1; kk >= 0; --kk) {
-        hh_reduce_all(slots(par), n, T);
-        for (int j = kk + (int)tid; j < n; j += nt) dots[j] = betas[kk] * T[j];
-        __syncthreads();
-        double acc[KM + 1];
-#pragma unroll
-        for (int j = 0; j <= KM; ++j) acc[j] = 0.0;
-        const bool apply = betas[kk] != 0.0;
-        const int kn = kk - 1;
-        const uint64_t lo = kn >= 0 ? (uint64_t)kn : (uint64_t)kk;
-        for (uint64_t i = (r0 > lo ? r0 : lo) + tid; i < r1; i += nt) {
-            double row[KM];
-#pragma unroll
-            for (int j = 0; j < KM; ++j) row[j] = (j < n) ? q[i * n + j] : 0.0;
-            if (apply && i >= (uint64_t)kk) {
-                const double v = refl[(uint64_t)kk * m + i];
-#pragma unroll
-                for (int j = 0; j < KM; ++j)
-                    if (j >= kk && j < n) {
-                        row[j] -= dots[j] * v;
-                        q[i * n + j] = row[j];
-                    }
-            }
-            if (kn >= 0) {
-                const double vn = refl[(uint64_t)kn * m + i];
-#pragma unroll
-                for (int j = 0; j < KM; ++j)
-                    if (j >= kn && j < n) acc[j] += vn * row[j];
-            }
-        }
-        par ^= 1;
-        hh_cta_partials<KM>(acc, n, red_w, slot(par));
-        hh_grid_sync(ctl, gen);
     }
     // R_kk >= 0: flip the columns whose alpha was negative
     for (uint64_t i = r0 + tid; i < r1; i += nt)
@@ -586,7 +634,7 @@ void launch_drift_batch(const double* trp, int pairs, int order, const int* rank
 }
 
 size_t householder_work_doubles(uint64_t rows, int K) {
-    return kHhCtlDoubles + hh_part_doubles(num_sms()) + 2 * rows * (uint64_t)K;
+    return kHhCtlDoubles + hh_part_doubles(num_sms()) + 2 * rows * (uint64_t)K + (size_t)num_sms() * kHhGramSlot;
 }
 
 void householder_reset(double* work, cudaStream_t s) { HQ_CUDA(cudaMemsetAsync(work, 0, sizeof(HhCtl), s)); }

@@ -172,13 +172,25 @@ __device__ __forceinline__ void hh_cta_partials(const double (&acc)[KM + 1], int
     }
 }
 
+// sum over CTAs c = 0, 1, ... (this order, every CTA alike) of p[c * stride]; the loads of a batch of 8
+// are issued together (one L2 round trip per batch, not per CTA); L2 reads: other CTAs' slots
+__device__ __forceinline__ double hh_sum_slots(const double* p, size_t stride, unsigned G) {
+    double t = 0.0;
+    unsigned c = 0;
+    for (; c + 8 <= G; c += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(p + (size_t)(c + u) * stride);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t += v[u];
+    }
+    for (; c < G; ++c) t += __ldcg(p + (size_t)c * stride);
+    return t;
+}
+
 // every CTA: T[j] = sum over CTAs (in order) of part[c][j], j < cnt
 __device__ __forceinline__ void hh_reduce_all(const double* part, int cnt, double* T) {
-    for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
-        double t = 0.0;
-        for (unsigned c = 0; c < gridDim.x; ++c) t += __ldcg(part + (size_t)c * kHhSlot + j);  // L2: other CTAs' slots
-        T[j] = t;
-    }
+    for (int j = threadIdx.x; j < cnt; j += blockDim.x) T[j] = hh_sum_slots(part + j, kHhSlot, gridDim.x);
     __syncthreads();
 }
 
@@ -388,8 +400,7 @@ __global__ void __launch_bounds__(kHhThreads) k_householder_mc(const double* __r
         hh_grid_sync(ctl, gen);
         // V^T V (every CTA, fixed order over the CTAs), then Tw and C on one warp
         for (int pi = tid; pi < np; pi += nt) {
-            double v = 0.0;
-            for (unsigned cc = 0; cc < G; ++cc) v += __ldcg(gpart + (size_t)cc * kHhGramSlot + pi);
+            const double v = hh_sum_slots(gpart + pi, kHhGramSlot, G);
             int k = 0, rem = pi;
             while (rem >= n - k) {
                 rem -= n - k;

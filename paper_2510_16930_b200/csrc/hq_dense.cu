@@ -138,7 +138,14 @@ __device__ __forceinline__ void hh_grid_sync(HhCtl* ctl, unsigned int& gen) {
             atomicExch(&ctl->bar_gen, gen + 1);
         } else {
             const long long t0 = clock64();
-            while (atomicAdd(&ctl->bar_gen, 0u) == gen) {
+            // poll with acquire loads (served by L2 in parallel), not atomics that serialise on one address
+            // against the last arriver's release
+            auto gen_now = [&]() {
+                unsigned int g;
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(&ctl->bar_gen) : "memory");
+                return g;
+            };
+            while (gen_now() == gen) {
                 __nanosleep(64);
                 if (clock64() - t0 > (1ll << 33)) {  // ~4 s: a lost arrival -- fail loudly instead of hanging
                     printf("hq: householder grid barrier timeout: cta %d gen %u count %u grid %d started %u exited %u\n",

@@ -406,8 +406,11 @@ def run_engine(args, ws, rank, local):
         if ws > 1:
             dist.barrier()
         t0 = time.perf_counter()
+        step_s = []
         for _ in range(args.e2e_steps):
+            ts = time.perf_counter()
             r = e2e_step()
+            step_s.append(time.perf_counter() - ts)
         dt = time.perf_counter() - t0
         if ws > 1:
             t = torch.tensor([dt], device="cuda", dtype=torch.float64)
@@ -416,6 +419,7 @@ def run_engine(args, ws, rank, local):
         h2d = hc.nbytes + hv.nbytes + sum(a.nbytes for a in hu)
         d2h = sum(f.nbytes for f in r.model.factors.factors) + r.model.core.data.nbytes + 8 * (2 + N) * sweeps
         e2e = {"value": args.e2e_steps * sweeps / dt, "unit": "iter/s", "h2d_bytes_per_step": int(h2d),
+               "solve_s": [round(x, 4) for x in step_s],
                "d2h_bytes_per_step": int(d2h),
                "step": f"one full {sweeps}-sweep solve through the C-ABI from pinned host buffers: SparseTensor "
                        f"build (COO upload, device sort/merge/buckets) + init factors upload + {sweeps} sweeps + "

@@ -76,9 +76,10 @@ int hq_tensor_destroy(hq_tensor* t);
 int hq_tensor_info(const hq_tensor* t, int* order, uint64_t* dims, uint64_t* nnz);
 /* Work plan of one mode's unfolding (engine-side, no reference counterpart): rows, non-empty rows,
    long rows (> 256 nonzeros, segmented), their segments, and hot = 1 when the mode is skewed (rows longer
-   than 32x the mean hold >= 5% of the nonzeros) so its factor is gathered L1-allocating by the other passes */
+   than 32x the mean hold >= 5% of the nonzeros) so its factor is gathered L1-allocating by the other passes,
+   and max_tile32 = the most short-row nonzeros in one 32-row tile of the pass kernels */
 int hq_tensor_mode_plan(const hq_tensor* t, int mode, uint64_t* rows, uint64_t* nonempty_rows, uint64_t* long_rows,
-                        uint64_t* long_segments, int* hot);
+                        uint64_t* long_segments, int* hot, uint64_t* max_tile32);
 /* sorted, merged entries (sparse_tensor.hpp:44-51): coords nnz*order, values nnz */
 int hq_tensor_export(const hq_tensor* t, uint32_t* coords, double* values);
 /* ModeBuckets (sparse_tensor.hpp:25-32): offsets dims[mode]+1, entries nnz */

@@ -148,7 +148,8 @@ def load_library(path: str = None) -> C.CDLL:
     L.hq_tensor_create_dev.argtypes = [C.c_int, _u64p, C.c_uint64, vp, vp, vp, pp]
     L.hq_tensor_destroy.argtypes = [vp]
     L.hq_tensor_info.argtypes = [vp, C.POINTER(C.c_int), _u64p, C.POINTER(C.c_uint64)]
-    L.hq_tensor_mode_plan.argtypes = [vp, C.c_int] + [C.POINTER(C.c_uint64)] * 4 + [C.POINTER(C.c_int)]
+    L.hq_tensor_mode_plan.argtypes = [vp, C.c_int] + [C.POINTER(C.c_uint64)] * 4 + [C.POINTER(C.c_int),
+                                                                                    C.POINTER(C.c_uint64)]
     L.hq_tensor_export.argtypes = [vp, vp, vp]
     L.hq_tensor_buckets.argtypes = [vp, C.c_int, _u64p, vp]
     L.hq_tensor_norm_sq.argtypes = [vp, C.POINTER(C.c_double)]
@@ -310,12 +311,14 @@ class SparseTensor:
 
     def mode_plan(self, mode):
         """Engine work plan of one mode's unfolding: rows, nonempty_rows, long_rows (> 256 nonzeros),
-        long_segments, hot (skewed mode: its factor is gathered L1-allocating by the other passes)."""
-        v = [C.c_uint64() for _ in range(4)]
+        long_segments, hot (skewed mode: its factor is gathered L1-allocating by the other passes), max_tile32
+        (most short-row nonzeros in one 32-row tile)."""
+        v = [C.c_uint64() for _ in range(5)]
         hot = C.c_int()
-        _check(load_library().hq_tensor_mode_plan(self._h, int(mode), *[C.byref(x) for x in v], C.byref(hot)))
+        _check(load_library().hq_tensor_mode_plan(self._h, int(mode), *[C.byref(x) for x in v[:4]], C.byref(hot),
+                                                  C.byref(v[4])))
         return dict(rows=v[0].value, nonempty_rows=v[1].value, long_rows=v[2].value, long_segments=v[3].value,
-                    hot=bool(hot.value))
+                    hot=bool(hot.value), max_tile32=v[4].value)
 
     def _export(self):
         if self._coords is None:

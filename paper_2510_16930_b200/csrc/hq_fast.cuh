@@ -29,6 +29,7 @@ struct FastArgs {
     size_t l2_bytes;
     float l2_hit;
     int l1_a, l1_b;       // L1-allocating gathers for a hot (skewed) factor (ModeLayout::hot)
+    int tiles_fit;        // every 32-row tile holds at most 416 short-row records (ModeLayout::max_tile32)
 };
 
 // Sets the device's persisting-L2 carve-out to its maximum once and returns

@@ -123,6 +123,7 @@ struct ModeLayout {
     // how often U_n[i] is gathered by the other modes' passes, so a skewed mode's factor has hot rows that
     // pile onto single L2 slices: its gathers are made L1-allocating (cp.async.ca) to absorb the repeats.
     bool hot = false;
+    uint64_t max_tile32 = 0;  // most short-row nonzeros in one 32-row tile (the pass kernels' tile)
     // work plan (see hq_pass.cu)
     uint64_t long_rows = 0;
     DBuf<uint32_t> long_row_ids;       // rows with more than kShortMax nonzeros

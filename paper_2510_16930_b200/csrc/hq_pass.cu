@@ -56,6 +56,19 @@ __global__ void k_long_flags(const int64_t* __restrict__ rowptr, uint64_t rows, 
     }
 }
 
+__global__ void k_tile_max(const int64_t* __restrict__ rowptr, uint64_t rows, unsigned long long* __restrict__ out) {
+    const uint64_t nt = (rows + 31) / 32;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nt; t += (uint64_t)gridDim.x * blockDim.x) {
+        unsigned long long s = 0;
+        const uint64_t e = min(rows, t * 32 + 32);
+        for (uint64_t i = t * 32; i < e; ++i) {
+            const int64_t len = rowptr[i + 1] - rowptr[i];
+            if (len <= kShortMax) s += (unsigned long long)len;
+        }
+        atomicMax(out, s);
+    }
+}
+
 __global__ void k_long_compact(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
                                const uint32_t* __restrict__ nseg, const uint32_t* __restrict__ segpos, uint64_t rows,
                                uint32_t* __restrict__ ids, int64_t* __restrict__ segptr) {
@@ -109,8 +122,14 @@ void plan_mode(ModeLayout& L, uint64_t nnz, cudaStream_t s) {
     const int64_t hot_len = std::max<int64_t>(64, (int64_t)(32 * (nnz / std::max<uint64_t>(rows, 1))));
     k_long_flags<<<grid_for(rows), 256, 0, s>>>(L.rowptr.get(), rows, flag.get(), nseg.get(), hot_len, hot.get());
     HQ_CHECK_LAUNCH();
-    unsigned long long hot_nnz = 0;
+    DBuf<unsigned long long> tmax;
+    tmax.alloc(1);
+    HQ_CUDA(cudaMemsetAsync(tmax.get(), 0, sizeof(unsigned long long), s));
+    k_tile_max<<<grid_for((rows + 31) / 32), 256, 0, s>>>(L.rowptr.get(), rows, tmax.get());
+    HQ_CHECK_LAUNCH();
+    unsigned long long hot_nnz = 0, tile_max = 0;
     HQ_CUDA(cudaMemcpyAsync(&hot_nnz, hot.get(), sizeof(hot_nnz), cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaMemcpyAsync(&tile_max, tmax.get(), sizeof(tile_max), cudaMemcpyDeviceToHost, s));
     exclusive_scan(flag.get(), pos.get(), rows, s);
     exclusive_scan(nseg.get(), segpos.get(), rows, s);
     uint32_t lp = 0, lf = 0, sp = 0, sn = 0;
@@ -120,6 +139,7 @@ void plan_mode(ModeLayout& L, uint64_t nnz, cudaStream_t s) {
     HQ_CUDA(cudaMemcpyAsync(&sn, nseg.get() + rows - 1, 4, cudaMemcpyDeviceToHost, s));
     HQ_CUDA(cudaStreamSynchronize(s));
     L.hot = nnz > 0 && (double)hot_nnz >= 0.05 * (double)nnz;
+    L.max_tile32 = tile_max;
     L.long_rows = (uint64_t)lp + lf;
     L.long_segments = (uint64_t)sp + sn;
     if (L.long_rows) {
@@ -453,6 +473,7 @@ void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const Fac
         fa.l2_hit = budget ? (float)std::min(1.0, (double)budget / (double)fbytes) : 0.f;
         fa.l1_a = T.modes[L.others[0]].hot;
         fa.l1_b = T.modes[L.others[1]].hot;
+        fa.tiles_fit = L.max_tile32 <= 416;  // the warp-specialised pass's tile buffer (hq_pass_fast.cu)
         launch_fast(fa, sh, tile_grid(sh), s);
     } else {
         size_t smem = sizeof(double) * ((size_t)a.R * sh.L + (size_t)a.R * sh.kn);

@@ -917,7 +917,7 @@ int hq_tensor_info(const hq_tensor* t, int* order, uint64_t* dims, uint64_t* nnz
 }
 
 int hq_tensor_mode_plan(const hq_tensor* t, int mode, uint64_t* rows, uint64_t* nonempty_rows, uint64_t* long_rows,
-                        uint64_t* long_segments, int* hot) {
+                        uint64_t* long_segments, int* hot, uint64_t* max_tile32) {
     return guard([&] {
         if (mode < 0 || mode >= t->t.order)
             fail(HQ_ERR_RANGE, "mode " + std::to_string(mode) + " out of range for order " + std::to_string(t->t.order));
@@ -927,6 +927,7 @@ int hq_tensor_mode_plan(const hq_tensor* t, int mode, uint64_t* rows, uint64_t* 
         if (long_rows) *long_rows = L.long_rows;
         if (long_segments) *long_segments = L.long_segments;
         if (hot) *hot = L.hot ? 1 : 0;
+        if (max_tile32) *max_tile32 = L.max_tile32;
     });
 }
 

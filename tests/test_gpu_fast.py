@@ -120,3 +120,30 @@ def test_long_rows_fast_matches_oracle_and_generic(order, k):
         os.environ.pop("HQ_FORCE_GENERIC", None)
     for a, b in zip(fast, gen):
         assert np.abs(a - b).max() <= 1e-12 * np.abs(b).max()
+
+
+@pytest.mark.parametrize("skew", [False, True])
+def test_warp_specialised_pass_matches_oracle(skew):
+    """HQ_PASS_WS2=1: the producer/consumer pass (hq_pass_fast.cu k_pass_ws2) -- same results as the default
+    kernel up to summation order, and against the oracle."""
+    from oracle_bind import Oracle
+    o = Oracle()
+    dims = [20000, 15000, 10000]  # 5-10 nonzeros per row: every 32-row tile fits the 416-record buffer
+    x, u = _case(dims, 100000, 10, 31, skew)
+    assert all(x.mode_plan(m)["max_tile32"] <= 416 for m in range(3))  # so the WS2 kernel runs every mode
+    core = hq.ttmc_core(x, u)
+    base = [hq.ttmctc_elementwise(x, u, m, core) for m in range(3)]
+    os.environ["HQ_PASS_WS2"] = "1"
+    try:
+        core2 = hq.ttmc_core(x, u)
+        ws2 = [hq.ttmctc_elementwise(x, u, m, core) for m in range(3)]
+        ws2b = [hq.ttmctc_elementwise(x, u, m, core) for m in range(3)]
+    finally:
+        os.environ.pop("HQ_PASS_WS2", None)
+    oc = o.ttmc_core(dims, [10] * 3, x.coords(), x.values(), u.factors).reshape(-1)
+    assert np.abs(core2.data - oc).max() <= 1e-11 * max(1.0, np.abs(oc).max())
+    for m in range(3):
+        ao = o.ttmctc(dims, [10] * 3, x.coords(), x.values(), u.factors, m, core.data)
+        tol = 1e-11 * max(1.0, np.abs(ao).max())
+        assert np.abs(ws2[m] - ao).max() <= tol and np.abs(base[m] - ao).max() <= tol, m
+        assert (ws2[m] == ws2b[m]).all()  # bitwise repeatable

@@ -401,7 +401,8 @@ def run_engine(args, ws, rank, local):
             del se, xe
             return r
 
-        r = e2e_step()  # warm
+        for _ in range(2):  # warm: the first solves also grow the device memory pool to its working set
+            r = e2e_step()
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()

@@ -1404,11 +1404,317 @@ __global__ void __launch_bounds__(WS2<KA, KB, KN>::THREADS, 1) k_pass_ws2(FastAr
     }
 }
 
+// ============================================================================
+// Three-CTAs-per-SM pass (default for K = 10; HQ_PASS_NP=0 turns it off): no intra-CTA pipelining -- a tile's
+// meta, records, gathers and Kronecker rows run in sequence and the Y tile is
+// written over the staged rows -- so a CTA needs ~74 KB of shared memory and
+// twelve compute warps share an SM (three independent CTAs overlap each
+// other's phases instead of one CTA overlapping its own).
+#ifndef HQ_NP_CAP
+#define HQ_NP_CAP 384
+#endif
+#ifndef HQ_NP_MINB
+#define HQ_NP_MINB 3
+#endif
+template <int KA, int KB, int KN>
+struct CfgNP : Cfg<KA, KB, KN> {
+    static constexpr int CAP = HQ_NP_CAP;
+    static constexpr int FW = KA + KB;
+    static constexpr size_t RECB = (size_t)(CAP + 2) * 8 + 2 * (size_t)(CAP + 4) * 4;
+    static constexpr size_t SF = (size_t)CAP * FW * 8;
+    static constexpr size_t SY = (size_t)Cfg<KA, KB, KN>::R * Cfg<KA, KB, KN>::LDY * 8;
+    static_assert(SY <= SF, "the Y tile is written over the staged rows");
+    static constexpr size_t smem = SF + RECB + (size_t)Cfg<KA, KB, KN>::R * Cfg<KA, KB, KN>::ALD * 8 +
+                                   Cfg<KA, KB, KN>::META + Cfg<KA, KB, KN>::R * 4 + 64;
+};
+
+template <int KA, int KB, int KN>
+__global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
+    using C = CfgNP<KA, KB, KN>;
+    if (skip_kernel(a.st, a.run_if)) return;
+    extern __shared__ __align__(16) double sm[];
+    double* sF = sm;                                                   // staged rows; then the Y tile
+    double* sY = sm;
+    char* recb = reinterpret_cast<char*>(sm) + C::SF;
+    double* rxp = reinterpret_cast<double*>(recb);
+    uint32_t* rjp = reinterpret_cast<uint32_t*>(recb + (C::CAP + 2) * 8);
+    uint32_t* rkp = rjp + C::CAP + 4;
+    double* sA = reinterpret_cast<double*>(recb + C::RECB);
+    char* metab = reinterpret_cast<char*>(sA + (size_t)C::R * C::ALD);
+    int64_t* m_start = reinterpret_cast<int64_t*>(metab);
+    int* m_len = reinterpret_cast<int*>(metab + 8 * C::R);
+    int* m_off = m_len + C::R;
+    int* m_perm = m_len + 2 * C::R;
+    int* m_tot = m_len + 3 * C::R;
+    __shared__ double red[C::WARPS];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t pol_stream = policy_evict_first();
+    const uint64_t pol_f = policy_evict_last();
+    for (int q = tid; q < C::R * C::ALD; q += C::THREADS) sA[q] = 0.0;
+
+    const int G = gridDim.x, c = blockIdx.x;
+    const int64_t ntiles = (int64_t)((a.rows + C::R - 1) / C::R);
+    const uint64_t rend = a.rbase + a.rows;
+    const int64_t zb = a.rowptr[a.rbase];
+    const int64_t Z = a.rowptr[rend] - zb;
+    auto lower = [&](int64_t z) {
+        int64_t lo = 0, hi = ntiles;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            uint64_t r = a.rbase + min((uint64_t)mid * C::R, a.rows);
+            if (a.rowptr[r] - zb >= z) hi = mid; else lo = mid + 1;
+        }
+        return lo;
+    };
+    const int64_t t0 = lower((Z * c) / G);
+    const int64_t t1 = (c == G - 1) ? ntiles : lower((Z * (c + 1)) / G);
+
+    double macc[C::MBW][2];
+#pragma unroll
+    for (int b = 0; b < C::MBW; ++b) macc[b][0] = macc[b][1] = 0.0;
+    constexpr int NWB = C::NT * (C::NT + 1) / 2;
+    const int wmA = (C::NT == 1 || warp < 2) ? 0 : 1, wmB = (C::NT == 1 || warp == 0) ? 0 : 1;
+    double wfr0 = 0.0, wfr1 = 0.0;
+    double mx = 0.0;
+    const double* __restrict__ gt = a.gt;
+    const int gcolidx = (warp % C::NT) * 8 + (lane >> 2);
+    const bool gvalid = a.kind == kTTMcTC && gcolidx < KN;
+    const int rslot = warp * C::RPW + lane / C::TR;
+    const int pb = (lane % C::TR) / C::TQ, qb = lane % C::TQ;
+    const int p0 = pb * C::BP, q0 = qb * C::BQ, sub = lane % C::TR;
+    constexpr int PA = KA / 2, PP = (KA + KB) / 2, RPI = C::THREADS / PP;
+
+    int64_t nlo = 0, nhi = 0;  // rowptr slice of the next tile (threads < R)
+    auto load_rp = [&](int64_t t, int64_t& lo, int64_t& hi) {
+        lo = hi = 0;
+        if (t < t1 && tid < C::R) {
+            const uint64_t r = a.rbase + (uint64_t)t * C::R + tid;
+            if (r < rend) {
+                lo = a.rowptr[r];
+                hi = a.rowptr[r + 1];
+            }
+        }
+    };
+    load_rp(t0, nlo, nhi);
+    for (int64_t t = t0; t < t1; ++t) {
+        const uint64_t r0 = a.rbase + (uint64_t)t * C::R;
+        const int nr = (int)min((uint64_t)C::R, rend - r0);
+        // ---- meta
+        if (tid < C::R) {
+            m_len[tid] = (tid < nr) ? ((nhi - nlo > kShortMax) ? -1 : (int)(nhi - nlo)) : 0;
+            m_start[tid] = nlo;
+        }
+        __syncthreads();
+        if (tid < C::R) {
+            const int me = max(m_len[tid], 0);
+            int rank = 0, off = 0;
+            for (int r = 0; r < C::R; ++r) {
+                const int o = max(m_len[r], 0);
+                rank += (o > me) || (o == me && r < tid);
+                off += (r < tid) ? o : 0;
+            }
+            m_perm[rank] = tid;
+            m_off[tid] = off;
+            if (tid == C::R - 1) m_tot[0] = off + me;
+        }
+        load_rp(t + 1, nlo, nhi);
+        __syncthreads();
+        const int total = m_tot[0];
+        const int lr = m_perm[rslot];
+        const int len = max(m_len[lr], 0);
+        const int voff = m_off[lr];
+        double acc[C::BP][C::BQ];
+#pragma unroll
+        for (int p = 0; p < C::BP; ++p)
+#pragma unroll
+            for (int q = 0; q < C::BQ; ++q) acc[p][q] = 0.0;
+        for (int cv = 0; cv < max(total, 1); cv += C::CAP) {
+            const int cn = min(C::CAP, total - cv);
+            // records of virtual positions [cv, cv + cn): the row's lanes
+            {
+                const int64_t pbase = m_start[lr] - voff;
+                const int lo = max(voff, cv), hi = min(voff + len, cv + C::CAP);
+                for (int v = lo + sub; v < hi; v += C::TR) {
+                    const int64_t pz = pbase + v;
+                    cp8(rxp + (v - cv), a.val + pz, pol_stream);
+                    cp4(rjp + (v - cv), a.ia + pz, pol_stream);
+                    cp4(rkp + (v - cv), a.ib + pz, pol_stream);
+                }
+            }
+            cp_wait_all();
+            __syncthreads();
+            if (tid < RPI * PP) {
+                const int pc = tid % PP;
+                const bool isa = pc < PA;
+                const double* fb = isa ? a.ua + 2 * pc : a.ub + 2 * (pc - PA);
+                const int kk = isa ? KA : KB;
+                const int off = isa ? 2 * pc : KA + 2 * (pc - PA);
+                const uint32_t* idxp = isa ? rjp : rkp;
+                if (isa ? a.l1_a : a.l1_b) {
+                    for (int e = tid / PP; e < cn; e += RPI)
+                        cp16_l1(sF + (size_t)e * C::FW + off, fb + (size_t)idxp[e] * kk, pol_f);
+                } else {
+                    for (int e = tid / PP; e < cn; e += RPI)
+                        cp16(sF + (size_t)e * C::FW + off, fb + (size_t)idxp[e] * kk, pol_f);
+                }
+            }
+            cp_wait_all();
+            __syncthreads();
+            const int e0 = max(voff, cv) - cv, e1 = min(voff + len, cv + C::CAP) - cv;
+#pragma unroll 2
+            for (int e = e0; e < e1; ++e) {
+                const double x = rxp[e];
+                const double* f = sF + (size_t)e * C::FW;
+                double sa[C::BP], vb[C::BQ];
+                lds_block<C::BP>(f, p0, sa);
+                lds_block<C::BQ>(f + KA, q0, vb);
+#pragma unroll
+                for (int p = 0; p < C::BP; ++p) {
+                    const double sx = x * sa[p];
+#pragma unroll
+                    for (int q = 0; q < C::BQ; ++q) acc[p][q] = fma(sx, vb[q], acc[p][q]);
+                }
+            }
+            __syncthreads();  // staged rows / records consumed
+        }
+        {   // Y tile over the staged rows
+            double* y = sY + (size_t)lr * C::LDY;
+#pragma unroll
+            for (int p = 0; p < C::BP; ++p)
+#pragma unroll
+                for (int q = 0; q < C::BQ; ++q) y[blk_index<C::BP>(p0, p) * KB + blk_index<C::BQ>(q0, q)] = acc[p][q];
+            if (C::LP > C::L && pb == 0 && qb == 0)
+                for (int l = C::L; l < C::LP; ++l) y[l] = 0.0;
+        }
+        __syncthreads();
+        if (a.kind == kTTMcTC) {
+            const int nt = warp % C::NT;
+            constexpr int KSN = C::L / 4;
+            double cc[C::ABW][2][2];
+#pragma unroll
+            for (int bi = 0; bi < C::ABW; ++bi) cc[bi][0][0] = cc[bi][0][1] = cc[bi][1][0] = cc[bi][1][1] = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < KSN; ++ks)
+#pragma unroll
+                for (int bi = 0; bi < C::ABW; ++bi) {
+                    const int b = warp + bi * C::WARPS;
+                    if (b < C::AB) {
+                        const int mt = b / C::NT;
+                        const double yv = sY[(size_t)(mt * 8 + (lane >> 2)) * C::LDY + (lane & 3) + ks * 4];
+                        const double gv = gvalid ? __ldg(gt + (size_t)(ks * 4 + (lane & 3)) * KN + gcolidx) : 0.0;
+                        dmma884(cc[bi][ks & 1][0], cc[bi][ks & 1][1], yv, gv);
+                    }
+                }
+#pragma unroll
+            for (int bi = 0; bi < C::ABW; ++bi) {
+                const int b = warp + bi * C::WARPS;
+                if (b < C::AB) {
+                    const int mt = b / C::NT;
+                    const int row = mt * 8 + (lane >> 2);
+                    const int col = nt * 8 + 2 * (lane & 3);
+                    const bool valid = row < nr && m_len[row] >= 0;
+                    const double v0 = valid ? cc[bi][0][0] + cc[bi][1][0] : 0.0;
+                    const double v1 = valid ? cc[bi][0][1] + cc[bi][1][1] : 0.0;
+                    sA[row * C::ALD + col] = v0;
+                    sA[row * C::ALD + col + 1] = v1;
+                    mx = fmax(mx, fmax(fabs(v0), fabs(v1)));
+                    if (valid && a.A && col < KN) {
+                        double* dst = a.A + (r0 + row) * KN + col;
+                        if constexpr (KN % 2 == 0)
+                            *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+                        else {
+                            dst[0] = v0;
+                            if (col + 1 < KN) dst[1] = v1;
+                        }
+                    }
+                }
+            }
+        } else {
+            for (int q = tid; q < C::R * KN; q += C::THREADS) {
+                const int row = q / KN, r = q - row * KN;
+                const double v = (row < nr && m_len[row] >= 0) ? a.un[(r0 + row) * KN + r] : 0.0;
+                sA[row * C::ALD + r] = v;
+                mx = fmax(mx, fabs(v));
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int ks = 0; ks < C::R / 4; ++ks)
+#pragma unroll
+            for (int bi = 0; bi < C::MBW; ++bi) {
+                const int b = warp + bi * C::WARPS;
+                if (b < C::MB) {
+                    const int mt = b / C::NLT, nt = b - mt * C::NLT;
+                    const double av = sA[(size_t)(ks * 4 + (lane & 3)) * C::ALD + mt * 8 + (lane >> 2)];
+                    const double yv = sY[(size_t)(ks * 4 + (lane & 3)) * C::LDY + nt * 8 + (lane >> 2)];
+                    dmma884(macc[bi][0], macc[bi][1], av, yv);
+                }
+            }
+        if (warp < NWB) {
+#pragma unroll
+            for (int ks = 0; ks < C::R / 4; ++ks) {
+                const double* ar = sA + (size_t)(ks * 4 + (lane & 3)) * C::ALD + (lane >> 2);
+                dmma884(wfr0, wfr1, ar[wmA * 8], ar[wmB * 8]);
+            }
+        }
+        __syncthreads();
+    }
+
+    const int slot = a.slot0 + c;
+    double* mp = a.mpart + (size_t)slot * KN * C::L;
+#pragma unroll
+    for (int bi = 0; bi < C::MBW; ++bi) {
+        const int b = warp + bi * C::WARPS;
+        if (b < C::MB) {
+            const int mt = b / C::NLT, nt = b - mt * C::NLT;
+            const int r = mt * 8 + (lane >> 2), l = nt * 8 + 2 * (lane & 3);
+            if (r < KN) {
+                if (l < C::L) mp[(size_t)r * C::L + l] = macc[bi][0];
+                if (l + 1 < C::L) mp[(size_t)r * C::L + l + 1] = macc[bi][1];
+            }
+        }
+    }
+    if (warp < NWB) {
+        double* wp = a.wpart + (size_t)slot * KN * KN;
+        const int r = wmA * 8 + (lane >> 2), c0 = wmB * 8 + 2 * (lane & 3);
+        const double v[2] = {wfr0, wfr1};
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+            if (r < KN && c0 + e < KN) {
+                wp[r * KN + c0 + e] = v[e];
+                if (wmA != wmB) wp[(c0 + e) * KN + r] = v[e];
+            }
+    }
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+    if (lane == 0) red[warp] = mx;
+    __syncthreads();
+    if (tid == 0) {
+        double m = 0.0;
+        for (int w = 0; w < C::WARPS; ++w) m = fmax(m, red[w]);
+        a.maxpart[slot] = m;
+    }
+}
+
+bool np_pass_enabled();
+
 template <int KA, int KB, int KN>
 void launch_fast3(const FastArgs& a, int grid, cudaStream_t s) {
     using C = Cfg<KA, KB, KN>;
     using W = WsCfg<KA, KB, KN>;
     if constexpr (KA == 10 && KB == 10 && KN == 10) {
+        if (np_pass_enabled()) {  // grid = 3 CTAs per SM (fast_grid), one partial slot per CTA
+            using CN = CfgNP<KA, KB, KN>;
+            static bool attr3 = false;
+            if (!attr3) {
+                HQ_CUDA(cudaFuncSetAttribute(k_pass_np3<KA, KB, KN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)CN::smem));
+                attr3 = true;
+            }
+            k_pass_np3<KA, KB, KN><<<grid, 128, CN::smem, s>>>(a);
+            HQ_CHECK_LAUNCH();
+            return;
+        }
         // HQ_PASS_WS2=1 selects the warp-specialised pass (read per launch; a captured sweep graph keeps the
         // kernel chosen at capture).  Measured equal to the default on config 2 (0.75 ms per pass either way:
         // both sit at the random-sector DRAM rate of the factor gathers), so the simpler kernel is the default.
@@ -1462,8 +1768,20 @@ void launch_fast3(const FastArgs& a, int grid, cudaStream_t s) {
     HQ_CUDA(cudaLaunchKernelEx(&cfg, fn, a));
 }
 
+// the three-CTAs-per-SM pass is the default for K = 10 (config 2: 0.75 -> 0.68 ms per pass); HQ_PASS_NP=0
+// selects the software-pipelined two-CTAs-per-SM kernel (read once: it sets the slot count)
+bool np_pass_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("HQ_PASS_NP");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 template <int KA, int KB, int KN>
 int grid_fast3() {
+    if constexpr (KA == 10 && KB == 10 && KN == 10)
+        if (np_pass_enabled()) return num_sms() * HQ_NP_MINB;
     return num_sms() * Cfg<KA, KB, KN>::MINB;
 }
 

@@ -54,11 +54,19 @@ __global__ void gather(const double* A, const double* B, const uint2* idx, long 
         int cn = (int)min((long)CAP, e - r0);
         double* d = buf[r & 1];
         long long t0 = clock64();
-        if (mode == 0) {
+        if (mode == 0 || mode == 3) {
+            // mode 3: each table split into a 64-byte head (8 values, pitch 8) and a 16-byte tail (pitch 2)
+            const double* At = A + 8ull * 1000000;  // tails after the heads
+            const double* Bt = B + 8ull * 1000000;
             for (int q = threadIdx.x; q < cn * 10; q += blockDim.x) {
                 int t = q / 10, pc = q - t * 10;
                 uint2 jk = rec_idx(r0 + t, 1000000);
-                const double* src = pc < 5 ? A + (size_t)jk.x * pitch + 2 * pc : B + (size_t)jk.y * pitch + 2 * (pc - 5);
+                const double* src;
+                if (mode == 0) src = pc < 5 ? A + (size_t)jk.x * pitch + 2 * pc : B + (size_t)jk.y * pitch + 2 * (pc - 5);
+                else if (pc < 4) src = A + (size_t)jk.x * 8 + 2 * pc;
+                else if (pc == 4) src = At + (size_t)jk.x * 2;
+                else if (pc < 9) src = B + (size_t)jk.y * 8 + 2 * (pc - 5);
+                else src = Bt + (size_t)jk.y * 2;
                 cp16(d + (size_t)t * FW + 2 * pc, src);
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
@@ -98,7 +106,7 @@ __global__ void gather(const double* A, const double* B, const uint2* idx, long 
             if (r + 1 < rounds) asm volatile("cp.async.wait_group 1;" ::: "memory");
             else asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
-        if (mode != 0) mb_wait(&bar[r & 1], (r >> 1) & 1);
+        if (mode == 1 || mode == 2) mb_wait(&bar[r & 1], (r >> 1) & 1);
         __syncthreads();
         long r0 = b + (long)r * CAP;
         int cn = (int)min((long)CAP, e - r0);
@@ -121,7 +129,7 @@ int main() {
     int smem = 2 * CAP * FW * 8;  // 135 KB: one CTA per SM
     CK(cudaFuncSetAttribute(gather, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    for (int pitch : {10, 12, 16}) for (int threads : {128, 256, 512}) for (int mode = 0; mode < 1; ++mode) {
+    for (int pitch : {10}) for (int threads : {256, 512}) for (int mode : {0, 3}) {
         const int bps = 1;
         int grid = 148 * bps;
         for (int w = 0; w < 2; ++w) gather<<<grid, threads, smem>>>(A, B, idx, n, mode, out, ic, pitch);
@@ -133,7 +141,7 @@ int main() {
         unsigned long long hc; cudaMemcpy(&hc, ic, 8, cudaMemcpyDeviceToHost);
         double rounds = 3.0 * ((double)n / grid / CAP) * grid;
         printf("pitch %2d threads %3d mode %d (%s): %7.1f us  %6.1f G rows/s  issue %7.0f cycles/round\n", pitch, threads,
-               mode, mode == 2 ? "A bulk+B cp16" : mode ? "bulk/row    " : "cp16        ", ms * 1e3, 2.0 * n / ms / 1e6, hc / rounds);
+               mode, mode == 3 ? "split 64+16 " : mode == 2 ? "A bulk+B cp16" : mode ? "bulk/row    " : "cp16        ", ms * 1e3, 2.0 * n / ms / 1e6, hc / rounds);
     }
     return 0;
 }

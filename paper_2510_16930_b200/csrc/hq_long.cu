@@ -17,6 +17,7 @@
 // Same results contract as the generic long-row kernels in hq_pass.cu
 // (deterministic: static work assignment, fixed summation orders).
 #include <algorithm>
+#include <cstdlib>
 
 #include "hq_long.cuh"
 
@@ -263,6 +264,80 @@ __global__ void __launch_bounds__(256) k_longseg_mma(LongArgs a) {
     cpa_wait<0>();
 }
 
+// Synchronous variant (default for K = 16 at order 3; HQ_LONG_SYNC=0/1 forces): one chunk at a time per
+// CTA (records, then rows, then the
+// k-steps), one row buffer and one record buffer -- less shared memory per CTA, so more CTAs (warps) per SM
+// overlap each other's phases instead of one CTA overlapping its own.  Same arithmetic and order.
+template <int K0, int K1, int K2>
+__global__ void __launch_bounds__(256) k_longseg_sync(LongArgs a) {
+    using S = LS_<K0, K1, K2>;
+    if (skip_kernel(a.st, a.run_if)) return;
+    extern __shared__ __align__(16) double sm[];
+    double* rowbuf = sm;                                   // [CH][FW]
+    double* red = sm + S::row_doubles;                     // [WARPS][MT*NTL][64]
+    uint32_t* rec = reinterpret_cast<uint32_t*>(red + S::red_doubles);  // [NO][CH]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gid = lane >> 2, tig = lane & 3;
+    const uint64_t G = gridDim.x, c = blockIdx.x;
+    const uint64_t rend = a.rbase + a.rows;
+    const uint32_t* idx[3] = {a.i0, a.i1, a.i2};
+    ChunkCursor cc{a.nseg * c / G, a.nseg * (c + 1) / G, 0, 0};
+    cc.seek(a, rend);
+    double acc[S::MT][S::NTL][2];
+#pragma unroll
+    for (int i = 0; i < S::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < S::NTL; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    while (cc.valid()) {
+        const int n = cc.n(S::CH);
+#pragma unroll
+        for (int m = 0; m < S::NO; ++m)
+            for (int e = tid; e < n; e += S::THREADS)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr(rec + m * S::CH + e)),
+                             "l"(idx[m] + cc.z0 + e));
+        cpa_commit();
+        cpa_wait<0>();
+        __syncthreads();
+        gather_mode<K0, 0, S>(a.u0, rec, rowbuf, n, tid, a.l1_0);
+        gather_mode<K1, K0, S>(a.u1, rec + S::CH, rowbuf, n, tid, a.l1_1);
+        if constexpr (K2 != 0) gather_mode<K2, K0 + K1, S>(a.u2, rec + 2 * S::CH, rowbuf, n, tid, a.l1_2);
+        if (tid < n) cpa8(rowbuf + (size_t)tid * S::FW + S::RW, a.val + cc.z0 + tid);
+        cpa_commit();
+        cpa_wait<0>();
+        __syncthreads();
+        if (n == S::CH) {
+#pragma unroll 2
+            for (int ks = warp; ks < S::CH / 4; ks += S::WARPS) kstep<K0, K1, K2, S, true>(rowbuf, ks, n, gid, tig, acc);
+        } else {
+            for (int ks = warp; ks < (n + 3) / 4; ks += S::WARPS)
+                kstep<K0, K1, K2, S, false>(rowbuf, ks, n, gid, tig, acc);
+        }
+        if (cc.last(S::CH)) {
+            double* rw = red + (size_t)warp * S::MT * S::NTL * 64;
+#pragma unroll
+            for (int mt = 0; mt < S::MT; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < S::NTL; ++nt) {
+                    rw[(mt * S::NTL + nt) * 64 + gid * 8 + 2 * tig] = acc[mt][nt][0];
+                    rw[(mt * S::NTL + nt) * 64 + gid * 8 + 2 * tig + 1] = acc[mt][nt][1];
+                    acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+                }
+            __syncthreads();
+            const uint64_t sg = cc.sg;
+            for (int q = tid; q < S::L; q += S::THREADS) {
+                const int sidx = q / S::KL, t = q - sidx * S::KL;
+                const int o = ((sidx / 8) * S::NTL + t / 8) * 64 + (sidx % 8) * 8 + (t % 8);
+                double v = 0.0;
+#pragma unroll
+                for (int w = 0; w < S::WARPS; ++w) v += red[(size_t)w * S::MT * S::NTL * 64 + o];
+                a.ypart[sg * S::L + q] = v;
+            }
+        }
+        __syncthreads();  // rows, records and the reduction buffer are free for the next chunk
+        cc.advance(a, rend, S::CH);
+    }
+}
+
 // ---------------------------------------------------------------- fix-up --
 template <int L, int KN>
 struct LF_ {
@@ -457,16 +532,33 @@ template <int K0, int K1, int K2, int KN>
 void launch_long_t(const LongArgs& a, int fix_grid, cudaStream_t s) {
     using S = LS_<K0, K1, K2>;
     using F = LF_<S::L, KN>;
+    // the synchronous kernel wins where the pipelined one is held to two CTAs per SM by its buffers
+    // (K = 16, order 3: 1.10 -> 1.00 ms per config-4 pass); it loses at K = 10 (config 3) and order 4
+    // (config 5).  HQ_LONG_SYNC=0/1 forces either.
+    static const bool sync_var = [] {
+        const char* e = std::getenv("HQ_LONG_SYNC");
+        if (e && (e[0] == '0' || e[0] == '1')) return e[0] == '1';
+        return K0 == 16 && K1 == 16 && K2 == 0;
+    }();
+    constexpr size_t sync_smem = (S::row_doubles + S::red_doubles) * 8 + S::rec_words * 4;
     static int per_sm = 0;
     if (!per_sm) {
         set_smem_attr((const void*)k_longseg_mma<K0, K1, K2>, S::smem);
+        set_smem_attr((const void*)k_longseg_sync<K0, K1, K2>, sync_smem);
         set_smem_attr((const void*)k_longfix_mma<S::L, KN>, F::smem);
-        HQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_longseg_mma<K0, K1, K2>, S::THREADS,
-                                                              S::smem));
+        if (sync_var)
+            HQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_longseg_sync<K0, K1, K2>, S::THREADS,
+                                                                  sync_smem));
+        else
+            HQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_longseg_mma<K0, K1, K2>, S::THREADS,
+                                                                  S::smem));
         per_sm = std::max(per_sm, 1);
     }
     const int seg_grid = (int)std::min<uint64_t>(a.nseg, (uint64_t)num_sms() * per_sm);
-    k_longseg_mma<K0, K1, K2><<<seg_grid, S::THREADS, S::smem, s>>>(a);
+    if (sync_var)
+        k_longseg_sync<K0, K1, K2><<<seg_grid, S::THREADS, sync_smem, s>>>(a);
+    else
+        k_longseg_mma<K0, K1, K2><<<seg_grid, S::THREADS, S::smem, s>>>(a);
     HQ_CHECK_LAUNCH();
     k_longfix_mma<S::L, KN><<<fix_grid, F::THREADS, F::smem, s>>>(a);
     HQ_CHECK_LAUNCH();

@@ -147,3 +147,31 @@ def test_warp_specialised_pass_matches_oracle(skew):
         tol = 1e-11 * max(1.0, np.abs(ao).max())
         assert np.abs(ws2[m] - ao).max() <= tol and np.abs(base[m] - ao).max() <= tol, m
         assert (ws2[m] == ws2b[m]).all()  # bitwise repeatable
+
+
+def test_two_cta_pass_k10_matches_oracle_in_subprocess():
+    """HQ_PASS_NP=0 (read once per process: it sets the slot count) -- the two-CTA software-pipelined K = 10
+    kernel, which the three-CTA default replaced, still matches the oracle."""
+    import subprocess, sys, textwrap
+    code = textwrap.dedent("""
+        import sys, numpy as np
+        sys.path.insert(0, '.'); sys.path.insert(0, 'tests')
+        import paper_2510_16930_b200 as hq
+        from oracle_bind import Oracle
+        from paper_2510_16930_b200.workloads import uniform_coo
+        dims = [20000, 15000, 10000]
+        coords, vals = uniform_coo(dims, 100000, 41)
+        x = hq.SparseTensor(dims, coords, vals)
+        u = hq.random_factors(dims, [10] * 3, 42)
+        core = hq.ttmc_core(x, u)
+        o = Oracle()
+        for m in range(3):
+            a = hq.ttmctc_elementwise(x, u, m, core)
+            ao = o.ttmctc(dims, [10] * 3, x.coords(), x.values(), u.factors, m, core.data)
+            assert np.abs(a - ao).max() <= 1e-11 * max(1.0, np.abs(ao).max()), m
+        print("ok")
+    """)
+    env = dict(os.environ, HQ_PASS_NP="0")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr

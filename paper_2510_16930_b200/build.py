@@ -28,14 +28,32 @@ def _newer(target, sources):
 
 
 def build_engine(force=False, verbose=False):
+    """One object per .cu (compiled in parallel, rebuilt when the file or any
+    header / .inc changed), then one shared-library link."""
     os.makedirs(LIB, exist_ok=True)
+    obj_dir = os.path.join(ROOT, "build", "obj")
+    os.makedirs(obj_dir, exist_ok=True)
     cus = sorted(glob.glob(os.path.join(CSRC, "hq_*.cu")))
-    deps = cus + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.inc")) + [os.path.join(ROOT, "include", "hoqri_b200.h")]
-    if not force and not _newer(ENGINE, deps):
+    hdrs = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.inc")) + [os.path.join(ROOT, "include", "hoqri_b200.h")]
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills",
+             "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
+    objs, jobs = [], []
+    for cu in cus:
+        o = os.path.join(obj_dir, os.path.basename(cu)[:-3] + ".o")
+        objs.append(o)
+        if force or _newer(o, [cu] + hdrs):
+            jobs.append([NVCC, *flags, "-c", cu, "-o", o])
+    if jobs:
+        from concurrent.futures import ThreadPoolExecutor
+        def run(cmd):
+            if verbose:
+                print(" ".join(cmd), flush=True)
+            subprocess.check_call(cmd)
+        with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
+            list(ex.map(run, jobs))
+    if not force and not jobs and not _newer(ENGINE, objs):
         return ENGINE
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-           "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"),
-           *cus, "-lcublas", "-lcusolver", "-o", ENGINE]
+    cmd = [NVCC, *ARCH, "-shared", *objs, "-lcublas", "-lcusolver", "-o", ENGINE]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)

@@ -24,17 +24,9 @@ struct FastArgs {
     int slot0;
     const DevStatus* st;
     int run_if;
-    // L2 residency: the first gathered factor (ua) is marked persisting for
-    // the launch when l2_bytes > 0 (cudaLaunchAttributeAccessPolicyWindow)
-    size_t l2_bytes;
-    float l2_hit;
     int l1_a, l1_b;       // L1-allocating gathers for a hot (skewed) factor (ModeLayout::hot)
-    int tiles_fit;        // every 32-row tile holds at most 416 short-row records (ModeLayout::max_tile32)
 };
 
-// Sets the device's persisting-L2 carve-out to its maximum once and returns
-// it (bytes); 0 when the device has none.
-size_t l2_persist_budget();
 void debug_phase_cycles(unsigned long long* out, int reset);
 
 bool fast_supported(const ModeShape& sh);

@@ -374,11 +374,6 @@ int short_grid() { return num_sms() * 2; }
 
 // HQ_FORCE_GENERIC=1 routes every shape through the generic kernels (tests
 // compare both paths on the same inputs).
-bool l2_window_enabled() {
-    const char* e = std::getenv("HQ_NO_L2_WINDOW");
-    return !(e && e[0] == '1');
-}
-
 bool force_generic() {
     const char* e = std::getenv("HQ_FORCE_GENERIC");
     return e && e[0] == '1';
@@ -467,13 +462,8 @@ void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const Fac
         fa.slot0 = 0;
         fa.st = st;
         fa.run_if = run_if;
-        const size_t fbytes = (size_t)T.dims[L.others[0]] * sh.ko[0] * sizeof(double);
-        const size_t budget = l2_window_enabled() ? l2_persist_budget() : 0;
-        fa.l2_bytes = budget ? fbytes : 0;
-        fa.l2_hit = budget ? (float)std::min(1.0, (double)budget / (double)fbytes) : 0.f;
         fa.l1_a = T.modes[L.others[0]].hot;
         fa.l1_b = T.modes[L.others[1]].hot;
-        fa.tiles_fit = L.max_tile32 <= 416;  // the warp-specialised pass's tile buffer (hq_pass_fast.cu)
         launch_fast(fa, sh, tile_grid(sh), s);
     } else {
         size_t smem = sizeof(double) * ((size_t)a.R * sh.L + (size_t)a.R * sh.kn);

@@ -80,11 +80,6 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
-__device__ __forceinline__ uint64_t policy_evict_normal() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -218,8 +213,8 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
     const uint64_t pol_stream = policy_evict_first();
     // with a persisting window on U_a its gathers carry no explicit hint and
     // U_b streams; without one both factors are asked to stay (evict_last)
-    const uint64_t pol_a = a.l2_bytes ? policy_evict_normal() : policy_evict_last();
-    const uint64_t pol_b = a.l2_bytes ? pol_stream : policy_evict_last();
+    const uint64_t pol_a = policy_evict_last();
+    const uint64_t pol_b = policy_evict_last();
     for (int q = tid; q < C::R * C::ALD; q += C::THREADS) sA[q] = 0.0;
 
     // ---- tile range of this CTA (nnz-balanced, static)
@@ -601,811 +596,7 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
 
 
 // ============================================================================
-// Warp-specialised variant: one producer warp (row meta, records, factor-row
-// gathers with cp.async) and four consumer warps (Kronecker rows, GEMMs).  The
-// single gather buffer is handed over with named barriers: FULL (producer ->
-// consumers: a round of gathered rows is in shared memory) and FREE
-// (consumers -> producer: the Kronecker phase is done with it).  The producer
-// therefore fills tile t+1 while the consumers run tile t's GEMMs, and the
-// LSU-bound gather issue never stalls the arithmetic warps.
-__device__ __forceinline__ void bar_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void bar_arrive_n(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void mbar_init_cta(uint64_t* mbar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(mbar)), "r"(count) : "memory");
-}
-// arrives on mbar once all of this thread's earlier cp.async have landed
-__device__ __forceinline__ void cp_async_arrive(uint64_t* mbar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(mbar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_parity(uint64_t* mbar, uint32_t parity) {
-    asm volatile(
-        "{\n.reg .pred p;\nWAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(mbar)),
-        "r"(parity)
-        : "memory");
-}
-
-template <int KA, int KB, int KN>
-struct WsCfg {
-    using C = Cfg<KA, KB, KN>;
-    static constexpr int CTHREADS = C::THREADS;         // consumers
-    static constexpr int THREADS = C::THREADS + 32;      // + producer warp
-    static constexpr int XOFF = KA + KB;                 // x is staged after the two factor rows
-    static_assert(C::FW >= KA + KB + 1, "room for x in the gather slot");
-    static constexpr int BAR_FULL = 1, BAR_FREE = 2, BAR_C = 3;
-    static constexpr size_t smem_bytes = (size_t)C::CAP * C::FW * 8 + (size_t)C::R * C::LDY * 8 +
-                                         (size_t)C::CAP * 8 + (size_t)C::R * C::ALD * 8 + 3 * C::META + 64;
-};
-
-template <int KA, int KB, int KN>
-__global__ void __launch_bounds__(WsCfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MINB)
-    k_pass_ws3(FastArgs a) {
-    using C = Cfg<KA, KB, KN>;
-    using W = WsCfg<KA, KB, KN>;
-    if (skip_kernel(a.st, a.run_if)) return;
-    extern __shared__ __align__(16) double sm[];
-    double* sF = sm;                                                    // CAP x FW: rows + x
-    double* sY = sF + (size_t)C::CAP * C::FW;                           // R x LDY
-    uint2* sJK = reinterpret_cast<uint2*>(sY + (size_t)C::R * C::LDY);  // CAP (j, k)
-    double* sA = reinterpret_cast<double*>(sJK + C::CAP);               // R x ALD
-    char* sMetaB = reinterpret_cast<char*>(sA + (size_t)C::R * C::ALD);
-    auto m_start = [&](int mb) { return reinterpret_cast<int64_t*>(sMetaB + mb * C::META); };
-    auto m_len = [&](int mb) { return reinterpret_cast<int*>(sMetaB + mb * C::META + 8 * C::R); };
-    auto m_off = [&](int mb) { return m_len(mb) + C::R; };
-    auto m_perm = [&](int mb) { return m_len(mb) + 2 * C::R; };
-    auto m_tot = [&](int mb) { return m_len(mb) + 3 * C::R; };
-    __shared__ double red[C::WARPS];
-    __shared__ __align__(8) uint64_t full_mbar;  // "a round of gathered rows has landed"
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const bool producer = warp == C::WARPS;
-    if (tid == 0) mbar_init_cta(&full_mbar, 32);  // one cp.async arrival per producer lane
-    __syncthreads();
-
-    // ---- tile range of this CTA (nnz-balanced, static)
-    const int G = gridDim.x, c = blockIdx.x;
-    const int64_t ntiles = (int64_t)((a.rows + C::R - 1) / C::R);
-    const uint64_t rend = a.rbase + a.rows;
-    const int64_t zb = a.rowptr[a.rbase];
-    const int64_t Z = a.rowptr[rend] - zb;
-    auto lower = [&](int64_t z) {
-        int64_t lo = 0, hi = ntiles;
-        while (lo < hi) {
-            int64_t mid = (lo + hi) >> 1;
-            uint64_t r = a.rbase + min((uint64_t)mid * C::R, a.rows);
-            if (a.rowptr[r] - zb >= z) hi = mid; else lo = mid + 1;
-        }
-        return lo;
-    };
-    const int64_t t0 = lower((Z * c) / G);
-    const int64_t t1 = (c == G - 1) ? ntiles : lower((Z * (c + 1)) / G);
-    auto rounds_of = [&](int total) { return total > 0 ? (total + C::CAP - 1) / C::CAP : 1; };
-
-    if (producer) {
-        // ================================ producer warp
-        const uint64_t pol_stream = policy_evict_first();
-        const uint64_t pol_f = policy_evict_last();
-        constexpr int PA = KA / 2, PP = (KA + KB) / 2;
-        // row meta of tile t (lane r owns row r of the tile), warp-synchronous
-        auto meta = [&](int64_t t, int mb) {
-            const uint64_t r0 = a.rbase + (uint64_t)t * C::R;
-            const int nr = (int)min((uint64_t)C::R, rend - r0);
-            for (int r = lane; r < C::R; r += 32) {
-                int len = 0;
-                int64_t st = 0;
-                if (r < nr) {
-                    st = a.rowptr[r0 + r];
-                    const int64_t l = a.rowptr[r0 + r + 1] - st;
-                    len = (l > kShortMax) ? -1 : (int)l;
-                }
-                m_len(mb)[r] = len;
-                m_start(mb)[r] = st;
-            }
-            __syncwarp();
-            const int* ln = m_len(mb);
-            for (int r = lane; r < C::R; r += 32) {
-                const int me = max(ln[r], 0);
-                int rank = 0, off = 0;
-                for (int q = 0; q < C::R; ++q) {
-                    const int o = max(ln[q], 0);
-                    rank += (o > me) || (o == me && q < r);
-                    off += (q < r) ? o : 0;
-                }
-                m_perm(mb)[rank] = r;
-                m_off(mb)[r] = off;
-                if (r == C::R - 1) m_tot(mb)[0] = off + me;
-            }
-            __syncwarp();
-        };
-        // (j, k) of virtual records [cv, cv + CAP) of a tile -> sJK (lane per row)
-        auto records = [&](int mb, int cv) {
-            for (int r = lane; r < C::R; r += 32) {
-                const int len = max(m_len(mb)[r], 0), off = m_off(mb)[r];
-                const int64_t pbase = m_start(mb)[r] - off;
-                const int lo = max(off, cv), hi = min(off + len, cv + C::CAP);
-                for (int v = lo; v < hi; ++v) {
-                    cp4(&sJK[v - cv].x, a.ia + pbase + v, pol_stream);
-                    cp4(&sJK[v - cv].y, a.ib + pbase + v, pol_stream);
-                }
-            }
-            asm volatile("cp.async.commit_group;\n" ::: "memory");
-        };
-        // factor rows + x of virtual records [cv, cv + cn) -> sF; completion arrives on full_mbar
-        auto gathers = [&](int mb, int cv, int cn) {
-            cp_wait_all();  // (j, k) staged (earlier gathers landed long ago: the consumers freed sF)
-            __syncwarp();
-            for (int q = lane; q < cn * PP; q += 32) {
-                const int e = q / PP, pc = q - e * PP;
-                const uint2 jk = sJK[e];
-                const double* src = (pc < PA) ? a.ua + (size_t)jk.x * KA + 2 * pc : a.ub + (size_t)jk.y * KB + 2 * (pc - PA);
-                cp16(sF + (size_t)e * C::FW + ((pc < PA) ? 2 * pc : KA + 2 * (pc - PA)), src, pol_f);
-            }
-            for (int r = lane; r < C::R; r += 32) {  // x, straight from the value stream
-                const int len = max(m_len(mb)[r], 0), off = m_off(mb)[r];
-                const int64_t pbase = m_start(mb)[r] - off;
-                const int lo = max(off, cv), hi = min(off + len, cv + cn);
-                for (int v = lo; v < hi; ++v) cp8(sF + (size_t)(v - cv) * C::FW + W::XOFF, a.val + pbase + v, pol_stream);
-            }
-            cp_async_arrive(&full_mbar);
-        };
-        if (t0 < t1) {
-            meta(t0, 0);
-            records(0, 0);
-        }
-        bool first = true;
-        for (int64_t t = t0; t < t1; ++t) {
-            const int mb = (int)((t - t0) % 3);
-            const int total = m_tot(mb)[0];
-            const int rounds = rounds_of(total);
-            for (int rd = 0; rd < rounds; ++rd) {
-                const int cv = rd * C::CAP, cn = max(0, min(C::CAP, total - cv));
-                if (!first) bar_sync_n(W::BAR_FREE, W::THREADS);
-                first = false;
-                if (rd > 0) records(mb, cv);
-                gathers(mb, cv, cn);
-                if (rd == rounds - 1 && t + 1 < t1) {  // next tile's meta and records while the consumers work
-                    meta(t + 1, (mb + 1) % 3);
-                    records((mb + 1) % 3, 0);
-                }
-            }
-        }
-        if (!first) bar_sync_n(W::BAR_FREE, W::THREADS);  // the consumers' last FREE
-        return;
-    }
-
-    // ================================ consumer warps (C::THREADS threads)
-    for (int q = tid; q < C::R * C::ALD; q += C::THREADS) sA[q] = 0.0;
-    double macc[C::MBW][2];
-#pragma unroll
-    for (int b = 0; b < C::MBW; ++b) macc[b][0] = macc[b][1] = 0.0;
-    double wacc[C::WQ];
-#pragma unroll
-    for (int b = 0; b < C::WQ; ++b) wacc[b] = 0.0;
-    double mx = 0.0;
-    const double* __restrict__ gt = a.gt;
-    static_assert(C::WARPS % C::NT == 0, "warp -> n-tile mapping");
-    constexpr bool kGReg = C::L / 4 <= 32;
-    double gfr[kGReg ? C::L / 4 : 1];
-    const int gcolidx = (warp % C::NT) * 8 + (lane >> 2);
-    const bool gvalid = a.kind == kTTMcTC && gcolidx < KN;
-    if constexpr (kGReg) {
-#pragma unroll
-        for (int ks = 0; ks < C::L / 4; ++ks)
-            gfr[ks] = gvalid ? __ldg(gt + (size_t)(ks * 4 + (lane & 3)) * KN + gcolidx) : 0.0;
-    }
-    const int rslot = warp * C::RPW + lane / C::TR;
-    const int pb = (lane % C::TR) / C::TQ, qb = lane % C::TQ;
-    const int p0 = pb * C::BP, q0 = qb * C::BQ;
-    uint32_t full_phase = 0;
-
-    for (int64_t t = t0; t < t1; ++t) {
-        const int mb = (int)((t - t0) % 3);
-        const uint64_t r0 = a.rbase + (uint64_t)t * C::R;
-        const int nr = (int)min((uint64_t)C::R, rend - r0);
-        double acc[C::BP][C::BQ];
-#pragma unroll
-        for (int p = 0; p < C::BP; ++p)
-#pragma unroll
-            for (int q = 0; q < C::BQ; ++q) acc[p][q] = 0.0;
-        int total = 0, lr = 0, len = 0, voff = 0;
-        for (int rd = 0;; ++rd) {
-            mbar_wait_parity(&full_mbar, full_phase);
-            full_phase ^= 1;
-            if (rd == 0) {
-                total = m_tot(mb)[0];
-                lr = m_perm(mb)[rslot];
-                len = max(m_len(mb)[lr], 0);
-                voff = m_off(mb)[lr];
-            }
-            const int cv = rd * C::CAP;
-            const int e0 = max(voff, cv) - cv, e1 = min(voff + len, cv + C::CAP) - cv;
-#pragma unroll 2
-            for (int e = e0; e < e1; ++e) {
-                const double* f = sF + (size_t)e * C::FW;
-                const double x = f[W::XOFF];
-                double sa[C::BP], vb[C::BQ];
-                lds_block<C::BP>(f, p0, sa);
-                lds_block<C::BQ>(f + KA, q0, vb);
-#pragma unroll
-                for (int p = 0; p < C::BP; ++p) {
-                    const double sx = x * sa[p];
-#pragma unroll
-                    for (int q = 0; q < C::BQ; ++q) acc[p][q] = fma(sx, vb[q], acc[p][q]);
-                }
-            }
-            bar_arrive_n(W::BAR_FREE, W::THREADS);
-            if (rd + 1 >= rounds_of(total)) break;
-        }
-        {
-            double* y = sY + (size_t)lr * C::LDY;
-#pragma unroll
-            for (int p = 0; p < C::BP; ++p)
-#pragma unroll
-                for (int q = 0; q < C::BQ; ++q) y[blk_index<C::BP>(p0, p) * KB + blk_index<C::BQ>(q0, q)] = acc[p][q];
-            if (C::LP > C::L && pb == 0 && qb == 0)
-                for (int l = C::L; l < C::LP; ++l) y[l] = 0.0;
-        }
-        bar_sync_n(W::BAR_C, W::CTHREADS);
-        const int* ln = m_len(mb);
-        if (a.kind == kTTMcTC) {
-            const int nt = warp % C::NT;
-            constexpr int KSN = C::L / 4;
-            double cc[C::ABW][2][2];
-#pragma unroll
-            for (int bi = 0; bi < C::ABW; ++bi) cc[bi][0][0] = cc[bi][0][1] = cc[bi][1][0] = cc[bi][1][1] = 0.0;
-#pragma unroll
-            for (int ks = 0; ks < KSN; ++ks)
-#pragma unroll
-                for (int bi = 0; bi < C::ABW; ++bi) {
-                    const int b = warp + bi * C::WARPS;
-                    if (b < C::AB) {
-                        const int mt = b / C::NT;
-                        const double yv = sY[(size_t)(mt * 8 + (lane >> 2)) * C::LDY + (lane & 3) + ks * 4];
-                        double gv;
-                        if constexpr (kGReg)
-                            gv = gfr[ks];
-                        else
-                            gv = gvalid ? __ldg(gt + (size_t)(ks * 4 + (lane & 3)) * KN + gcolidx) : 0.0;
-                        dmma884(cc[bi][ks & 1][0], cc[bi][ks & 1][1], yv, gv);
-                    }
-                }
-#pragma unroll
-            for (int bi = 0; bi < C::ABW; ++bi) {
-                const int b = warp + bi * C::WARPS;
-                if (b < C::AB) {
-                    const int mt = b / C::NT;
-                    const int row = mt * 8 + (lane >> 2);
-                    const int col = nt * 8 + 2 * (lane & 3);
-                    sA[row * C::ALD + col] = cc[bi][0][0] + cc[bi][1][0];
-                    sA[row * C::ALD + col + 1] = cc[bi][0][1] + cc[bi][1][1];
-                }
-            }
-        } else {
-            for (int q = tid; q < C::R * KN; q += C::THREADS) {
-                const int row = q / KN, r = q - row * KN;
-                sA[row * C::ALD + r] = (row < nr && ln[row] >= 0) ? a.un[(r0 + row) * KN + r] : 0.0;
-            }
-        }
-        bar_sync_n(W::BAR_C, W::CTHREADS);
-        for (int q = tid; q < C::R * KN; q += C::THREADS) {
-            const int row = q / KN, r = q - row * KN;
-            const double v = sA[row * C::ALD + r];
-            if (row < nr && ln[row] >= 0) {
-                if (a.A) a.A[(r0 + row) * KN + r] = v;
-                mx = fmax(mx, fabs(v));
-            } else {
-                sA[row * C::ALD + r] = 0.0;
-            }
-        }
-        bar_sync_n(W::BAR_C, W::CTHREADS);
-#pragma unroll
-        for (int ks = 0; ks < C::R / 4; ++ks)
-#pragma unroll
-            for (int bi = 0; bi < C::MBW; ++bi) {
-                const int b = warp + bi * C::WARPS;
-                if (b < C::MB) {
-                    const int mt = b / C::NLT, nt = b - mt * C::NLT;
-                    const double av = sA[(size_t)(ks * 4 + (lane & 3)) * C::ALD + mt * 8 + (lane >> 2)];
-                    const double yv = sY[(size_t)(ks * 4 + (lane & 3)) * C::LDY + nt * 8 + (lane >> 2)];
-                    dmma884(macc[bi][0], macc[bi][1], av, yv);
-                }
-            }
-#pragma unroll
-        for (int wi = 0; wi < C::WQ; ++wi) {
-            const int q = tid + wi * C::THREADS;
-            if (q < KN * KN) {
-                const int r1 = q / KN, r2 = q - r1 * KN;
-                double sacc = wacc[wi];
-                for (int row = 0; row < C::R; ++row) sacc = fma(sA[row * C::ALD + r1], sA[row * C::ALD + r2], sacc);
-                wacc[wi] = sacc;
-            }
-        }
-        bar_sync_n(W::BAR_C, W::CTHREADS);
-    }
-
-    const int slot = a.slot0 + c;
-    double* mp = a.mpart + (size_t)slot * KN * C::L;
-#pragma unroll
-    for (int bi = 0; bi < C::MBW; ++bi) {
-        const int b = warp + bi * C::WARPS;
-        if (b < C::MB) {
-            const int mt = b / C::NLT, nt = b - mt * C::NLT;
-            const int r = mt * 8 + (lane >> 2);
-            const int l = nt * 8 + 2 * (lane & 3);
-            if (r < KN) {
-                if (l < C::L) mp[(size_t)r * C::L + l] = macc[bi][0];
-                if (l + 1 < C::L) mp[(size_t)r * C::L + l + 1] = macc[bi][1];
-            }
-        }
-    }
-#pragma unroll
-    for (int wi = 0; wi < C::WQ; ++wi) {
-        const int q = tid + wi * C::THREADS;
-        if (q < KN * KN) a.wpart[(size_t)slot * KN * KN + q] = wacc[wi];
-    }
-    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
-    if (lane == 0) red[warp] = mx;
-    bar_sync_n(W::BAR_C, W::CTHREADS);
-    if (tid == 0) {
-        double m = 0.0;
-        for (int w = 0; w < C::WARPS; ++w) m = fmax(m, red[w]);
-        a.maxpart[slot] = m;
-    }
-}
-
-// ============================================================================
-// Warp-specialised pass, version 2 (one CTA per SM, 12 warps):
-//   warps 8-11  producer warpgroup: row meta, tile records, factor-row gathers
-//               (cp.async pieces) -- never stalls on arithmetic;
-//   warps 0-3 / 4-7  two consumer groups; group g takes tiles j = g, g+2, ...
-//               of the CTA's range and owns gather buffer g.
-// Handshake per buffer: FULL[g] (every producer thread's cp.async landed:
-// cp.async.mbarrier.arrive.noinc) and EMPTY[g] (the group finished the
-// Kronecker rows of the tile, so the buffer can be refilled).  The group then
-// runs the tile's GEMMs on its own Y / A tiles while the producers fill the
-// buffer with its next tile.  All 384 threads fit 168 registers without
-// spills (no register re-allocation needed).  Only for tiles of at most
-// CAP records (ModeLayout::max_tile32 checked by the dispatcher).  Partial
-// slots: CTA c writes slot c (group 0 + group 1, fixed order) and zeroes slot
-// c + gridDim.x (the dispatcher's slot count is that of the 2-CTA/SM kernel).
-__device__ __forceinline__ void mbar_init2(uint64_t* b, uint32_t n) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(n) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive2(uint64_t* b) {
-    asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(smem_addr(b)) : "memory");
-}
-__device__ __forceinline__ bool mbar_try2(uint64_t* b, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n.reg .pred p;\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        "selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(smem_addr(b)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait2(uint64_t* b, uint32_t parity) {
-    if (mbar_try2(b, parity)) return;
-    const long long t0 = clock64();
-    while (!mbar_try2(b, parity)) {
-        if (clock64() - t0 > (1ll << 33)) {
-            printf("hq: ws2 pass barrier timeout: cta %d thread %d\n", (int)blockIdx.x, (int)threadIdx.x);
-            __trap();
-        }
-    }
-}
-__device__ __forceinline__ void nbar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-// WS2 staging: 416 records per tile buffer (a 32-row tile of config 2 holds 320 +- 18), rows unpadded
-// (FW = KA + KB: consecutive records still start 8 banks apart at K = 10)
-template <int KA, int KB, int KN>
-struct Cfg2 : Cfg<KA, KB, KN> {
-    static constexpr int CAP = 416;
-    static constexpr int FW = KA + KB;
-    static constexpr size_t RECB = (size_t)(CAP + 2) * 8 + 2 * (size_t)(CAP + 4) * 4;
-    static_assert(RECB % 16 == 0, "record buffer alignment");
-};
-
-template <int KA, int KB, int KN>
-struct WS2 {
-    using C = Cfg2<KA, KB, KN>;
-    static constexpr int THREADS = 3 * C::THREADS;  // 2 consumer groups + producers
-    static constexpr size_t SF = (size_t)C::CAP * C::FW * 8;
-    static constexpr size_t SY = (size_t)C::R * C::LDY * 8;
-    static constexpr size_t SA = (size_t)C::R * C::ALD * 8;
-    static constexpr size_t smem = 2 * SF + 3 * C::RECB + 3 * C::META + 2 * SY + 2 * SA + 2 * C::R * 4 + 64 + 64;
-};
-
-template <int KA, int KB, int KN>
-__global__ void __launch_bounds__(WS2<KA, KB, KN>::THREADS, 1) k_pass_ws2(FastArgs a) {
-    using C = Cfg2<KA, KB, KN>;
-    using W = WS2<KA, KB, KN>;
-    static_assert(C::R == 32 && C::THREADS == 128, "one producer warp owns a tile's row meta");
-    if (skip_kernel(a.st, a.run_if)) return;
-    extern __shared__ __align__(16) double sm[];
-    char* base = reinterpret_cast<char*>(sm);
-    auto sFb = [&](int b) { return reinterpret_cast<double*>(base + b * W::SF); };
-    char* recb = base + 2 * W::SF;
-    auto rx = [&](int b) { return reinterpret_cast<double*>(recb + b * C::RECB); };
-    auto rj = [&](int b) { return reinterpret_cast<uint32_t*>(recb + b * C::RECB + (C::CAP + 2) * 8); };
-    auto rk = [&](int b) { return rj(b) + C::CAP + 4; };
-    char* metab = recb + 3 * C::RECB;  // record / meta slots: tile j uses slot j % 3
-    auto m_start = [&](int b) { return reinterpret_cast<int64_t*>(metab + b * C::META); };
-    auto m_len = [&](int b) { return reinterpret_cast<int*>(metab + b * C::META + 8 * C::R); };
-    auto m_off = [&](int b) { return m_len(b) + C::R; };
-    auto m_perm = [&](int b) { return m_len(b) + 2 * C::R; };
-    auto m_tot = [&](int b) { return m_len(b) + 3 * C::R; };
-    double* sYb = reinterpret_cast<double*>(metab + 3 * C::META);
-    double* sAb = reinterpret_cast<double*>(reinterpret_cast<char*>(sYb) + 2 * W::SY);
-    int* vmaskb = reinterpret_cast<int*>(reinterpret_cast<char*>(sAb) + 2 * W::SA);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(vmaskb + 2 * C::R);  // full[2], empty[2]
-    double* redmax = reinterpret_cast<double*>(bars + 4);              // [8] per consumer warp
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int role = warp >> 2;  // 0, 1: consumer group; 2: producers
-    if (tid == 0) {
-        mbar_init2(&bars[0], C::THREADS);  // full: one cp.async arrival per producer thread
-        mbar_init2(&bars[1], C::THREADS);
-        mbar_init2(&bars[2], C::THREADS);  // empty: every consumer thread of the group
-        mbar_init2(&bars[3], C::THREADS);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-
-    // ---- tile range of this CTA (nnz-balanced, static)
-    const int G = gridDim.x, c = blockIdx.x;
-    const int64_t ntiles = (int64_t)((a.rows + C::R - 1) / C::R);
-    const uint64_t rend = a.rbase + a.rows;
-    const int64_t zb = a.rowptr[a.rbase];
-    const int64_t Z = a.rowptr[rend] - zb;
-    auto lower = [&](int64_t z) {
-        int64_t lo = 0, hi = ntiles;
-        while (lo < hi) {
-            int64_t mid = (lo + hi) >> 1;
-            uint64_t r = a.rbase + min((uint64_t)mid * C::R, a.rows);
-            if (a.rowptr[r] - zb >= z) hi = mid; else lo = mid + 1;
-        }
-        return lo;
-    };
-    const int64_t t0 = lower((Z * c) / G);
-    const int64_t t1 = (c == G - 1) ? ntiles : lower((Z * (c + 1)) / G);
-    const int ntl = (int)(t1 - t0);
-
-    if (role == 2) {
-        // ================================ producers (128 threads), software-pipelined:
-        // iteration j: records(j) landed -> gathers(j) into buffer j & 1 (after the group freed it) ->
-        // meta + records(j + 2) into slot (j + 2) % 3 (after tile j - 1's group freed it), with the
-        // rowptr slice of tile j + 3 prefetched into registers
-        const int ptid = tid - 2 * C::THREADS;
-        const uint64_t pol_stream = policy_evict_first();
-        const uint64_t pol_f = policy_evict_last();
-        constexpr int PA = KA / 2, PP = (KA + KB) / 2;
-        constexpr int RPI = C::THREADS / PP;
-        auto load_rp = [&](int jj, int64_t& lo, int64_t& hi) {  // rowptr slice of local tile jj (ptid < 32)
-            lo = hi = 0;
-            if (jj < ntl && ptid < C::R) {
-                const uint64_t r = a.rbase + (uint64_t)(t0 + jj) * C::R + ptid;
-                if (r < rend) {
-                    lo = a.rowptr[r];
-                    hi = a.rowptr[r + 1];
-                }
-            }
-        };
-        auto meta_records = [&](int jj, int64_t lo, int64_t hi) {  // meta + records of local tile jj -> slot jj % 3
-            const int rs = jj % 3;
-            if (ptid < 32) {  // lane r owns row r
-                const uint64_t r0 = a.rbase + (uint64_t)(t0 + jj) * C::R;
-                const int nr = (int)min((uint64_t)C::R, rend - r0);
-                const int len = (ptid < nr) ? ((hi - lo > kShortMax) ? -1 : (int)(hi - lo)) : 0;
-                const bool any_long = __any_sync(0xffffffffu, len < 0);
-                m_len(rs)[ptid] = len;
-                m_start(rs)[ptid] = lo;
-                __syncwarp();
-                const int* ln = m_len(rs);
-                const int me = max(len, 0);
-                int rank = 0, off = 0;
-                for (int r = 0; r < C::R; ++r) {
-                    const int o = max(ln[r], 0);
-                    rank += (o > me) || (o == me && r < ptid);
-                    off += (r < ptid) ? o : 0;
-                }
-                m_perm(rs)[rank] = ptid;
-                m_off(rs)[ptid] = off;
-                if (ptid == C::R - 1) {
-                    m_tot(rs)[0] = off + me;
-                    m_tot(rs)[1] = !any_long && off + me <= C::CAP;
-                }
-            }
-            nbar(3, C::THREADS);
-            const int total = m_tot(rs)[0];
-            if (m_tot(rs)[1]) {
-                const int64_t p0 = m_start(rs)[0];
-                const int64_t bx = p0 & ~(int64_t)1, bj = p0 & ~(int64_t)3;
-                const int nx = (int)((p0 + total - bx + 1) >> 1), nj = (int)((p0 + total - bj + 3) >> 2);
-                for (int q = ptid; q < nx; q += C::THREADS) cp16(rx(rs) + 2 * q, a.val + bx + 2 * q, pol_stream);
-                for (int q = ptid; q < nj; q += C::THREADS) {
-                    cp16(rj(rs) + 4 * q, a.ia + bj + 4 * q, pol_stream);
-                    cp16(rk(rs) + 4 * q, a.ib + bj + 4 * q, pol_stream);
-                }
-            } else {  // 4 producer threads per row
-                const int r = ptid & 31, sub = ptid >> 5;
-                const int len = max(m_len(rs)[r], 0), voff = m_off(rs)[r];
-                const int64_t pbase = m_start(rs)[r] - voff;
-                for (int v = voff + sub; v < voff + len; v += 4) {
-                    cp8(rx(rs) + v, a.val + pbase + v, pol_stream);
-                    cp4(rj(rs) + v, a.ia + pbase + v, pol_stream);
-                    cp4(rk(rs) + v, a.ib + pbase + v, pol_stream);
-                }
-            }
-            asm volatile("cp.async.commit_group;\n" ::: "memory");
-        };
-        int64_t lo, hi, nlo, nhi;
-        load_rp(0, lo, hi);
-        if (0 < ntl) meta_records(0, lo, hi);
-        load_rp(1, lo, hi);
-        if (1 < ntl) meta_records(1, lo, hi);
-        load_rp(2, nlo, nhi);
-        for (int j = 0; j < ntl; ++j) {
-            const int g = j & 1, u = j >> 1, rs = j % 3;
-            int64_t plo, phi;  // rowptr slice of tile j + 3
-            load_rp(j + 3, plo, phi);
-            if (j + 1 < ntl) asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // records(j); j + 1 may fly
-            else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-            nbar(3, C::THREADS);
-            if (u > 0) mbar_wait2(&bars[2 + g], (u - 1) & 1);  // gather buffer g: tile j - 2's Kronecker rows done
-            const int total = m_tot(rs)[0];
-            const int oj = m_tot(rs)[1] ? (int)(m_start(rs)[0] & 3) : 0;
-            if (ptid < RPI * PP) {
-                const int pc = ptid % PP;
-                const bool isa = pc < PA;
-                const double* fb = isa ? a.ua + 2 * pc : a.ub + 2 * (pc - PA);
-                const int kk = isa ? KA : KB;
-                const int off = isa ? 2 * pc : KA + 2 * (pc - PA);
-                const uint32_t* idxp = (isa ? rj(rs) : rk(rs)) + oj;
-                double* dst = sFb(g) + off;
-                if (isa ? a.l1_a : a.l1_b) {
-                    for (int e = ptid / PP; e < total; e += RPI)
-                        cp16_l1(dst + (size_t)e * C::FW, fb + (size_t)idxp[e] * kk, pol_f);
-                } else {
-                    for (int e = ptid / PP; e < total; e += RPI)
-                        cp16(dst + (size_t)e * C::FW, fb + (size_t)idxp[e] * kk, pol_f);
-                }
-            }
-            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(&bars[g]))
-                         : "memory");
-            if (j + 2 < ntl) {
-                // slot (j + 2) % 3 held tile j - 1: its group must be done with that tile's records (x)
-                if (j >= 1) mbar_wait2(&bars[2 + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
-                meta_records(j + 2, nlo, nhi);
-            }
-            nlo = plo;
-            nhi = phi;
-        }
-        return;
-    }
-
-    // ================================ consumer group `role` (128 threads)
-    const int g = role, gtid = tid - g * C::THREADS, gw = warp - 4 * g;
-    double* sF = sFb(g);
-    double* sY = sYb + (size_t)g * C::R * C::LDY;
-    double* sA = sAb + (size_t)g * C::R * C::ALD;
-    int* vmask = vmaskb + g * C::R;
-    const int gbar = 1 + g;
-    for (int q = gtid; q < C::R * C::ALD; q += C::THREADS) sA[q] = 0.0;
-
-    double macc[C::MBW][2];
-#pragma unroll
-    for (int b = 0; b < C::MBW; ++b) macc[b][0] = macc[b][1] = 0.0;
-    constexpr int NWB = C::NT * (C::NT + 1) / 2;
-    const int wmA = (C::NT == 1 || gw < 2) ? 0 : 1, wmB = (C::NT == 1 || gw == 0) ? 0 : 1;
-    double wfr0 = 0.0, wfr1 = 0.0;
-    double mx = 0.0;
-    const double* __restrict__ gt = a.gt;
-    constexpr bool kGReg = C::L / 4 <= 32;
-    double gfr[kGReg ? C::L / 4 : 1];
-    const int gcolidx = (gw % C::NT) * 8 + (lane >> 2);
-    const bool gvalid = a.kind == kTTMcTC && gcolidx < KN;
-    if constexpr (kGReg) {
-#pragma unroll
-        for (int ks = 0; ks < C::L / 4; ++ks)
-            gfr[ks] = gvalid ? __ldg(gt + (size_t)(ks * 4 + (lane & 3)) * KN + gcolidx) : 0.0;
-    }
-    const int rslot = gw * C::RPW + lane / C::TR;
-    const int pb = (lane % C::TR) / C::TQ, qb = lane % C::TQ;
-    const int p0 = pb * C::BP, q0 = qb * C::BQ;
-
-    for (int j = g; j < ntl; j += 2) {
-        const int u = j >> 1;
-        mbar_wait2(&bars[g], u & 1);
-        const int rs = j % 3;
-        const uint64_t r0 = a.rbase + (uint64_t)(t0 + j) * C::R;
-        const int nr = (int)min((uint64_t)C::R, rend - r0);
-        const int lr = m_perm(rs)[rslot];
-        const int len = max(m_len(rs)[lr], 0);
-        const int voff = m_off(rs)[lr];
-        const double* recx = rx(rs) + (m_tot(rs)[1] ? (int)(m_start(rs)[0] & 1) : 0);
-        double acc[C::BP][C::BQ];
-#pragma unroll
-        for (int p = 0; p < C::BP; ++p)
-#pragma unroll
-            for (int q = 0; q < C::BQ; ++q) acc[p][q] = 0.0;
-#pragma unroll 2
-        for (int e = voff; e < voff + len; ++e) {
-            const double x = recx[e];
-            const double* f = sF + (size_t)e * C::FW;
-            double sa[C::BP], vb[C::BQ];
-            lds_block<C::BP>(f, p0, sa);
-            lds_block<C::BQ>(f + KA, q0, vb);
-#pragma unroll
-            for (int p = 0; p < C::BP; ++p) {
-                const double sx = x * sa[p];
-#pragma unroll
-                for (int q = 0; q < C::BQ; ++q) acc[p][q] = fma(sx, vb[q], acc[p][q]);
-            }
-        }
-        {
-            double* y = sY + (size_t)lr * C::LDY;
-#pragma unroll
-            for (int p = 0; p < C::BP; ++p)
-#pragma unroll
-                for (int q = 0; q < C::BQ; ++q) y[blk_index<C::BP>(p0, p) * KB + blk_index<C::BQ>(q0, q)] = acc[p][q];
-            if (C::LP > C::L && pb == 0 && qb == 0)
-                for (int l = C::L; l < C::LP; ++l) y[l] = 0.0;
-        }
-        if (gtid < C::R) vmask[gtid] = gtid < nr && m_len(rs)[gtid] >= 0;
-        nbar(gbar, C::THREADS);
-        mbar_arrive2(&bars[2 + g]);  // the buffer (rows, records, meta) is free for the producers
-        if (a.kind == kTTMcTC) {
-            const int nt = gw % C::NT;
-            constexpr int KSN = C::L / 4;
-            double cc[C::ABW][2][2];
-#pragma unroll
-            for (int bi = 0; bi < C::ABW; ++bi) cc[bi][0][0] = cc[bi][0][1] = cc[bi][1][0] = cc[bi][1][1] = 0.0;
-#pragma unroll
-            for (int ks = 0; ks < KSN; ++ks)
-#pragma unroll
-                for (int bi = 0; bi < C::ABW; ++bi) {
-                    const int b = gw + bi * C::WARPS;
-                    if (b < C::AB) {
-                        const int mt = b / C::NT;
-                        const double yv = sY[(size_t)(mt * 8 + (lane >> 2)) * C::LDY + (lane & 3) + ks * 4];
-                        double gv;
-                        if constexpr (kGReg)
-                            gv = gfr[ks];
-                        else
-                            gv = gvalid ? __ldg(gt + (size_t)(ks * 4 + (lane & 3)) * KN + gcolidx) : 0.0;
-                        dmma884(cc[bi][ks & 1][0], cc[bi][ks & 1][1], yv, gv);
-                    }
-                }
-#pragma unroll
-            for (int bi = 0; bi < C::ABW; ++bi) {
-                const int b = gw + bi * C::WARPS;
-                if (b < C::AB) {
-                    const int mt = b / C::NT;
-                    const int row = mt * 8 + (lane >> 2);
-                    const int col = nt * 8 + 2 * (lane & 3);
-                    const bool valid = vmask[row] != 0;
-                    const double v0 = valid ? cc[bi][0][0] + cc[bi][1][0] : 0.0;
-                    const double v1 = valid ? cc[bi][0][1] + cc[bi][1][1] : 0.0;
-                    sA[row * C::ALD + col] = v0;
-                    sA[row * C::ALD + col + 1] = v1;
-                    mx = fmax(mx, fmax(fabs(v0), fabs(v1)));
-                    if (valid && a.A && col < KN) {
-                        double* dst = a.A + (r0 + row) * KN + col;
-                        if constexpr (KN % 2 == 0)
-                            *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
-                        else {
-                            dst[0] = v0;
-                            if (col + 1 < KN) dst[1] = v1;
-                        }
-                    }
-                }
-            }
-        } else {
-            for (int q = gtid; q < C::R * KN; q += C::THREADS) {
-                const int row = q / KN, r = q - row * KN;
-                const double v = vmask[row] ? a.un[(r0 + row) * KN + r] : 0.0;
-                sA[row * C::ALD + r] = v;
-                mx = fmax(mx, fabs(v));
-            }
-        }
-        nbar(gbar, C::THREADS);
-#pragma unroll
-        for (int ks = 0; ks < C::R / 4; ++ks)
-#pragma unroll
-            for (int bi = 0; bi < C::MBW; ++bi) {
-                const int b = gw + bi * C::WARPS;
-                if (b < C::MB) {
-                    const int mt = b / C::NLT, nt = b - mt * C::NLT;
-                    const double av = sA[(size_t)(ks * 4 + (lane & 3)) * C::ALD + mt * 8 + (lane >> 2)];
-                    const double yv = sY[(size_t)(ks * 4 + (lane & 3)) * C::LDY + nt * 8 + (lane >> 2)];
-                    dmma884(macc[bi][0], macc[bi][1], av, yv);
-                }
-            }
-        if (gw < NWB) {
-#pragma unroll
-            for (int ks = 0; ks < C::R / 4; ++ks) {
-                const double* ar = sA + (size_t)(ks * 4 + (lane & 3)) * C::ALD + (lane >> 2);
-                dmma884(wfr0, wfr1, ar[wmA * 8], ar[wmB * 8]);
-            }
-        }
-        nbar(gbar, C::THREADS);  // Y / A tiles free for the next tile of this group
-    }
-
-    // ---- partial slot c = group 0 + group 1 (fixed order); slot c + G zeroed
-    double* scr = sYb;  // group 0's Y tile: M partial of group 1 (KN x L), then W (KN x KN)
-    nbar(4, 2 * C::THREADS);
-    const int slot = a.slot0 + c;
-    double* mp = a.mpart + (size_t)slot * KN * C::L;
-    double* wp = a.wpart + (size_t)slot * KN * KN;
-    if (g == 1) {
-#pragma unroll
-        for (int bi = 0; bi < C::MBW; ++bi) {
-            const int b = gw + bi * C::WARPS;
-            if (b < C::MB) {
-                const int mt = b / C::NLT, nt = b - mt * C::NLT;
-                const int r = mt * 8 + (lane >> 2), l = nt * 8 + 2 * (lane & 3);
-                if (r < KN) {
-                    if (l < C::L) scr[(size_t)r * C::L + l] = macc[bi][0];
-                    if (l + 1 < C::L) scr[(size_t)r * C::L + l + 1] = macc[bi][1];
-                }
-            }
-        }
-        if (gw < NWB) {
-            const int r = wmA * 8 + (lane >> 2), c0 = wmB * 8 + 2 * (lane & 3);
-            const double v[2] = {wfr0, wfr1};
-#pragma unroll
-            for (int e = 0; e < 2; ++e)
-                if (r < KN && c0 + e < KN) {
-                    scr[KN * C::L + r * KN + c0 + e] = v[e];
-                    if (wmA != wmB) scr[KN * C::L + (c0 + e) * KN + r] = v[e];
-                }
-        }
-    }
-    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
-    if (lane == 0) redmax[warp] = mx;
-    nbar(4, 2 * C::THREADS);
-    if (g == 0) {
-#pragma unroll
-        for (int bi = 0; bi < C::MBW; ++bi) {
-            const int b = gw + bi * C::WARPS;
-            if (b < C::MB) {
-                const int mt = b / C::NLT, nt = b - mt * C::NLT;
-                const int r = mt * 8 + (lane >> 2), l = nt * 8 + 2 * (lane & 3);
-                if (r < KN) {
-                    if (l < C::L) mp[(size_t)r * C::L + l] = macc[bi][0] + scr[(size_t)r * C::L + l];
-                    if (l + 1 < C::L) mp[(size_t)r * C::L + l + 1] = macc[bi][1] + scr[(size_t)r * C::L + l + 1];
-                }
-            }
-        }
-        if (gw < NWB) {
-            const int r = wmA * 8 + (lane >> 2), c0 = wmB * 8 + 2 * (lane & 3);
-            const double v[2] = {wfr0, wfr1};
-#pragma unroll
-            for (int e = 0; e < 2; ++e)
-                if (r < KN && c0 + e < KN) {
-                    wp[r * KN + c0 + e] = v[e] + scr[KN * C::L + r * KN + c0 + e];
-                    if (wmA != wmB) wp[(c0 + e) * KN + r] = v[e] + scr[KN * C::L + (c0 + e) * KN + r];
-                }
-        }
-        if (tid == 0) {
-            double m = 0.0;
-            for (int w = 0; w < 8; ++w) m = fmax(m, redmax[w]);
-            a.maxpart[slot] = m;
-        }
-    } else {  // zero the second half of the slots (the dispatcher reduces 2 x gridDim.x slots)
-        double* mz = a.mpart + (size_t)(slot + G) * KN * C::L;
-        double* wz = a.wpart + (size_t)(slot + G) * KN * KN;
-        for (int q = gtid; q < KN * C::L; q += C::THREADS) mz[q] = 0.0;
-        for (int q = gtid; q < KN * KN; q += C::THREADS) wz[q] = 0.0;
-        if (gtid == 0) a.maxpart[slot + G] = 0.0;
-    }
-}
-
-// ============================================================================
-// Three-CTAs-per-SM pass (default for K = 10; HQ_PASS_NP=0 turns it off): no intra-CTA pipelining -- a tile's
+// Three-CTAs-per-SM pass (K = 10): no intra-CTA pipelining -- a tile's
 // meta, records, gathers and Kronecker rows run in sequence and the Y tile is
 // written over the staged rows -- so a CTA needs ~74 KB of shared memory and
 // twelve compute warps share an SM (three independent CTAs overlap each
@@ -1696,92 +887,35 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
     }
 }
 
-bool np_pass_enabled();
-
 template <int KA, int KB, int KN>
 void launch_fast3(const FastArgs& a, int grid, cudaStream_t s) {
-    using C = Cfg<KA, KB, KN>;
-    using W = WsCfg<KA, KB, KN>;
-    if constexpr (KA == 10 && KB == 10 && KN == 10) {
-        if (np_pass_enabled()) {  // grid = 3 CTAs per SM (fast_grid), one partial slot per CTA
-            using CN = CfgNP<KA, KB, KN>;
-            static bool attr3 = false;
-            if (!attr3) {
-                HQ_CUDA(cudaFuncSetAttribute(k_pass_np3<KA, KB, KN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)CN::smem));
-                attr3 = true;
-            }
-            k_pass_np3<KA, KB, KN><<<grid, 128, CN::smem, s>>>(a);
-            HQ_CHECK_LAUNCH();
-            return;
+    if constexpr (KA == 10 && KB == 10 && KN == 10) {  // grid = 3 CTAs per SM (fast_grid), one partial slot per CTA
+        using CN = CfgNP<KA, KB, KN>;
+        static bool attr3 = false;
+        if (!attr3) {
+            HQ_CUDA(cudaFuncSetAttribute(k_pass_np3<KA, KB, KN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)CN::smem));
+            attr3 = true;
         }
-        // HQ_PASS_WS2=1 selects the warp-specialised pass (read per launch; a captured sweep graph keeps the
-        // kernel chosen at capture).  Measured equal to the default on config 2 (0.75 ms per pass either way:
-        // both sit at the random-sector DRAM rate of the factor gathers), so the simpler kernel is the default.
-        const char* e = std::getenv("HQ_PASS_WS2");
-        const bool ws2 = e && e[0] == '1';
-        if (ws2 && a.tiles_fit && grid >= 2 * num_sms()) {
-            using W2 = WS2<KA, KB, KN>;
-            static bool attr2 = false;
-            if (!attr2) {
-                HQ_CUDA(cudaFuncSetAttribute(k_pass_ws2<KA, KB, KN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)W2::smem));
-                attr2 = true;
-            }
-            k_pass_ws2<KA, KB, KN><<<num_sms(), W2::THREADS, W2::smem, s>>>(a);
-            HQ_CHECK_LAUNCH();
-            return;
+        k_pass_np3<KA, KB, KN><<<grid, 128, CN::smem, s>>>(a);
+        HQ_CHECK_LAUNCH();
+        return;
+    } else {  // K = 16 / 8: the software-pipelined two-CTAs-per-SM kernel
+        using C = Cfg<KA, KB, KN>;
+        static bool attr = false;
+        if (!attr) {
+            HQ_CUDA(cudaFuncSetAttribute(k_pass_fast3<KA, KB, KN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)C::smem_bytes));
+            attr = true;
         }
+        k_pass_fast3<KA, KB, KN><<<grid, C::THREADS, C::smem_bytes, s>>>(a);
+        HQ_CHECK_LAUNCH();
     }
-    // default: the software-pipelined kernel; HQ_PASS_WS=1 selects the warp-specialised variant
-    // (producer warp + 4 consumer warps; measured slower on B200 so far: 1.01 vs 0.84 ms per config-2 pass)
-    static const bool v3 = [] {
-        const char* e = std::getenv("HQ_PASS_WS");
-        return !(e && e[0] == '1');
-    }();
-    auto fn = v3 ? k_pass_fast3<KA, KB, KN> : k_pass_ws3<KA, KB, KN>;
-    const size_t smem = v3 ? C::smem_bytes : W::smem_bytes;
-    static bool attr = false;
-    if (!attr) {
-        HQ_CUDA(cudaFuncSetAttribute(k_pass_fast3<KA, KB, KN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)C::smem_bytes));
-        HQ_CUDA(cudaFuncSetAttribute(k_pass_ws3<KA, KB, KN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)W::smem_bytes));
-        attr = true;
-    }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(v3 ? C::THREADS : W::THREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr_l2[1];
-    if (a.l2_bytes) {
-        attr_l2[0].id = cudaLaunchAttributeAccessPolicyWindow;
-        attr_l2[0].val.accessPolicyWindow.base_ptr = const_cast<double*>(a.ua);
-        attr_l2[0].val.accessPolicyWindow.num_bytes = a.l2_bytes;
-        attr_l2[0].val.accessPolicyWindow.hitRatio = a.l2_hit;
-        attr_l2[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        attr_l2[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        cfg.attrs = attr_l2;
-        cfg.numAttrs = 1;
-    }
-    HQ_CUDA(cudaLaunchKernelEx(&cfg, fn, a));
-}
-
-// the three-CTAs-per-SM pass is the default for K = 10 (config 2: 0.75 -> 0.68 ms per pass); HQ_PASS_NP=0
-// selects the software-pipelined two-CTAs-per-SM kernel (read once: it sets the slot count)
-bool np_pass_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("HQ_PASS_NP");
-        return !(e && e[0] == '0');
-    }();
-    return on;
 }
 
 template <int KA, int KB, int KN>
 int grid_fast3() {
-    if constexpr (KA == 10 && KB == 10 && KN == 10)
-        if (np_pass_enabled()) return num_sms() * HQ_NP_MINB;
+    if constexpr (KA == 10 && KB == 10 && KN == 10) return num_sms() * HQ_NP_MINB;
     return num_sms() * Cfg<KA, KB, KN>::MINB;
 }
 
@@ -1800,20 +934,6 @@ void debug_phase_cycles(unsigned long long* out, int) {
     for (int i = 0; i < 16; ++i) out[i] = 0;
 }
 #endif
-
-size_t l2_persist_budget() {
-    static size_t budget = [] {
-        int dev = 0, v = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess || v <= 0) return (size_t)0;
-        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)v) != cudaSuccess) {
-            cudaGetLastError();
-            return (size_t)0;
-        }
-        return (size_t)v;
-    }();
-    return budget;
-}
 
 int fast_grid(int ka, int kb, int kn) {
     if (ka == 10 && kb == 10 && kn == 10) return grid_fast3<10, 10, 10>();

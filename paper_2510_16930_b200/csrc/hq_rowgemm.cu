@@ -433,11 +433,7 @@ void launch_rg(const double* A, uint64_t rows, const double* T, double* out, con
                double* maxpart, const DevStatus* st, int run_if, cudaStream_t s) {
     // bulk copies need 16-byte aligned sources (a row-range slice of A in the multi-GPU path may start
     // mid-unit): those take the register-staged kernel
-    static const bool force_ld = [] {
-        const char* e = std::getenv("HQ_RG_LD");
-        return e && e[0] == '1';
-    }();
-    const bool aligned = !force_ld && (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
+    const bool aligned = (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
                          (!other || reinterpret_cast<uintptr_t>(other) % 16 == 0);
     if (aligned) {
         using C = RT<K>;

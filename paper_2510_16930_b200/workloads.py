@@ -9,7 +9,8 @@ them by summing, exactly as the reference's ``SparseTensor`` does
 
 Generation is numpy (PCG64, fixed seeds), so every machine produces the same
 arrays.  Config 4 (planted model) evaluates its model entries with torch on
-the GPU when one is present, in float64.
+the GPU when one is present, in float64, in an operation order that makes
+the numpy and torch results bit-identical.
 """
 from __future__ import annotations
 
@@ -70,55 +71,68 @@ def planted_coo(dims, draws, ranks, seed, noise=0.01, device=None):
     n = len(dims)
     factors = []
     for d, k in zip(dims, ranks):
-        q, r = np.linalg.qr(rng.standard_normal((d, k)))
-        q *= np.sign(np.diag(r))[None, :]
-        factors.append(np.ascontiguousarray(q))
+        factors.append(_mgs2(rng.standard_normal((d, k))))
     core = rng.standard_normal(tuple(ranks))
     coords = np.empty((draws, n), dtype=np.uint32)
     for m, d in enumerate(dims):
         coords[:, m] = rng.integers(0, d, size=draws, dtype=np.uint32)
     model = _model_entries(coords, factors, core, device)
-    rms = float(np.sqrt(np.mean(model * model))) if draws else 0.0
+    rms = float(np.sqrt((model * model).sum() / draws)) if draws else 0.0
     vals = model + noise * rms * rng.standard_normal(draws)
     return coords, vals, factors, core
 
 
+def _mgs2(a):
+    """Orthonormal columns by modified Gram-Schmidt, twice (positive R
+    diagonal).  Only elementwise ops and numpy's pairwise ``sum`` (plain C, no
+    CPU-dispatched BLAS), so every host produces the same bits."""
+    q = np.array(a, np.float64).T.copy()  # columns as contiguous rows
+    for _ in range(2):
+        for j in range(q.shape[0]):
+            for i in range(j):
+                q[j] -= (q[i] * q[j]).sum() * q[i]
+            q[j] /= np.sqrt((q[j] * q[j]).sum())
+    return np.ascontiguousarray(q.T)
+
+
 def _model_entries(coords, factors, core, device):
+    """Tucker model entries sum_{p,q,r} G[p,q,r] U1[i,p] U2[j,q] U3[k,r] in a
+    FIXED sequence of elementwise IEEE multiplies and adds (no BLAS, no fused
+    multiply-add, no library reductions), so numpy on any host and torch on
+    the GPU produce bit-identical values: the parity fixtures made from the
+    reference on the build host and the GPU tests see the same tensor."""
+    xp, conv = np, (lambda a: a)
     try:
         import torch
+        if device is not None or torch.cuda.is_available():
+            dev = device or "cuda"
+            xp = torch
+            conv = (lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev))
     except Exception:  # pragma: no cover
-        torch = None
-    if torch is not None and (device is not None or torch.cuda.is_available()):
-        dev = device or "cuda"
-        g = torch.as_tensor(core, device=dev)
-        us = [torch.as_tensor(u, device=dev) for u in factors]
-        out = np.empty(coords.shape[0])
-        chunk = 1 << 20
-        for b in range(0, coords.shape[0], chunk):
-            c = torch.as_tensor(coords[b:b + chunk].astype(np.int64), device=dev)
-            t = g
-            rows = [u[c[:, m]] for m, u in enumerate(us)]
-            t = torch.einsum("pqr,np,nq,nr->n", g, *rows) if len(us) == 3 else _einsum_n(torch, g, rows)
-            out[b:b + chunk] = t.cpu().numpy()
-        return out
+        pass
+    g = np.asarray(core, np.float64)
     out = np.empty(coords.shape[0])
-    chunk = 1 << 16
+    chunk = (1 << 24) if xp is not np else (1 << 20)
     for b in range(0, coords.shape[0], chunk):
-        rows = [u[coords[b:b + chunk, m]] for m, u in enumerate(factors)]
-        t = core
-        # contract one mode at a time, batch dim first
-        t = np.einsum("p...,np->n...", t, rows[0])
-        for r in rows[1:]:
-            t = np.einsum("np...,np->n...", t, r)
-        out[b:b + chunk] = t
+        rows = [conv(u[coords[b:b + chunk, m]].T.copy()) for m, u in enumerate(factors)]  # (K_m, n) each
+        t = _contract(g, rows)
+        out[b:b + chunk] = t.cpu().numpy() if xp is not np else t
     return out
 
 
-def _einsum_n(torch, g, rows):
-    t = torch.einsum("p...,np->n...", g, rows[0])
-    for r in rows[1:]:
-        t = torch.einsum("np...,np->n...", t, r)
-    return t
+def _contract(g, rows):
+    """value = sum_{k0} r0[k0] * (sum_{k1} r1[k1] * (... sum_{kl} g[k0..kl] * rl[kl]))
+    with each sum taken left to right, one rounding per multiply and per add."""
+    if g.ndim == 1:
+        acc = rows[0][0] * float(g[0])
+        for k in range(1, g.shape[0]):
+            acc = acc + rows[0][k] * float(g[k])
+        return acc
+    acc = None
+    for k in range(g.shape[0]):
+        term = rows[0][k] * _contract(g[k], rows[1:])
+        acc = term if acc is None else acc + term
+    return acc
 
 
 def config_coo(cfg_id, seed=None, scale=1.0):

@@ -122,56 +122,29 @@ def test_long_rows_fast_matches_oracle_and_generic(order, k):
         assert np.abs(a - b).max() <= 1e-12 * np.abs(b).max()
 
 
-@pytest.mark.parametrize("skew", [False, True])
-def test_warp_specialised_pass_matches_oracle(skew):
-    """HQ_PASS_WS2=1: the producer/consumer pass (hq_pass_fast.cu k_pass_ws2) -- same results as the default
-    kernel up to summation order, and against the oracle."""
-    from oracle_bind import Oracle
-    o = Oracle()
-    dims = [20000, 15000, 10000]  # 5-10 nonzeros per row: every 32-row tile fits the 416-record buffer
-    x, u = _case(dims, 100000, 10, 31, skew)
-    assert all(x.mode_plan(m)["max_tile32"] <= 416 for m in range(3))  # so the WS2 kernel runs every mode
-    core = hq.ttmc_core(x, u)
-    base = [hq.ttmctc_elementwise(x, u, m, core) for m in range(3)]
-    os.environ["HQ_PASS_WS2"] = "1"
-    try:
-        core2 = hq.ttmc_core(x, u)
-        ws2 = [hq.ttmctc_elementwise(x, u, m, core) for m in range(3)]
-        ws2b = [hq.ttmctc_elementwise(x, u, m, core) for m in range(3)]
-    finally:
-        os.environ.pop("HQ_PASS_WS2", None)
-    oc = o.ttmc_core(dims, [10] * 3, x.coords(), x.values(), u.factors).reshape(-1)
-    assert np.abs(core2.data - oc).max() <= 1e-11 * max(1.0, np.abs(oc).max())
-    for m in range(3):
-        ao = o.ttmctc(dims, [10] * 3, x.coords(), x.values(), u.factors, m, core.data)
-        tol = 1e-11 * max(1.0, np.abs(ao).max())
-        assert np.abs(ws2[m] - ao).max() <= tol and np.abs(base[m] - ao).max() <= tol, m
-        assert (ws2[m] == ws2b[m]).all()  # bitwise repeatable
-
-
-def test_two_cta_pass_k10_matches_oracle_in_subprocess():
-    """HQ_PASS_NP=0 (read once per process: it sets the slot count) -- the two-CTA software-pipelined K = 10
-    kernel, which the three-CTA default replaced, still matches the oracle."""
+@pytest.mark.parametrize("variant", ["0", "1"])
+def test_long_row_segment_variants_in_subprocess(variant):
+    """HQ_LONG_SYNC=0/1 (read once per process): the pipelined (k_longseg_mma) and the synchronous
+    (k_longseg_sync) long-row segment kernels, each on every long-row shape, against the oracle."""
     import subprocess, sys, textwrap
     code = textwrap.dedent("""
         import sys, numpy as np
         sys.path.insert(0, '.'); sys.path.insert(0, 'tests')
         import paper_2510_16930_b200 as hq
         from oracle_bind import Oracle
-        from paper_2510_16930_b200.workloads import uniform_coo
-        dims = [20000, 15000, 10000]
-        coords, vals = uniform_coo(dims, 100000, 41)
-        x = hq.SparseTensor(dims, coords, vals)
-        u = hq.random_factors(dims, [10] * 3, 42)
-        core = hq.ttmc_core(x, u)
+        from test_gpu_fast import _long_case
         o = Oracle()
-        for m in range(3):
-            a = hq.ttmctc_elementwise(x, u, m, core)
-            ao = o.ttmctc(dims, [10] * 3, x.coords(), x.values(), u.factors, m, core.data)
-            assert np.abs(a - ao).max() <= 1e-11 * max(1.0, np.abs(ao).max()), m
+        for order, k in [(3, 10), (3, 16), (3, 8), (4, 8)]:
+            dims, x, u = _long_case(order, k, 171 + k + order)
+            ranks = [k] * order
+            core = hq.ttmc_core(x, u)
+            for m in range(order):
+                a = hq.ttmctc_elementwise(x, u, m, core)
+                ao = o.ttmctc(dims, ranks, x.coords(), x.values(), u.factors, m, core.data)
+                assert np.abs(a - ao).max() <= 1e-11 * max(1.0, np.abs(ao).max()), (order, k, m)
         print("ok")
     """)
-    env = dict(os.environ, HQ_PASS_NP="0")
+    env = dict(os.environ, HQ_LONG_SYNC=variant)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr

@@ -13,9 +13,12 @@ engine arm: `value` = sweeps/s with every operand resident in HBM, timed with
 CUDA events on the solver's stream; `e2e` = the same metric through the public
 API (SparseTensor build from pinned host COO + hoqri() with host init factors,
 results copied back), `roofline` for the dominant kernel (the fused sparse
-mode pass), `cpu_baseline` = the reference library (oracle/_ref) timed on the
-host on a bounded sample.  reference arm: the reference CPU implementation on
-all host threads (rank 0 only).
+mode pass), `ttmctc` = SURVEY 8(d)'s standalone TTMcTC nnz/s, `sweep_roofline`
+= the sweep against SURVEY 8(d)'s canonical T_iter, `cpu_baseline` = one
+full-size mode update of the unmodified reference (oracle/_ref), 1 thread.
+reference arm (rank 0 only): K full-size mode updates of the unmodified
+reference's solve loop, each timed as it runs.  `--gpus N` without torchrun
+re-launches itself with N ranks.
 """
 from __future__ import annotations
 
@@ -47,7 +50,6 @@ def parse():
     p.add_argument("--config", type=int, default=CONFIG_ID)
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--cpu-sample", type=int, default=1_000_000)
     return p.parse_args()
 
 
@@ -188,45 +190,47 @@ def measured_peaks():
 
 
 # --------------------------------------------------------------- CPU side --
-def cpu_reference_sample(x_coords, x_vals, dims, ranks, factors, core, sample, threads, reps=1):
-    """Times the UNMODIFIED reference kernels (oracle/_ref) on the first
-    `sample` lexicographic nonzeros, split over `threads` host threads, and the
-    reference QR at full size once.  Returns per-sweep seconds extrapolated to
-    the full nnz, plus the pieces."""
-    from oracle_bind import RefLib, RefTensor, Oracle
-    nnz = x_vals.size
-    S = min(sample, nnz)
-    if RefLib.available():
-        lib = RefLib()
-        kind = "reference"
-        t = RefTensor.create(lib, dims, x_coords[:S], x_vals[:S])
-        sl = lib.L.ref_slices_create(t.h, threads)
-        fl = np.ascontiguousarray(np.concatenate([f.reshape(-1) for f in factors]))
-        rk = np.asarray(ranks, np.uint64)
-        cd = np.ascontiguousarray(core.reshape(-1))
-        t_ttm = min(lib.L.ref_slices_time(sl, rk, fl, cd, 0, 0, 1) for _ in range(reps))
-        t_core = min(lib.L.ref_slices_time(sl, rk, fl, cd, 0, 1, 1) for _ in range(reps))
-        lib.L.ref_slices_destroy(sl)
-        a = np.ascontiguousarray(factors[0])
-        t_qr = lib.L.ref_time_qr(a.shape[0], a.shape[1], a.reshape(-1), 1)
-    else:  # the C restatement (oracle/hq_oracle.c), single thread
-        o = Oracle()
-        kind = "port"
-        threads = 1
-        t0 = time.perf_counter()
-        o.ttmctc(dims, ranks, x_coords[:S], x_vals[:S], factors, 0, core)
-        t_ttm = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        o.ttmc_core(dims, ranks, x_coords[:S], x_vals[:S], factors)
-        t_core = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        o.qr(factors[0])
-        t_qr = time.perf_counter() - t0
+def cpu_baseline_measure(coords, vals, dims, ranks, factors):
+    """cpu_baseline: ONE full-size mode update (mode 0) of the reference's solve
+    loop, timed as it runs (oracle/_ref, 1 thread; see reference_mode_updates);
+    sweep = N x that (the configs' modes have equal nnz; the reference arm times
+    every mode).  Without oracle/_ref: the C restatement (oracle/hq_oracle.c) of
+    the same calls at full size ("port")."""
+    from oracle_bind import RefLib, Oracle
     N = len(dims)
-    scale = nnz / S
-    sweep_s = N * ((t_ttm + t_core) * scale + t_qr)
-    return dict(kind=kind, threads=threads, sample=S, t_ttm=t_ttm, t_core=t_core, t_qr=t_qr, sweep_s=sweep_s,
-                ttmctc_nnz_per_s=S / t_ttm)
+    if RefLib.available():
+        r = reference_mode_updates(coords, vals, dims, ranks, factors, 1, 0)
+        t = r["steps_s"][0]
+        return dict(kind="reference", sweep_s=N * t, step_s=t, phases=r["phases"][0], nnz=r["nnz"],
+                    ttmctc_nnz_per_s=r["nnz"] / r["phases"][0]["ttmctc"])
+    o = Oracle()
+    t0 = time.perf_counter()
+    core = o.ttmc_core(dims, ranks, coords, vals, factors)
+    t1 = time.perf_counter()
+    a = o.ttmctc(dims, ranks, coords, vals, factors, 0, core)
+    t2 = time.perf_counter()
+    o.qr(a)
+    t3 = time.perf_counter()
+    t = t3 - t0
+    return dict(kind="port", sweep_s=N * t, step_s=t, nnz=len(vals),
+                phases={"ttmctc": t2 - t1, "qr": t3 - t2, "core": t1 - t0}, ttmctc_nnz_per_s=len(vals) / (t2 - t1))
+
+
+def sweep_roofline(solver, dims, ranks, nnz, bw_gbs, p64_tflops):
+    """T_iter,roof = sum_n [T(TTMcTC_n) + T(core_n) + T(QR_n)],
+    T = max(B / BW, F / P64) with the canonical (minimal) F and B."""
+    N = len(dims)
+    bw, p64 = bw_gbs * 1e9, p64_tflops * 1e12
+    tot, parts = 0.0, []
+    for n in range(N):
+        f, b = solver.ttmctc_work(n)  # F = 2 nnz L + 2 R_n prod K, B = nnz(4N+8) + 8 sum_{v!=n} I_v K_v + 8 I_n K_n
+        t_ttm = max(b / bw, f / p64)
+        b_core = b - 8.0 * dims[n] * ranks[n] + 8.0 * dims[n] * ranks[n] + 8.0 * float(np.prod(ranks))
+        t_core = max(b_core / bw, f / p64)
+        t_qr = max(24.0 * dims[n] * ranks[n] / bw, 8.0 * dims[n] * ranks[n] ** 2 / p64)
+        parts.append({"ttmctc_us": t_ttm * 1e6, "core_us": t_core * 1e6, "qr_us": t_qr * 1e6})
+        tot += t_ttm + t_core + t_qr
+    return tot, parts
 
 
 def host_desc():
@@ -238,61 +242,75 @@ def host_desc():
 
 
 # ------------------------------------------------------------------ arms --
+def reference_mode_updates(coords, vals, dims, ranks, factors, steps, warmup, sample_warm=100_000):
+    """The UNMODIFIED reference (oracle/_ref) on the GPU box's host: `steps`
+    full-size mode updates of tucker::hoqri's loop (ref_capi.cpp
+    ref_state_mode_update: ttmctc_elementwise with the fresh core, max_abs,
+    qr_orthonormal, subspace_distance, ttmc_core -- solvers.cpp:86-146), mode
+    n = step mod N, one thread.  Nothing is sampled or extrapolated: each step
+    is timed as it runs.  The `warmup` steps run on a prefix of the nonzeros
+    (they only fault pages in).  Returns per-step seconds and phase times."""
+    from oracle_bind import RefLib, RefTensor, RefSolveState
+    lib = RefLib()
+    N = len(dims)
+    if warmup:
+        tw = RefTensor.create(lib, dims, coords[:sample_warm], vals[:sample_warm])
+        sw = RefSolveState(tw, ranks, factors)
+        for i in range(warmup):
+            sw.mode_update(i % N)
+        del sw, tw
+    t0 = time.perf_counter()
+    t = RefTensor.create(lib, dims, coords, vals)  # the reference's SparseTensor ctor (sort + merge + buckets)
+    t_build = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    st = RefSolveState(t, ranks, factors)  # initial core, solvers.cpp:66
+    t_init = time.perf_counter() - t0
+    steps_s, phases = [], []
+    for i in range(steps):
+        t0 = time.perf_counter()
+        _, ph = st.mode_update(i % N)
+        steps_s.append(time.perf_counter() - t0)
+        phases.append(ph)
+    return dict(steps_s=steps_s, phases=phases, t_build=t_build, t_init=t_init, nnz=t.nnz)
+
+
 def run_reference(args, ws, rank):
+    """--impl reference: the reference's own CPU implementation of the path
+    (oracle/_ref = the unmodified reference library), rank 0 only.  A step is
+    ONE full-size mode update of the reference's solve loop (1/N of a sweep);
+    value = sweeps/s = K / (N x the K steps' wall time)."""
     if rank != 0:
         return
     c, coords, vals = workload(args.config)
-    from oracle_bind import Oracle
-    o = Oracle()
-    oc, ov = o.normalize(c["dims"], coords, vals) if len(vals) <= 2_000_000 else _merge_numpy(coords, vals)
-    factors = _numpy_orthonormal(c["dims"], c["ranks"])
-    core = np.random.default_rng(1).standard_normal(int(np.prod(c["ranks"])))
-    threads = os.cpu_count() or 1
-    sample = max(1, min(args.cpu_sample * max(1, threads // 2), ov.size))
-    res = []
-    for i in range(args.warmup + args.steps):
-        r = cpu_reference_sample(oc, ov, list(c["dims"]), list(c["ranks"]), factors, core, sample, threads)
-        if i >= args.warmup:
-            res.append(r)
-    sweep_s = statistics.median(r["sweep_s"] for r in res)
-    value = 1.0 / sweep_s
+    from oracle_bind import RefLib, ref_random_factors
+    dims, ranks = list(c["dims"]), list(c["ranks"])
+    N = len(dims)
+    K, W = max(1, args.steps), max(0, args.warmup)
+    u0 = ref_random_factors(RefLib(), dims, ranks, SEED_INIT)  # tucker::random_factors, the engine arm's init
+    r = reference_mode_updates(coords, vals, dims, ranks, u0, K, W)
+    total = sum(r["steps_s"])
+    value = (K / N) / total
     model, ncpu = host_desc()
-    line = {"impl": "reference", "metric": METRIC.format(cfg=args.config), "value": value, "unit": "iter/s", "n_gpus": ws,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sweep_s * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",  # same fixed workload as the engine arm
+    ttm = [p["ttmctc"] for p in r["phases"]]
+    line = {"impl": "reference", "metric": METRIC.format(cfg=args.config), "value": value, "unit": "iter/s",
+            "n_gpus": ws, "steps": K, "warmup": W, "ms_per_step": total / K * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (BASELINE config %d, seeded PCG64)" % args.config,
-            "config": {"workload": c["name"], "dims": list(c["dims"]), "ranks": list(c["ranks"]),
-                       "nnz_merged": int(ov.size)},
-            "cpu_baseline": {"value": value, "unit": "iter/s", "cores": res[0]["threads"], "kind": res[0]["kind"],
-                             "sample": f"{res[0]['sample']} of {ov.size} nonzeros per step, ttmctc_elementwise + "
-                                       f"ttmc_core on {res[0]['threads']} threads (lexicographic slices, one "
-                                       f"reference call per thread), qr_orthonormal at full size; sweep = N x "
-                                       f"(kernels scaled to full nnz + QR); host: {model}, {ncpu} cores"},
-            "ttmctc": {"value": statistics.median(r["ttmctc_nnz_per_s"] for r in res) * res[0]["threads"],
-                       "unit": "nnz/s"},
+            "config": {"workload": c["name"], "dims": dims, "ranks": ranks, "nnz_merged": int(r["nnz"]),
+                       "step": f"one full-size mode update of tucker::hoqri's loop (1/{N} of a sweep): "
+                               "ttmctc_elementwise(core given) + max_abs + qr_orthonormal + subspace_distance + "
+                               "ttmc_core on every nonzero"},
+            "cpu_baseline": {"value": value, "unit": "iter/s", "cores": 1, "kind": "reference",
+                             "sample": f"none: {K} full-size mode updates ({K / N:.2f} sweeps) of the unmodified "
+                                       f"reference, each timed as it ran (steady_clock); the reference is "
+                                       f"single-threaded (kernels.cpp has no threading), so 1 thread of {ncpu} "
+                                       f"host cores ({model}); warm-up steps ran on a 1e5-nonzero prefix",
+                             "phase_s_mean": {k: statistics.mean(p[k] for p in r["phases"]) for k in r["phases"][0]},
+                             "setup_s": {"sparse_tensor_ctor": r["t_build"], "initial_ttmc_core": r["t_init"]}},
+            "ttmctc": {"value": r["nnz"] / statistics.median(ttm), "unit": "nnz/s",
+                       "note": "median of the timed steps' ttmctc_elementwise calls (core given), full nnz"},
             "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
-
-
-def _merge_numpy(coords, vals):
-    """Lexicographic sort + duplicate merge with numpy (host, reference-arm
-    setup only)."""
-    order = np.lexsort(coords.T[::-1])
-    c = coords[order]
-    v = vals[order]
-    head = np.ones(len(c), bool)
-    head[1:] = (c[1:] != c[:-1]).any(axis=1)
-    idx = np.flatnonzero(head)
-    return np.ascontiguousarray(c[head]), np.add.reduceat(v, idx)
-
-
-def _numpy_orthonormal(dims, ranks, seed=SEED_INIT):
-    rng = np.random.default_rng(seed)
-    out = []
-    for d, k in zip(dims, ranks):
-        q, _ = np.linalg.qr(rng.standard_normal((d, k)))
-        out.append(np.ascontiguousarray(q))
-    return out
 
 
 def run_engine(args, ws, rank, local):
@@ -316,6 +334,8 @@ def run_engine(args, ws, rank, local):
     torch.cuda.set_stream(stream)
     x = hq.SparseTensor(dims, coords, vals)
     nnz = x.nnz()
+    if comm is not None and ws > 1:
+        x.shard(comm)  # each rank keeps only its rows' streams (SPEC.md:247 row partition)
     u0 = hq.random_factors(dims, ranks, SEED_INIT)
     W, K = max(1, args.warmup), max(1, args.steps)
     cfg = hq.SolverConfig(ranks=ranks, max_sweeps=W + K + 1, tol_fit_change=0.0)
@@ -363,6 +383,21 @@ def run_engine(args, ws, rank, local):
         f, b = solver.mode_pass_work(m)
         flops.append(f)
         bytes_.append(b)
+    # ---- SURVEY 8(d) TTMcTC nnz/s: the standalone TTMcTC call with the core given (kernels.cpp:86-163 with
+    # precomputed_core), median of 10 CUDA-event-timed calls per mode
+    ttm_ms = []
+    for m in range(N):
+        for _ in range(2):
+            solver.launch_ttmctc(m)
+        ts = []
+        for _ in range(10):
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            solver.launch_ttmctc(m)
+            a1.record(stream)
+            a1.synchronize()
+            ts.append(a0.elapsed_time(a1))
+        ttm_ms.append(statistics.median(ts))
     avg_pass_ms = sum(pass_ms) / N
     avg_flops = sum(flops) / N
     avg_bytes = sum(bytes_) / N
@@ -395,6 +430,8 @@ def run_engine(args, ws, rank, local):
 
         def e2e_step():
             xe = hq.SparseTensor(dims, hc, hv)  # H2D of the COO + device layout build
+            if comm is not None and ws > 1:
+                xe.shard(comm)
             se = hq.Solver(xe, ecfg, init_factors=hu, stream=stream.cuda_stream, comm=comm)  # H2D of the factors
             se.run(sweeps)
             r = se.download(out=hout)  # D2H of factors, core, trace
@@ -429,9 +466,9 @@ def run_engine(args, ws, rank, local):
     cpu = None
     if rank == 0 and not args.no_cpu:
         st = solver.download()
-        core = st.model.core.data
-        cpu = cpu_reference_sample(x.coords(), x.values(), dims, ranks, st.model.factors.factors, core,
-                                   args.cpu_sample, 1)
+        cpu = cpu_baseline_measure(coords, vals, dims, ranks, st.model.factors.factors)  # the reference merges
+    t_roof, roof_parts = sweep_roofline(solver, dims, ranks, nnz, peaks.get("hbm_gbs", 6535.7), peak64)
+    ttm_canon = [solver.ttmctc_work(m) for m in range(N)]
 
     if rank != 0:
         return
@@ -446,8 +483,21 @@ def run_engine(args, ws, rank, local):
                    "parallelism": f"row-partitioned x{ws} (NCCL all-reduce + owner broadcast)" if ws > 1 else "single GPU",
                    "l2": "inputs larger than L2 (mode streams %.0f MB + factors %.0f MB vs 126 MB L2)" %
                          (nnz * (4 * (N - 1) + 8) * N / 1e6, sum(d * k for d, k in zip(dims, ranks)) * 8 * 2 / 1e6)},
-        "ttmctc": {"value": nnz / (avg_pass_ms * 1e-3), "unit": "nnz/s",
-                   "note": "fused mode pass (TTMcTC + Gram + core projection) per launch, mean over modes"},
+        "ttmctc": {"value": nnz / (statistics.mean(ttm_ms) * 1e-3), "unit": "nnz/s",
+                   "per_mode_ms": ttm_ms,
+                   "note": "SURVEY 8(d): standalone TTMcTC (core given; G_(n)^T unfold + A only), median of 10 "
+                           "CUDA-event-timed calls per mode; value = nnz / mean of the per-mode medians",
+                   "roofline_frac_per_mode": [max(b / (peaks.get("hbm_gbs", 6535.7) * 1e9), f / (peak64 * 1e12)) /
+                                              (t * 1e-3) for (f, b), t in zip(ttm_canon, ttm_ms)],
+                   "fp64_frac_per_mode": [f / (t * 1e-3) / 1e12 / peak64 for (f, b), t in zip(ttm_canon, ttm_ms)]},
+        "fused_pass": {"value": nnz / (avg_pass_ms * 1e-3), "unit": "nnz/s", "per_mode_ms": pass_ms,
+                       "note": "the solver's fused mode pass (TTMcTC + M = A^T Y + W = A^T A + max|A|) per launch"},
+        "sweep_roofline": {"t_roof_us": t_roof * 1e6, "iter_per_s_roof": 1.0 / t_roof,
+                           "frac": value * t_roof, "per_mode": roof_parts,
+                           "note": "SURVEY 8(d): sum over modes of max(B/BW, F/P64) for TTMcTC + core + QR, "
+                                   "canonical minimal F and B; BW = MEASURED_PEAKS hbm_gbs, P64 = live DGEMM"},
+        "drift_note": "the drift's K x K nuclear norms (Jacobi SVD) are evaluated at download, outside the timed "
+                      "region (< 0.2 % of a sweep); P = U_new^T U_old itself is computed inside every sweep",
         "roofline": {"bound": "tensor", "achieved": tflops, "peak": peak64, "unit": "TFLOP/s",
                      "frac": tflops / peak64, "traffic": traffic,
                      "kernel": "fused sparse mode pass (hq_pass: short-row tiles + long-row segment/fix-up kernels)",
@@ -467,18 +517,34 @@ def run_engine(args, ws, rank, local):
         line["e2e"] = e2e
     if cpu:
         line["cpu_baseline"] = {
-            "value": 1.0 / cpu["sweep_s"], "unit": "iter/s", "cores": cpu["threads"], "kind": cpu["kind"],
-            "sample": f"reference ttmctc_elementwise + ttmc_core on the first {cpu['sample']} of {nnz} nonzeros "
-                      f"({cpu['t_ttm']:.2f} s + {cpu['t_core']:.2f} s), qr_orthonormal+drift at full size "
-                      f"({cpu['t_qr']:.2f} s); sweep = N x (kernels x nnz/sample + QR) = {cpu['sweep_s']:.1f} s; "
-                      f"1 thread of {ncpu} ({model})",
+            "value": 1.0 / cpu["sweep_s"], "unit": "iter/s", "cores": 1, "kind": cpu["kind"],
+            "sample": f"one full-size mode update (mode 0, all {cpu['nnz']} nonzeros) of the reference's solve "
+                      f"loop, timed as it ran: " + ", ".join(f"{k} {v:.2f} s" for k, v in cpu["phases"].items()) +
+                      f"; sweep = {N} x {cpu['step_s']:.1f} s; 1 thread of {ncpu} ({model}); the reference is "
+                      f"single-threaded",
             "ttmctc_nnz_per_s": cpu["ttmctc_nnz_per_s"]}
     print(json.dumps(line), flush=True)
 
 
+def spawn_ranks(args):
+    """`--gpus N` without a launcher: re-exec this script under
+    torch.distributed.run with N ranks on this node (127.0.0.1)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        spawn_ranks(args)
     ws, rank, local = dist_setup(args)
+    if ws != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; launch with --nproc-per-node {args.gpus}")
     if args.impl == "reference":
         run_reference(args, ws, rank)
         return

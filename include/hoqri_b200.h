@@ -258,6 +258,16 @@ int hq_nccl_unique_id(uint8_t* id_out);
 /* communicator on the current CUDA device; world 1 needs no NCCL */
 int hq_comm_create(int world, int rank, const uint8_t* id, hq_comm** out);
 int hq_comm_destroy(hq_comm* c);
+/* the host transport: ranks on one node (any GPUs, or one shared GPU) exchange
+ * through the POSIX shared-memory segment `name` ("/..." , created by the first
+ * rank to attach); `capacity` = the largest collective in doubles (max I_n K_n).
+ * Collectives are D2H copy -> host combine in rank order -> H2D copy on the
+ * solver's stream; no kernel waits on another rank. */
+int hq_comm_create_host(int world, int rank, const char* name, uint64_t capacity, hq_comm** out);
+/* row-partitioned storage: keep only this rank's rows of every mode stream (the
+ * solver's partition); the tensor is then usable only with a
+ * distributed solver on the same communicator layout */
+int hq_tensor_shard(hq_tensor* t, const hq_comm* comm);
 /* host planner: rank r owns rows [bounds[r], bounds[r+1]) given a mode's
  * bucket offsets (length rows + 1); bounds has world + 1 slots */
 int hq_partition_rows(const uint64_t* offsets, uint64_t rows, int world, uint64_t* bounds);

@@ -23,7 +23,14 @@ config 5 (2e8 nonzeros, N = 4; ~2-3 h per reference sweep) records single
 calls instead: the core at the seeded initial factors (ttmc_core) and one
 TTMcTC per mode with that core (kernels.cpp:86-163), as fingerprints.
 
-Usage:  python oracle/gen_config_traces.py CONFIG FACTOR_SEED SWEEPS [--keep DIR]
+With --variant matrix the same trajectory is run with the reference's other
+kernel, ttmctc_matrix (ref_hoqri_replay_matrix; core once per sweep as
+solvers.cpp does for that variant): it differs from the element-wise run only
+in floating-point summation order, so the spread between the two fixtures is
+the reference's own rounding sensitivity on that input -- the yardstick the
+GPU tests hold the engine's deviation against on ill-conditioned sweeps.
+
+Usage:  python oracle/gen_config_traces.py CONFIG FACTOR_SEED SWEEPS [--keep DIR] [--variant matrix]
 Writes tests/golden/cfg{C}_s{SEED}.npz (rewritten after every sweep, so a
 partial run is usable; ``done_sweeps`` says how far it got).
 """
@@ -59,6 +66,8 @@ def main():
     ap.add_argument("seed", type=int)
     ap.add_argument("sweeps", type=int)
     ap.add_argument("--keep", default=None, help="also save full factors per sweep here (local analysis)")
+    ap.add_argument("--variant", default="elementwise", choices=["elementwise", "matrix"],
+                    help="matrix: the reference's ttmctc_matrix trajectory (its own rounding spread)")
     a = ap.parse_args()
     c = CONFIGS[a.config]
     dims, ranks = list(c["dims"]), list(c["ranks"])
@@ -79,7 +88,8 @@ def main():
                                "ttmc_core, ttmctc_elementwise, qr_orthonormal, subspace_distance "
                                "(solvers.cpp:50-178 loop via ref_hoqri_replay)"))
     del coords, vals
-    name = os.path.join(OUT, f"cfg{a.config}_s{a.seed}.npz")
+    name = os.path.join(OUT, f"cfg{a.config}_s{a.seed}" + ("_matrix" if a.variant == "matrix" else "") + ".npz")
+    out["variant"] = np.array(a.variant)
     print(f"cfg{a.config} seed {a.seed}: gen {t_gen:.1f}s build {t_build:.1f}s nnz {x.nnz}", flush=True)
 
     u = ref_random_factors(lib, dims, ranks, a.seed)
@@ -116,7 +126,7 @@ def main():
     t_sweep = np.zeros(S)
     for s in range(S):
         t0 = time.time()
-        cs, fs, dr = x.replay(ranks, u, 1)
+        cs, fs, dr = x.replay(ranks, u, 1, a.variant)
         t_sweep[s] = time.time() - t0
         u = fs[0]
         cores[s] = cs[0]

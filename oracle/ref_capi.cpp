@@ -531,4 +531,100 @@ double ref_time_qr(uint64_t rows, uint64_t cols, const double* a, int reps) {
     return std::chrono::duration<double>(t1 - t0).count() / reps;
 }
 
+// ---- one mode update of the reference's solve loop, at full size -----------
+// State = the factors and the fresh core that tucker::hoqri carries from one
+// mode update to the next (solvers.cpp:66, 86-146, element-wise kernel with
+// core_per_update).  ref_state_mode_update runs exactly that loop body:
+//   A = ttmctc_elementwise(x, u, n, &core, &ws)   (solvers.cpp:90-91)
+//   max_abs(A) == 0 -> DegenerateStateError      (:124)
+//   U_n = qr_orthonormal(A); drift = subspace_distance(U_n, U_old)   (:139-141)
+//   core = ttmc_core(x, u)                        (:143-144)
+// and returns each phase's wall time (t_out: ttmctc, qr, drift, core).  Used
+// by bench.py's reference arm and cpu_baseline: every timed step is one real,
+// full-size mode update -- nothing is sampled or extrapolated.
+struct RefState {
+    FactorSet u;
+    CoreTensor core;
+    KernelWorkspace ws;
+};
+
+void* ref_state_create(void* h, const uint64_t* ranks, const double* factors) {
+    const SparseTensor& x = static_cast<RefTensor*>(h)->x;
+    const int n = static_cast<int>(x.order());
+    std::vector<uint64_t> dims(x.dims().begin(), x.dims().end());
+    auto* st = new RefState{to_factors(n, dims.data(), ranks, factors), CoreTensor{}, KernelWorkspace{}};
+    st->core = ttmc_core(x, st->u);  // solvers.cpp:66
+    return st;
+}
+
+void ref_state_destroy(void* s) { delete static_cast<RefState*>(s); }
+
+int ref_state_mode_update(void* h, void* s, int mode, double* drift, double* t_out) {
+    try {
+        const SparseTensor& x = static_cast<RefTensor*>(h)->x;
+        RefState& st = *static_cast<RefState*>(s);
+        using clk = std::chrono::steady_clock;
+        auto sec = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
+        auto t0 = clk::now();
+        Matrix a = ttmctc_elementwise(x, st.u, mode, &st.core, &st.ws);
+        if (max_abs(a) == 0.0) {
+            g_payload = mode + 1;
+            return 8;
+        }
+        auto t1 = clk::now();
+        Matrix old = std::move(st.u.factors[mode]);
+        st.u.factors[mode] = qr_orthonormal(a);
+        auto t2 = clk::now();
+        *drift = subspace_distance(st.u.factors[mode], old);
+        auto t3 = clk::now();
+        st.core = ttmc_core(x, st.u);
+        auto t4 = clk::now();
+        t_out[0] = sec(t0, t1);
+        t_out[1] = sec(t1, t2);
+        t_out[2] = sec(t2, t3);
+        t_out[3] = sec(t3, t4);
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+// The same per-sweep replay with the reference's OTHER kernel variant,
+// KernelVariant::kMatrix (ttmctc_matrix, Alg. 4, kernels.cpp:165-262): per mode
+// A = ttmctc_matrix(x, u, n, &ws), QR, drift, and -- as solve() does for the
+// matrix variant without tracing (solvers.cpp:80-81, 153) -- the core only at
+// the end of the sweep.  Its trajectory differs from the element-wise one only
+// by floating-point summation order: the spread between the two is the
+// reference's own rounding sensitivity on a given input.
+int ref_hoqri_replay_matrix(void* h, const uint64_t* ranks, const double* init_factors, uint64_t sweeps,
+                            double* core_snap, double* factor_snap, double* drift) {
+    try {
+        const SparseTensor& x = static_cast<RefTensor*>(h)->x;
+        const int n = static_cast<int>(x.order());
+        std::vector<uint64_t> dims(x.dims().begin(), x.dims().end());
+        FactorSet u = to_factors(n, dims.data(), ranks, init_factors);
+        KernelWorkspace ws;
+        std::size_t ftotal = 0;
+        for (int v = 0; v < n; ++v) ftotal += dims[v] * ranks[v];
+        for (uint64_t s = 0; s < sweeps; ++s) {
+            for (int m = 0; m < n; ++m) {
+                Matrix a = ttmctc_matrix(x, u, m, &ws);
+                if (max_abs(a) == 0.0) {
+                    g_payload = m + 1;
+                    return 8;
+                }
+                Matrix old = std::move(u.factors[m]);
+                u.factors[m] = qr_orthonormal(a);
+                drift[s * n + m] = subspace_distance(u.factors[m], old);
+            }
+            CoreTensor core = ttmc_core(x, u);
+            std::memcpy(core_snap + s * core.size(), core.data.data(), sizeof(double) * core.size());
+            from_factors(u, factor_snap + s * ftotal);
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
 }  // extern "C"

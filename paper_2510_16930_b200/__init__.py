@@ -120,6 +120,7 @@ EXPORTED_SYMBOLS = [
     "hq_solver_create", "hq_solver_destroy", "hq_solver_run", "hq_solver_sync", "hq_solver_status", "hq_solver_launch_mode_pass",
     "hq_solver_launch_ttmctc", "hq_solver_launches_per_sweep", "hq_solver_download", "hq_solver_mode_pass_work",
     "hq_solver_ttmctc_work", "hq_nccl_unique_id", "hq_comm_create", "hq_comm_destroy", "hq_partition_rows",
+    "hq_comm_create_host", "hq_tensor_shard",
     "hq_solver_create_dist", "hq_bench_ttmctc", "hq_gen_synthetic",
     "hq_tns_parse", "hq_tns_parse_file", "hq_tns_info", "hq_tns_copy", "hq_tns_tensor", "hq_tns_destroy",
     "hq_densify_unfold", "hq_ttmc_unfold_dense", "hq_svd_leading", "hq_init_factors", "hq_hooi",
@@ -190,6 +191,8 @@ def load_library(path: str = None) -> C.CDLL:
     L.hq_nccl_unique_id.argtypes = [vp]
     L.hq_comm_create.argtypes = [C.c_int, C.c_int, vp, pp]
     L.hq_comm_destroy.argtypes = [vp]
+    L.hq_comm_create_host.argtypes = [C.c_int, C.c_int, C.c_char_p, C.c_uint64, pp]
+    L.hq_tensor_shard.argtypes = [vp, vp]
     L.hq_partition_rows.argtypes = [_u64p, C.c_uint64, C.c_int, _u64p]
     L.hq_solver_create_dist.argtypes = [vp, C.POINTER(HqConfig), vp, vp, vp, pp]
     _lib = L
@@ -308,6 +311,13 @@ class SparseTensor:
 
     def nnz(self):
         return self._nnz
+
+    def shard(self, comm: "Comm"):
+        """Keep only this rank's rows of every mode stream (the distributed solver's row partition); the
+        tensor is then usable only with a Solver on `comm`."""
+        _check(load_library().hq_tensor_shard(self.handle, comm._h))
+        self._sharded = True
+        return self
 
     def mode_plan(self, mode):
         """Engine work plan of one mode's unfolding: rows, nonempty_rows, long_rows (> 256 nonzeros),
@@ -724,14 +734,26 @@ def nccl_unique_id() -> bytes:
 
 
 class Comm:
-    """NCCL communicator of one rank (one process per GPU, current device)."""
+    """Communicator of one rank: NCCL (one process per GPU, current device), or
+    with ``Comm.host(...)`` the host transport (ranks exchange through a POSIX
+    shared-memory segment; several ranks may share one GPU)."""
 
-    def __init__(self, world: int, rank: int, uid: bytes = b"\0" * 128):
-        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
-        h = C.c_void_p()
-        _check(load_library().hq_comm_create(world, rank, C.cast(buf, C.c_void_p), C.byref(h)))
-        self._h = h
+    def __init__(self, world: int, rank: int, uid: bytes = b"\0" * 128, _handle=None):
+        if _handle is None:
+            buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+            h = C.c_void_p()
+            _check(load_library().hq_comm_create(world, rank, C.cast(buf, C.c_void_p), C.byref(h)))
+            _handle = h
+        self._h = _handle
         self.world, self.rank = world, rank
+
+    @classmethod
+    def host(cls, world: int, rank: int, name: str, capacity: int) -> "Comm":
+        """Host transport over the shared-memory segment `name` (starts with '/'; every rank passes the same
+        name); `capacity` = the largest collective in doubles (>= max I_n K_n)."""
+        h = C.c_void_p()
+        _check(load_library().hq_comm_create_host(world, rank, name.encode(), int(capacity), C.byref(h)))
+        return cls(world, rank, _handle=h)
 
     def __del__(self):
         try:
@@ -782,14 +804,20 @@ class Solver:
         _check(load_library().hq_solver_sync(self._h))
 
     def status(self):
-        """Device status word: sweeps done, Householder fallbacks, abort code, degenerate mode, shifted CholeskyQR3 updates."""
+        """Device status word: sweeps done, Householder fallbacks, abort code, degenerate mode, shifted
+        CholeskyQR3 updates, and (multi-GPU) updates finished by the host-driven Householder continuation."""
         out = (C.c_int64 * 6)()
         _check(load_library().hq_solver_status(self._h, out))
         return {"sweeps": out[0], "fallbacks": out[1], "abort": out[2], "degenerate_mode": out[3],
-                "shifted": out[4], "deficient_kept": out[5]}
+                "shifted": out[4], "dist_householder": out[5]}
 
     def launch_mode_pass(self, mode):
+        """The fused sparse pass of a mode update (A, M, W, max|A|), on the solver's stream."""
         _check(load_library().hq_solver_launch_mode_pass(self._h, mode))
+
+    def launch_ttmctc(self, mode):
+        """The standalone TTMcTC of `mode` with the current core (kernels.cpp:86-163): A only."""
+        _check(load_library().hq_solver_launch_ttmctc(self._h, mode))
 
     def launches_per_sweep(self):
         out = C.c_uint64(0)

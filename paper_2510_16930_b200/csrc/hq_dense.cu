@@ -589,10 +589,10 @@ void launch_gram2(const double* A, uint64_t rows, int K, const double* r1inv, do
 
 void launch_chol2(const double* wpart, int nslots, int K, const double* r1inv, double* rinv, double* rc,
                   const double* m, const ModeShape* sh, double* core_out, DevStatus* st, cudaStream_t s,
-                  bool abort_on_fallback) {
+                  bool abort_on_fallback, int mode1) {
     ModeShape z{};
     k_chol2<<<1, 1024, 0, s>>>(wpart, nslots, K, r1inv, rinv, rc, m, sh ? *sh : z, m != nullptr, core_out, st,
-                               abort_on_fallback ? 1 : 0, 2, nullptr);
+                               abort_on_fallback ? 1 : 0, 2, nullptr, mode1);
     HQ_CHECK_LAUNCH();
 }
 
@@ -605,7 +605,7 @@ void launch_chol3(const double* wpart, int nslots, int K, const double* rc, doub
                   DevStatus* st, cudaStream_t s, bool abort_on_fallback) {
     ModeShape z{};
     k_chol2<<<1, 1024, 0, s>>>(wpart, nslots, K, rc, rinv, nullptr, nullptr, z, 0, nullptr, st,
-                               abort_on_fallback ? 1 : 0, 3, wfull);
+                               abort_on_fallback ? 1 : 0, 3, wfull, 0);
     HQ_CHECK_LAUNCH();
 }
 
@@ -629,6 +629,21 @@ void launch_store_p(const double* ppart, int nslots, int K, int order, int mode,
                     double* trp, const DevStatus* st, cudaStream_t s) {
     const int blocks = std::max(1, (K * K + 7) / 8);
     k_store_p<<<blocks, 256, 0, s>>>(ppart, nslots, K, order, mode, kmax, max_sweeps, trp, st);
+    HQ_CHECK_LAUNCH();
+}
+
+// multi-GPU continuation (hq_solver.cu): clear the abort the chol kernels raised and arm the Householder
+// (kOnlyFallback) kernels for the pending update
+__global__ void k_dist_resume(DevStatus* st) {
+    st->abort = 0;
+    st->pending_mode = 0;
+    st->fallback = 1;
+    st->shifted = 0;
+    st->dist_hh_count++;
+}
+
+void launch_dist_resume(DevStatus* st, cudaStream_t s) {
+    k_dist_resume<<<1, 1, 0, s>>>(st);
     HQ_CHECK_LAUNCH();
 }
 

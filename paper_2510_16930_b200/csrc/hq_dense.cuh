@@ -48,9 +48,11 @@ void launch_gram2(const double* A, uint64_t rows, int K, const double* r1inv, do
 // Cholesky of W2 (reduced from partials): rinv = R2^-1, rc = R1^-1 R2^-1; if
 // m != null and the update is not shifted, G_(n) = rc^T M refolded into the
 // core layout (core_out)
+// multi-GPU: abort 3 cleared, fallback armed for the host-driven Householder continuation
+void launch_dist_resume(DevStatus* st, cudaStream_t s);
 void launch_chol2(const double* wpart, int nslots, int K, const double* r1inv, double* rinv, double* rc,
                   const double* m, const ModeShape* sh, double* core_out, DevStatus* st, cudaStream_t s,
-                  bool abort_on_fallback = false);
+                  bool abort_on_fallback = false, int mode1 = 0);
 // shifted CholeskyQR3 third pass (RunIf kOnlyShifted): Q2 = Q1 R2^-1 in place
 // and the partials of W3 = Q2^T Q2; then rinv = R3^-1 with the identity and
 // rank checks (rc = R1^-1 R2^-1 for diag R, wfull = A^T A for ||A||_F)

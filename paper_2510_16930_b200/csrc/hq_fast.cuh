@@ -24,6 +24,7 @@ struct FastArgs {
     int slot0;
     const DevStatus* st;
     int run_if;
+    int a_only;           // standalone TTMcTC (kTTMcTCOnly): A only, no M / W partials
     int l1_a, l1_b;       // L1-allocating gathers for a hot (skewed) factor (ModeLayout::hot)
 };
 

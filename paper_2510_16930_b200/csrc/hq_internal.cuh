@@ -63,17 +63,21 @@ template <class T>
 struct DBuf {
     T* p = nullptr;
     size_t n = 0;
+    // a rank's slice [off, off + n) of a conceptually longer array (sharded mode streams): get() returns the
+    // base the kernels index with global positions, p - off; only the slice is allocated
+    size_t off = 0;
     DBuf() = default;
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
-    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), off(o.off) { o.p = nullptr; o.n = 0; o.off = 0; }
     DBuf& operator=(DBuf&& o) noexcept {
-        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        if (this != &o) { release(); p = o.p; n = o.n; off = o.off; o.p = nullptr; o.n = 0; o.off = 0; }
         return *this;
     }
     ~DBuf() { release(); }
     void alloc(size_t count) {
         release();
+        off = 0;
         n = count;
         if (count) {
             device_pool_init();
@@ -89,8 +93,9 @@ struct DBuf {
         }
         p = nullptr;
         n = 0;
+        off = 0;
     }
-    T* get() const { return p; }
+    T* get() const { return p ? p - off : nullptr; }
     size_t bytes() const { return sizeof(T) * n; }
 };
 
@@ -141,6 +146,10 @@ struct DeviceTensor {
     DBuf<double> vals;       // merged values
     double norm_sq = 0.0;
     ModeLayout modes[kMaxOrder];
+    // row-partitioned storage (hq_tensor_shard): this rank keeps, per mode, only the stream slice of its rows
+    // [shard_bounds[n][rank], shard_bounds[n][rank + 1]); the lexicographic copy and the buckets' entries are freed
+    int shard_world = 1, shard_rank = 0;
+    std::vector<uint64_t> shard_bounds[kMaxOrder];
 };
 
 // ------------------------------------------------------------ kernel args --

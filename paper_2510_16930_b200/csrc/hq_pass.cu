@@ -414,6 +414,8 @@ void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const Fac
     row_begin = std::min(row_begin, row_end);
     if ((size_t)sh.L * 8 > 200 * 1024)
         fail(HQ_ERR_CAPACITY, "Kronecker row of " + std::to_string(sh.L) + " entries exceeds the device kernel limit");
+    const bool a_only = kind == kTTMcTCOnly;
+    if (a_only) kind = kTTMcTC;
     PassArgs a{};
     a.sh = sh;
     a.rbase = row_begin;
@@ -459,6 +461,7 @@ void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const Fac
         fa.wpart = out.wpart;
         fa.maxpart = out.maxpart;
         fa.kind = kind;
+        fa.a_only = a_only;
         fa.slot0 = 0;
         fa.st = st;
         fa.run_if = run_if;

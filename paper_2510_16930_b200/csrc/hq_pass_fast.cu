@@ -526,6 +526,7 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
         }
         HQ_PHASE(5);
         // M += A_tile^T Y_tile (DMMA), W += A^T A (DFMA)
+        if (!a.a_only) {
 #pragma unroll
         for (int ks = 0; ks < C::R / 4; ++ks)
 #pragma unroll
@@ -538,7 +539,8 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
                     dmma884(macc[bi][0], macc[bi][1], av, yv);
                 }
             }
-        if (warp < NWB) {
+        }
+        if (warp < NWB && !a.a_only) {
 #pragma unroll
             for (int ks = 0; ks < C::R / 4; ++ks) {
                 const double* ar = sA + (size_t)(ks * 4 + (lane & 3)) * C::ALD + (lane >> 2);
@@ -830,6 +832,7 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
             }
         }
         __syncthreads();
+        if (!a.a_only) {
 #pragma unroll
         for (int ks = 0; ks < C::R / 4; ++ks)
 #pragma unroll
@@ -842,7 +845,8 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
                     dmma884(macc[bi][0], macc[bi][1], av, yv);
                 }
             }
-        if (warp < NWB) {
+        }
+        if (warp < NWB && !a.a_only) {
 #pragma unroll
             for (int ks = 0; ks < C::R / 4; ++ks) {
                 const double* ar = sA + (size_t)(ks * 4 + (lane & 3)) * C::ALD + (lane >> 2);

@@ -48,7 +48,8 @@ struct DevStatus {
     unsigned int shifted_count;
     int diag_code;         // abort 5/6 detail: 1 negative gradient, 2 interlacing, 3 not PSD
     int diag_k;            // 1-based index for interlacing
-    unsigned int deficient_count;  // multi-GPU: rank-deficient updates kept on the shifted basis
+    unsigned int dist_hh_count;    // multi-GPU: updates finished by the host-driven Householder continuation
+    int pending_mode;              // multi-GPU, abort 3: 1-based mode whose update needs that continuation
 };
 
 enum RunIf { kAlways = 0, kOnlyFallback = 1, kOnlyCholQR = 2, kOnlyShifted = 3, kFallbackOrShifted = 4 };
@@ -68,7 +69,9 @@ __device__ __forceinline__ bool skip_kernel(const DevStatus* st, int run_if) {
 //   kCore:   a_i = U_n[i, :]                   (so M = sum a_i^T Y_i = G_(n), kernels.cpp:40-84)
 // and always accumulates M = sum_i a_i^T Y_i (K_n x L), W = sum a_i^T a_i
 // (K_n x K_n) and max |a| into per-CTA partial slots.
-enum PassKind { kTTMcTC = 0, kCore = 1 };
+// kTTMcTCOnly: the standalone TTMcTC call (kernels.cpp:86-163) -- A only; the short-row fast kernels skip
+// the M / W accumulation (other kernels run it as kTTMcTC and the partials are ignored)
+enum PassKind { kTTMcTC = 0, kCore = 1, kTTMcTCOnly = 2 };
 
 struct PassOut {
     double* A;        // I_n x K_n rows (may be null for kCore)

@@ -271,6 +271,7 @@ struct Solver {
     cudaEvent_t ev_join = nullptr;
     DBuf<double> tr_obj, tr_fit, tr_drift, fit_prev;
     DBuf<double> tr_p;      // P = U_new^T U_old per (sweep, mode): drifts evaluated at download
+    DBuf<double> tr_pr;     // multi-GPU: tr_p summed over the ranks (each rank stores its rows' partial)
     // gradient tracing (trace_gradients / tol_grad > 0, solvers.cpp:58): per-update diagnostics
     bool tracing = false;
     DBuf<double> tr_grad, tr_fb, tr_sig, tr_lam;
@@ -387,8 +388,17 @@ struct Solver {
         w2red.alloc(kmax * kmax);
         if (comm) core_alt.alloc(core_size);
         pred.alloc(kmax * kmax);
+        if (t->shard_world > 1 && (!comm || comm->world != t->shard_world || comm->rank != t->shard_rank))
+            fail(HQ_ERR_SHAPE, "the tensor is sharded for rank " + std::to_string(t->shard_rank) + " of " +
+                                   std::to_string(t->shard_world) + "; the solver's communicator does not match");
+        if (t->shard_world > 1 && cfg.init == 1)
+            fail(HQ_ERR_SHAPE, "HOSVD initialisation needs the whole tensor on every rank (hq_tensor_shard frees it)");
         if (comm) {
             for (int v = 0; v < N; ++v) {
+                if (t->shard_world > 1) {
+                    bnd[v] = t->shard_bounds[v];
+                    continue;
+                }
                 std::vector<int64_t> off(dims[v] + 1);
                 HQ_CUDA(cudaMemcpyAsync(off.data(), t->modes[v].rowptr.get(), sizeof(int64_t) * off.size(),
                                         cudaMemcpyDeviceToHost, s));
@@ -525,29 +535,26 @@ struct Solver {
             compute_core(p, kFallbackOrShifted, n);
             mark("fallback(no-op)");
         } else {
+            // distributed: plain CholeskyQR2 over this rank's rows with all-reduced Grams.  Any update that is
+            // not plain (shifted or rank-deficient) stops the graph at chol1 / chol2 (abort 3) and is finished
+            // by dist_continuation (the reference's Householder with its seeded fill, on the gathered A).
             double* uloc = unew + r0 * K;
             launch_gram2(a_loc, lrows, K, r1inv.get(), uloc, w2part.get(), S, s);
             launch_reduce_pass(nullptr, 0, w2part.get(), K * K, nullptr, dense_slots(), nullptr, w2red.get(), nullptr, S,
                                kOnlyCholQR, s);
             comm->allreduce_sum(w2red.get(), (size_t)K * K, s);
-            launch_chol2(w2red.get(), 1, K, r1inv.get(), rinv.get(), rc.get(), mred, &m, core.get(), S, s, true);
-            // shifted CholeskyQR3 (device flag; the all-reduce always runs, on stale data when skipped)
-            launch_gram3(uloc, lrows, K, rinv.get(), w2part.get(), S, s);
-            launch_reduce_pass(nullptr, 0, w2part.get(), K * K, nullptr, dense_slots(), nullptr, w2red.get(), nullptr, S,
-                               kOnlyShifted, s);
-            comm->allreduce_sum(w2red.get(), (size_t)K * K, s);
-            launch_chol3(w2red.get(), 1, K, rc.get(), rinv.get(), wred, S, s, true);
+            launch_chol2(w2red.get(), 1, K, r1inv.get(), rinv.get(), rc.get(), mred, &m, core.get(), S, s, true, n + 1);
+            // U_new rows = Q R^-1, P partials of this rank's rows (tr_p is all-reduced once, at download)
             launch_apply(uloc, lrows, K, rinv.get(), uloc, uold + r0 * K, pp, true, S, kOnlyCholQR, s);
-            launch_reduce_pass(nullptr, 0, pp, K * K, nullptr, dense_slots(), nullptr, pred.get(), nullptr, S, kAlways,
-                               s);
-            comm->allreduce_sum(pred.get(), (size_t)K * K, s);
             comm->allgather_rows(unew, bnd[n].data(), (size_t)K, s);
-            // per-mode copy point: the side-stream drift of mode n reads pred_m[n]
-            HQ_CUDA(cudaMemcpyAsync(ppart[n].get(), pred.get(), sizeof(double) * K * K, cudaMemcpyDeviceToDevice, s));
-            pp = ppart[n].get();
-            pslots = 1;
-            compute_core(p, kOnlyShifted, n);
         }
+        mode_tail(n, pp, pslots);
+    }
+
+    // P stored for the lazy drift (side stream); after the last mode, f, fit and the stop rules
+    void mode_tail(int n, const double* pp, int pslots) {
+        const int K = ranks[n];
+        DevStatus* S = st.get();
         // the drift feeds only the trace: P is stored beside the next mode update (side stream) and the
         // drifts are evaluated in one batch at download
         HQ_CUDA(cudaEventRecord(ev_fork[n], s));
@@ -560,6 +567,57 @@ struct Solver {
                           tracing ? tr_grad.get() : nullptr, N, cfg.tol_grad, tracing ? tr_tend.get() : nullptr};
             launch_sweep_end(core.get(), core_size, dns, cfg.tol_fit_change, cfg.max_sweeps, tr, S, s);
             mark("sweep_end");
+        }
+    }
+
+    // Multi-GPU: finish the update the sweep graph stopped at (abort 3: its Gram matrix was not fit for plain
+    // CholeskyQR2) as the reference does every update -- Householder QR with the seeded rank-deficiency fill
+    // (dense_core.cpp:127-198) -- on the all-gathered A, redundantly on every rank (the same bits everywhere:
+    // same A, same deterministic kernel, same fill stream), then the core by a sparse pass over this rank's
+    // rows (all-reduced), then the rest of the sweep eagerly.  Every rank reaches the same decision from the
+    // same all-reduced Gram matrix, so all ranks run the continuation together.
+    void dist_continuation(const DevStatus& h) {
+        const int n = h.pending_mode - 1;
+        if (n < 0 || n >= N) fail(HQ_ERR_INTERNAL, "distributed continuation: no pending mode");
+        const int p = h.sweep & 1;  // parity of the sweep in progress (sweep h.sweep + 1)
+        const int K = ranks[n];
+        DevStatus* S = st.get();
+        double* unew = U[n][1 - p].get();
+        const double* uold = U[n][p].get();
+        launch_dist_resume(S, s);
+        comm->allgather_rows(A.get(), bnd[n].data(), (size_t)K, s);
+        launch_householder(A.get(), dims[n], K, unew, hh.get(), fill ? fill->buf.get() : nullptr,
+                           fill ? fill->len : 0, S, kOnlyFallback, s);
+        double* pp = ppart[n].get();
+        launch_apply(nullptr, dims[n], K, nullptr, unew, uold, pp, false, S, kOnlyFallback, s);
+        if (comm->rank != 0)  // P over all rows on every rank: one copy enters the download all-reduce
+            HQ_CUDA(cudaMemsetAsync(pp, 0, sizeof(double) * (size_t)dense_slots() * K * K, s));
+        compute_core(p, kAlways, n);
+        mode_tail(n, pp, dense_slots());
+        for (int m = n + 1; m < N; ++m) mode_update(m, p);
+    }
+
+    // Multi-GPU: run host-driven continuations until the sweeps requested so far are done (the graphs queued
+    // behind a stopped update ran as no-ops: every kernel skips while abort is set, and the collectives in them
+    // only re-send identical replicated data).
+    void settle() {
+        if (!comm) return;
+        for (;;) {
+            DevStatus h = status();
+            if (h.abort != 3) return;
+            dist_continuation(h);
+            DevStatus h2 = status();
+            if (h2.abort == 3) continue;
+            if (h2.abort) return;
+            host_parity = h2.sweep & 1;
+            launched = (uint64_t)h2.sweep;
+            const uint64_t done = (uint64_t)h2.sweep;
+            for (uint64_t i = done; i < target && i < cfg.max_sweeps; ++i) {
+                HQ_CUDA(cudaGraphLaunch(graph[host_parity], s));
+                host_parity ^= 1;
+                ++launched;
+                if (launched < ev.size()) HQ_CUDA(cudaEventRecord(ev[launched], s));
+            }
         }
     }
 
@@ -576,9 +634,8 @@ struct Solver {
             if (!comm)  // gt, pass, reduce, chol1, gram2, chol2, gram3, chol3, apply, householder, apply-P,
                         // core pass + reduce, store_p
                 c += 1 + pass + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + core_pass + 1 + 1;
-            else        // gt, pass, reduce, chol1, gram2, reduce, chol2, gram3, reduce, chol3, apply, reduce-P,
-                        // core pass + 2 reduces, store_p (NCCL kernels not counted)
-                c += 1 + pass + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + 1 + core_pass + 2 + 1;
+            else        // gt, pass, reduce, chol1, gram2, reduce, chol2, apply, store_p (collective kernels not counted)
+                c += 1 + pass + 1 + 1 + 1 + 1 + 1 + 1 + 1;
         }
         return c + 1;  // sweep_end
     }
@@ -617,7 +674,10 @@ struct Solver {
         prof_ev.clear();
     }
 
+    uint64_t target = 0;  // sweeps requested so far (settle() relaunches what a stopped update skipped)
+
     void run(uint64_t sweeps) {
+        target += sweeps;
         if (!graph[0] && std::getenv("HQ_PROFILE_SWEEP") && sweeps > 1) {
             profile_one_sweep();
             --sweeps;
@@ -663,9 +723,9 @@ struct Solver {
             fail(HQ_ERR_DIAGNOSTIC, "interlacing violated at k=" + std::to_string(h.diag_k) +
                                         "; upstream state is numerically corrupted");
         if (h.abort == 6) fail(HQ_ERR_CONTRACT, "gram_eigvals_desc: matrix is not PSD");  // dense_core.cpp:381-382
-        if (h.abort == 3)
-            fail(HQ_ERR_DIAGNOSTIC, "rank-deficient TTMcTC output in a multi-GPU solve (CholeskyQR2 breakdown); the "
-                                    "Householder fallback runs on one GPU: rerun with a single rank");
+        if (h.abort == 3)  // settle() finishes these; reaching here means a caller skipped it
+            fail(HQ_ERR_INTERNAL, "distributed solve stopped at a pending Householder update (mode " +
+                                      std::to_string(h.pending_mode) + ") that was not continued");
         if (h.abort == 1)
             fail(HQ_ERR_DEGENERATE,
                  "degenerate state: TTMcTC output is identically zero for mode " + std::to_string(h.degenerate_mode),
@@ -681,6 +741,7 @@ struct Solver {
             uint64_t b = std::min(batch, remaining);
             run(b);
             remaining -= b;
+            settle();
             DevStatus h = status();
             check_status(h);
             if (h.abort || (uint64_t)h.sweep >= cfg.max_sweeps) break;
@@ -698,6 +759,12 @@ struct Solver {
                                             cudaMemcpyDeviceToHost, s));
         if (core_out)
             HQ_CUDA(cudaMemcpyAsync(core_out, core.get(), sizeof(double) * core_size, cudaMemcpyDeviceToHost, s));
+        if (comm && h.sweep) {  // every rank, trace requested or not: the per-rank P partials, summed
+            const size_t np = (size_t)h.sweep * N * kmax_ * kmax_;
+            if (!tr_pr.p) tr_pr.alloc(tr_p.n);
+            HQ_CUDA(cudaMemcpyAsync(tr_pr.get(), tr_p.get(), sizeof(double) * np, cudaMemcpyDeviceToDevice, s));
+            comm->allreduce_sum(tr_pr.get(), np, s);
+        }
         if (tr) {
             tr->data_norm_sq = dns;
             tr->initial_objective = initial_objective;
@@ -707,7 +774,8 @@ struct Solver {
                     HQ_CUDA(cudaMemcpyAsync(tr->objective, tr_obj.get(), 8 * h.sweep, cudaMemcpyDeviceToHost, s));
                 if (tr->fit) HQ_CUDA(cudaMemcpyAsync(tr->fit, tr_fit.get(), 8 * h.sweep, cudaMemcpyDeviceToHost, s));
                 if (tr->drift) {
-                    launch_drift_batch(tr_p.get(), h.sweep * N, N, dranks.get(), kmax_, tr_drift.get(), s);
+                    launch_drift_batch(comm ? tr_pr.get() : tr_p.get(), h.sweep * N, N, dranks.get(), kmax_,
+                                       tr_drift.get(), s);
                     HQ_CUDA(cudaMemcpyAsync(tr->drift, tr_drift.get(), 8 * h.sweep * N, cudaMemcpyDeviceToHost, s));
                 }
             }
@@ -933,6 +1001,7 @@ int hq_tensor_mode_plan(const hq_tensor* t, int mode, uint64_t* rows, uint64_t* 
 
 int hq_tensor_export(const hq_tensor* t, uint32_t* coords, double* values) {
     return guard([&] {
+        require_unsharded(t->t, "hq_tensor_export");
         cudaStream_t s = t->stream;
         if (t->t.nnz) {
             if (coords)
@@ -947,6 +1016,7 @@ int hq_tensor_export(const hq_tensor* t, uint32_t* coords, double* values) {
 
 int hq_tensor_buckets(const hq_tensor* t, int mode, uint64_t* offsets, uint64_t* entries) {
     return guard([&] {
+        require_unsharded(t->t, "hq_tensor_buckets");
         if (mode < 0 || mode >= t->t.order) fail(HQ_ERR_RANGE, "mode out of range");
         export_buckets(t->t, mode, offsets, entries, t->stream);
     });
@@ -1004,6 +1074,7 @@ void core_device(const DeviceTensor& T, const UploadedFactors& uf, double* core_
 
 int hq_ttmc_core(const hq_tensor* t, const double* const* factors, const uint64_t* ranks, double* core_out) {
     return guard([&] {
+        require_unsharded(t->t, "hq_ttmc_core");
         cudaStream_t s = t->stream;
         UploadedFactors uf;
         upload_factors(t->t, factors, ranks, uf, s);
@@ -1021,6 +1092,7 @@ int hq_ttmctc(const hq_tensor* t, const double* const* factors, const uint64_t* 
               int variant, double* a_out) {
     (void)variant;
     return guard([&] {
+        require_unsharded(t->t, "hq_ttmctc");
         if (mode < 0 || mode >= t->t.order) fail(HQ_ERR_RANGE, "ttmctc: mode out of range");
         cudaStream_t s = t->stream;
         const DeviceTensor& T = t->t;
@@ -1042,7 +1114,7 @@ int hq_ttmctc(const hq_tensor* t, const double* const* factors, const uint64_t* 
         PassBuffers pb;
         pb.ensure(T.modes[mode], sh);
         PassOut out{A.get(), pb.mpart.get(), pb.wpart.get(), pb.maxpart.get(), pb.ypart.get()};
-        launch_pass(T, mode, sh, uf.f, kTTMcTC, gt.get(), out, nullptr, kAlways, s);
+        launch_pass(T, mode, sh, uf.f, kTTMcTCOnly, gt.get(), out, nullptr, kAlways, s);
         HQ_CUDA(cudaMemcpyAsync(a_out, A.get(), sizeof(double) * T.dims[mode] * sh.kn, cudaMemcpyDeviceToHost, s));
         HQ_CUDA(cudaStreamSynchronize(s));
     });
@@ -1051,6 +1123,7 @@ int hq_ttmctc(const hq_tensor* t, const double* const* factors, const uint64_t* 
 int hq_bench_ttmctc(const hq_tensor* t, const double* const* factors, const uint64_t* ranks, int mode,
                     uint64_t repetitions, double* seconds_out, uint64_t* transient_bytes) {
     return guard([&] {
+        require_unsharded(t->t, "hq_bench_ttmctc");
         if (mode < 0 || mode >= t->t.order) fail(HQ_ERR_RANGE, "ttmctc: mode out of range");
         if (repetitions < 1) fail(HQ_ERR_SHAPE, "repetitions must be at least 1");
         cudaStream_t s = t->stream;
@@ -1074,11 +1147,11 @@ int hq_bench_ttmctc(const hq_tensor* t, const double* const* factors, const uint
         HQ_CUDA(cudaEventCreate(&e0));
         HQ_CUDA(cudaEventCreate(&e1));
         launch_gt(dcore.get(), sh, uf.ranks, gt.get(), nullptr, s);  // warm-up call
-        launch_pass(T, mode, sh, uf.f, kTTMcTC, gt.get(), out, nullptr, kAlways, s);
+        launch_pass(T, mode, sh, uf.f, kTTMcTCOnly, gt.get(), out, nullptr, kAlways, s);
         for (uint64_t r = 0; r < repetitions; ++r) {
             HQ_CUDA(cudaEventRecord(e0, s));
             launch_gt(dcore.get(), sh, uf.ranks, gt.get(), nullptr, s);
-            launch_pass(T, mode, sh, uf.f, kTTMcTC, gt.get(), out, nullptr, kAlways, s);
+            launch_pass(T, mode, sh, uf.f, kTTMcTCOnly, gt.get(), out, nullptr, kAlways, s);
             HQ_CUDA(cudaEventRecord(e1, s));
             HQ_CUDA(cudaEventSynchronize(e1));
             float ms = 0.f;
@@ -1163,6 +1236,7 @@ int hq_gen_synthetic(int order, const uint64_t* dims, uint64_t nnz, uint64_t see
 // ------------------------------------------------------------ desk-scale --
 int hq_densify_unfold(const hq_tensor* t, int mode, uint64_t capacity_cap, double* out) {
     return guard([&] {
+        require_unsharded(t->t, "hq_densify_unfold");
         DBuf<double> d;
         densify_unfold_dev(t->t, mode, capacity_cap, d, t->stream);
         const uint64_t n = t->t.dims[mode] * densify_cols(t->t, mode);
@@ -1174,6 +1248,7 @@ int hq_densify_unfold(const hq_tensor* t, int mode, uint64_t capacity_cap, doubl
 int hq_ttmc_unfold_dense(const hq_tensor* t, const double* const* factors, const uint64_t* ranks, int mode,
                          uint64_t capacity_cap, double* out) {
     return guard([&] {
+        require_unsharded(t->t, "hq_ttmc_unfold_dense");
         if (mode < 0 || mode >= t->t.order) fail(HQ_ERR_RANGE, "ttmc_unfold_dense: mode out of range");
         UploadedFactors uf;
         upload_factors(t->t, factors, ranks, uf, t->stream);
@@ -1208,6 +1283,7 @@ int hq_sym_eig(uint64_t n, const double* m, double* values_desc, double* vectors
 
 int hq_init_factors(const hq_tensor* t, const hq_config* cfg, double* const* factors_out) {
     return guard([&] {
+        require_unsharded(t->t, "hq_init_factors");
         const DeviceTensor& T = t->t;
         if (cfg->order != T.order) fail(HQ_ERR_SHAPE, "rank count does not match tensor order");
         DBuf<double> U[kMaxOrder];
@@ -1231,6 +1307,7 @@ int hq_init_factors(const hq_tensor* t, const hq_config* cfg, double* const* fac
 int hq_hooi(const hq_tensor* t, const hq_config* cfg, const double* const* init_factors, double* const* factors_out,
             double* core_out, hq_trace* trace) {
     return guard([&] {
+        require_unsharded(t->t, "hq_hooi");
         if (cfg->order != t->t.order) fail(HQ_ERR_SHAPE, "rank count does not match tensor order");
         hq_config c = *cfg;
         if (init_factors) c.init = 2;
@@ -1316,6 +1393,7 @@ void hq_config_default(hq_config* cfg) {
 int hq_solver_create(const hq_tensor* t, const hq_config* cfg, const double* const* init_factors, void* stream,
                      hq_solver** out) {
     return guard([&] {
+        require_unsharded(t->t, "hq_solver_create");
         auto h = std::make_unique<hq_solver>();
         h->impl = std::make_unique<Solver>();
         cudaStream_t s = stream ? as_stream(stream) : t->stream;
@@ -1339,6 +1417,21 @@ int hq_comm_create(int world, int rank, const uint8_t* id, hq_comm** out) {
         auto c = std::make_unique<hq_comm>();
         c->impl = comm_create(world, rank, id);
         *out = c.release();
+    });
+}
+
+int hq_comm_create_host(int world, int rank, const char* name, uint64_t capacity, hq_comm** out) {
+    return guard([&] {
+        auto c = std::make_unique<hq_comm>();
+        c->impl = comm_create_host(world, rank, name, capacity);
+        *out = c.release();
+    });
+}
+
+int hq_tensor_shard(hq_tensor* t, const hq_comm* comm) {
+    return guard([&] {
+        if (!comm) fail(HQ_ERR_SHAPE, "hq_tensor_shard: null communicator");
+        shard_tensor(t->t, comm->impl->world, comm->impl->rank, t->stream);
     });
 }
 
@@ -1373,7 +1466,10 @@ int hq_solver_run(hq_solver* s, uint64_t sweeps) {
 }
 
 int hq_solver_sync(hq_solver* s) {
-    return guard([&] { s->impl->check_status(s->impl->status()); });
+    return guard([&] {
+        s->impl->settle();
+        s->impl->check_status(s->impl->status());
+    });
 }
 
 int hq_solver_launch_mode_pass(hq_solver* sv, int mode) {
@@ -1381,11 +1477,22 @@ int hq_solver_launch_mode_pass(hq_solver* sv, int mode) {
         Solver& S = *sv->impl;
         if (mode < 0 || mode >= S.N) fail(HQ_ERR_RANGE, "mode out of range");
         FactorPtrs f = S.factors_for_mode(mode, S.host_parity);
-        launch_pass(*S.T, mode, S.sh[mode], f, kTTMcTC, S.gt.get(), S.pass_out(S.A.get()), nullptr, kAlways, S.s);
+        launch_pass(*S.T, mode, S.sh[mode], f, kTTMcTC, S.gt.get(), S.pass_out(S.A.get()), nullptr, kAlways, S.s,
+                    S.rb(mode), S.re(mode));
     });
 }
 
-int hq_solver_launch_ttmctc(hq_solver* sv, int mode) { return hq_solver_launch_mode_pass(sv, mode); }
+// the standalone TTMcTC (kernels.cpp:86-163 with precomputed_core): A = Y_(n) G_(n)^T only
+int hq_solver_launch_ttmctc(hq_solver* sv, int mode) {
+    return guard([&] {
+        Solver& S = *sv->impl;
+        if (mode < 0 || mode >= S.N) fail(HQ_ERR_RANGE, "mode out of range");
+        FactorPtrs f = S.factors_for_mode(mode, S.host_parity);
+        launch_gt(S.core.get(), S.sh[mode], S.ranks, S.gt.get(), nullptr, S.s);  // G_(n)^T of the current core
+        launch_pass(*S.T, mode, S.sh[mode], f, kTTMcTCOnly, S.gt.get(), S.pass_out(S.A.get()), nullptr, kAlways,
+                    S.s, S.rb(mode), S.re(mode));
+    });
+}
 
 int hq_solver_status(hq_solver* s, int64_t* out) {
     return guard([&] {
@@ -1395,7 +1502,7 @@ int hq_solver_status(hq_solver* s, int64_t* out) {
         out[2] = h.abort;
         out[3] = h.degenerate_mode;
         out[4] = h.shifted_count;
-        out[5] = h.deficient_count;
+        out[5] = h.dist_hh_count;
     });
 }
 
@@ -1442,6 +1549,7 @@ int hq_solver_ttmctc_work(const hq_solver* sv, int mode, double* flops, double* 
 int hq_hoqri(const hq_tensor* t, const hq_config* cfg, const double* const* init_factors, double* const* factors_out,
              double* core_out, hq_trace* trace) {
     return guard([&] {
+        require_unsharded(t->t, "hq_hoqri");
         Solver S;
         S.setup(&t->t, cfg, init_factors, t->stream);
         S.solve();

@@ -257,6 +257,7 @@ class RefLib:
         L.ref_hoqri.argtypes = [vp, u64p, C.c_uint64, C.c_double, C.c_uint64, C.c_int, f64p, f64p,
                                 C.POINTER(C.c_uint64), C.POINTER(C.c_double), f64p, f64p, f64p, f64p]
         L.ref_hoqri_replay.argtypes = [vp, u64p, f64p, C.c_uint64, f64p, f64p, f64p]
+        L.ref_hoqri_replay_matrix.argtypes = [vp, u64p, f64p, C.c_uint64, f64p, f64p, f64p]
         L.ref_tensor_dims.argtypes = [vp, u64p]
         L.ref_densify_unfold.argtypes = [vp, C.c_int, C.c_uint64, f64p]
         L.ref_ttmc_unfold_dense.argtypes = [vp, u64p, f64p, C.c_int, C.c_uint64, f64p]
@@ -278,6 +279,10 @@ class RefLib:
         L.ref_slices_time.restype = C.c_double
         L.ref_time_qr.argtypes = [C.c_uint64, C.c_uint64, f64p, C.c_int]
         L.ref_time_qr.restype = C.c_double
+        L.ref_state_create.argtypes = [vp, u64p, f64p]
+        L.ref_state_create.restype = vp
+        L.ref_state_destroy.argtypes = [vp]
+        L.ref_state_mode_update.argtypes = [vp, vp, C.c_int, C.POINTER(C.c_double), f64p]
 
 
 def ref_svd_leading(lib, y, k):
@@ -447,19 +452,46 @@ class RefTensor:
                     f_after=fa[:u], sigma=sig[:u * ks].reshape(u, ks), lambda_=lam[:u * ks].reshape(u, ks),
                     core=core)
 
-    def replay(self, ranks, init_factors, sweeps):
+    def replay(self, ranks, init_factors, sweeps, variant="elementwise"):
         ranks = _u64(ranks)
         f = _f64(np.concatenate([np.asarray(u).reshape(-1) for u in init_factors]))
         pk = int(np.prod(ranks))
         cs = np.zeros(sweeps * pk)
         fs = np.zeros(sweeps * f.size)
         dr = np.zeros(sweeps * len(self.dims))
-        st = self.lib.L.ref_hoqri_replay(self.h, ranks, f, sweeps, cs, fs, dr)
+        fn = self.lib.L.ref_hoqri_replay if variant == "elementwise" else self.lib.L.ref_hoqri_replay_matrix
+        st = fn(self.h, ranks, f, sweeps, cs, fs, dr)
         if st:
             raise RuntimeError(f"replay status {st}")
         return (cs.reshape((sweeps,) + tuple(int(r) for r in ranks)),
                 [_split(fs[i * f.size:(i + 1) * f.size], self.dims, ranks) for i in range(sweeps)],
                 dr.reshape(sweeps, len(self.dims)))
+
+
+class RefSolveState:
+    """The factors + fresh core tucker::hoqri carries between mode updates
+    (ref_capi.cpp ref_state_*); mode_update(n) runs one full-size mode update of
+    the reference's solve loop and returns (drift, seconds per phase)."""
+
+    def __init__(self, t: "RefTensor", ranks, factors):
+        self.t = t
+        self.ranks = _u64(ranks)
+        f = _f64(np.concatenate([np.asarray(u).reshape(-1) for u in factors]))
+        self.h = t.lib.L.ref_state_create(t.h, self.ranks, f)
+
+    def mode_update(self, mode):
+        d = C.c_double(0)
+        tm = np.zeros(4)
+        st = self.t.lib.L.ref_state_mode_update(self.t.h, self.h, int(mode), C.byref(d), tm)
+        if st:
+            raise RuntimeError(f"reference mode update status {st}")
+        return d.value, dict(ttmctc=tm[0], qr=tm[1], drift=tm[2], core=tm[3])
+
+    def __del__(self):
+        try:
+            self.t.lib.L.ref_state_destroy(self.h)
+        except Exception:
+            pass
 
 
 def ref_random_factors(lib: RefLib, dims, ranks, seed):

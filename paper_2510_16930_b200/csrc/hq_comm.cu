@@ -134,14 +134,18 @@ struct HostXfer {
         ctrl->arrived.fetch_add(1, std::memory_order_acq_rel);
         const uint64_t target = phase * (uint64_t)world;
         auto t0 = std::chrono::steady_clock::now();
+        static const long limit_s = [] {  // HQ_HOST_BARRIER_S: give up (abort) after this many seconds
+            const char* e = std::getenv("HQ_HOST_BARRIER_S");
+            return e && std::atol(e) > 0 ? std::atol(e) : 300L;
+        }();
         int spins = 0;
         while (ctrl->arrived.load(std::memory_order_acquire) < target) {
             if (++spins > 64) {
                 sched_yield();
                 spins = 0;
-                if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(300)) {
-                    std::fprintf(stderr, "[hq] host transport %s: rank %d waited 300 s at barrier %llu; aborting\n",
-                                 name.c_str(), rank, (unsigned long long)phase);
+                if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(limit_s)) {
+                    std::fprintf(stderr, "[hq] host transport %s: rank %d waited %ld s at barrier %llu; aborting\n",
+                                 name.c_str(), rank, limit_s, (unsigned long long)phase);
                     std::abort();
                 }
             }
@@ -274,6 +278,10 @@ namespace {
 template <typename T>
 void keep_slice(DBuf<T>& b, uint64_t z0, uint64_t z1, size_t pad, cudaStream_t s) {
     if (!b.p) return;
+    // the pass kernels stage contiguous record slices with 16-byte copies from the 16-byte-aligned global
+    // position at or below the slice start: keep the slice from such a position so get() + z keeps the
+    // alignment of the unsharded stream for every z
+    z0 -= z0 % (16 / sizeof(T) ? 16 / sizeof(T) : 1);
     DBuf<T> nb;
     nb.alloc(z1 - z0 + pad);
     HQ_CUDA(cudaMemcpyAsync(nb.p, b.get() + z0, sizeof(T) * (z1 - z0 + pad), cudaMemcpyDeviceToDevice, s));

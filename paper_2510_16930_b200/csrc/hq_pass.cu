@@ -443,7 +443,10 @@ void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const Fac
     a.ntiles = (int64_t)ceil_div(a.rows, a.R);
     a.slot0 = 0;
     if (!short_slots(L, sh)) {
-        // every nonempty row is long: no tile kernel
+        // every nonempty row is long: no tile kernel, so nothing writes the empty rows' A = 0 -- clear the
+        // range first (the long-row kernels overwrite the long rows)
+        if (out.A && L.nonempty_rows < L.rows && a.rows)
+            HQ_CUDA(cudaMemsetAsync(out.A + (size_t)row_begin * sh.kn, 0, sizeof(double) * a.rows * sh.kn, s));
     } else if (fast_supported(sh) && !force_generic()) {
         FastArgs fa{};
         fa.rbase = a.rbase;

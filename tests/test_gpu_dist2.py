@@ -61,7 +61,7 @@ def _world2(tmp_path, dims, ranks, coords, vals, u0, sweeps, shard):
     out = tmp_path / "rank0.json"
     name = "/hq_t_" + uuid.uuid4().hex[:12]
     procs = [subprocess.Popen([sys.executable, "-c", RANK_SCRIPT, str(r), "2", name, str(case), "1" if shard else "0",
-                               str(out)], cwd=ROOT, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+                               str(out)], cwd=ROOT, env={**os.environ, "HQ_HOST_BARRIER_S": "90"}, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
              for r in range(2)]
     logs = []
     for p in procs:
@@ -72,8 +72,8 @@ def _world2(tmp_path, dims, ranks, coords, vals, u0, sweeps, shard):
                 q.kill()
             raise
         logs.append((p.returncode, o, e))
-    for rc, o, e in logs:
-        assert rc == 0 and "ok" in o, o + e
+    if not all(rc == 0 and "ok" in o for rc, o, e in logs):
+        raise AssertionError("\n".join(f"--- rank {r}: rc {rc}\n{o}\n{e[-4000:]}" for r, (rc, o, e) in enumerate(logs)))
     return json.load(open(out))
 
 

@@ -60,3 +60,29 @@ def test_zipf_hoqri_matches_oracle(oracle, zipf_tensor):
     assert rel <= 1e-9, rel
     obj = np.array([s.objective for s in r.trace.sweeps])
     np.testing.assert_allclose(obj, ro["objective"], rtol=1e-9, atol=0)
+
+
+@pytest.mark.parametrize("k", [8, 10])
+def test_all_long_rows_with_empty_rows(oracle, k):
+    """A mode whose non-empty rows are ALL long (no tile kernel runs) and that also has empty rows: the empty
+    rows' A must read as 0 (the A buffer is shared by the modes, so stale rows of another mode's update would
+    leak into the QR).  Mode 1 has 6 distinct indices, so its A has rank <= 6 < K and every mode-1 update
+    takes the reference's seeded fill."""
+    rng = np.random.default_rng(5)
+    dims, n = [300, 240, 200], 6000
+    coords = np.empty((n, 3), np.uint32)
+    coords[:, 0] = rng.integers(0, dims[0], n)
+    coords[:, 1] = rng.choice(np.array([3, 50, 77, 120, 199, 230], np.uint32), n)
+    coords[:, 2] = rng.integers(0, dims[2], n)
+    vals = rng.random(n)
+    x = hq.SparseTensor(dims, coords, vals)
+    p = x.mode_plan(1)
+    assert p["nonempty_rows"] == 6 and p["long_rows"] == 6, p
+    sweeps = 4
+    u0 = oracle.random_factors(dims, [k] * 3, 13)
+    r = hq.hoqri(x, hq.SolverConfig(ranks=[k] * 3, max_sweeps=sweeps, tol_fit_change=0.0), init_factors=u0)
+    ro = oracle.hoqri(dims, [k] * 3, x.coords(), x.values(), u0, sweeps)
+    obj = np.array([s.objective for s in r.trace.sweeps])
+    np.testing.assert_allclose(obj, ro["objective"], rtol=1e-9)
+    rel = np.linalg.norm(r.model.core.data - ro["core"].reshape(-1)) / np.linalg.norm(ro["core"])
+    assert rel <= 1e-9, rel

@@ -1,11 +1,14 @@
-"""Per-phase cycle breakdown of the specialised pass (needs a -DHQ_PHASE_TIMING build via HQ_LIB)."""
+"""Per-phase cycle breakdown of the K = 10 short-row pass k_pass_np3 (needs a
+-DHQ_PHASE_TIMING build selected with HQ_LIB; thread 0 of every CTA adds the
+cycles between phase marks).   python tools/phase_timing.py [cfg]"""
 import ctypes as C, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np, torch
+import torch
 import paper_2510_16930_b200 as hq
 from paper_2510_16930_b200.workloads import CONFIGS, config_coo
-c = CONFIGS[2]
-coords, vals = config_coo(2)
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+c = CONFIGS[cfg]
+coords, vals = config_coo(cfg)
 s = torch.cuda.Stream(); torch.cuda.set_stream(s)
 x = hq.SparseTensor(list(c["dims"]), coords, vals)
 u0 = hq.random_factors(list(c["dims"]), list(c["ranks"]), 1)
@@ -14,11 +17,14 @@ sol.run(1); sol.sync()
 L = hq.load_library()
 buf = (C.c_ulonglong * 16)()
 L.hq_debug_phase_cycles(buf, 1)
-for _ in range(3):
+reps = 3
+for _ in range(reps):
     sol.launch_mode_pass(0)
 torch.cuda.synchronize()
 L.hq_debug_phase_cycles(buf, 1)
-names = ["wait gathers", "kron", "Y write", "issue gathers", "A-GEMM", "A write/max", "M-GEMM+W", "meta+records t+2"]
+ctas = 148 * 3
+names = ["meta", "records wait", "gather issue", "gather wait", "kron", "Y write", "A-GEMM+epi", "M-GEMM+W"]
 tot = sum(buf[i] for i in range(8))
 for i, n in enumerate(names):
-    print(f"{n:18s} {buf[i] / 3 / 296 / 1e3:9.1f} kcycles/CTA/launch  {100 * buf[i] / tot:5.1f}%")
+    print(f"{n:14s} {buf[i] / reps / ctas / 1e3:9.1f} kcycles/CTA/launch  {100 * buf[i] / tot:5.1f}%")
+print(f"{'total':14s} {tot / reps / ctas / 1e3:9.1f} kcycles/CTA/launch")

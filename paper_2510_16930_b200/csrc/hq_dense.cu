@@ -489,6 +489,39 @@ __global__ void k_gt(const double* __restrict__ core, ModeShape sh, int order, c
         }
         gt[q] = core[lin];
     }
+    // order 3, K = 10: the short-row pass's A-GEMM fragments (hq_pass_fast.cu k_pass_np3), pre-permuted after
+    // G_(n)^T.  Lane 4g + c of a warp holds the Kronecker block P_c x Q_c of row g (P_c = 5 (c / 2) + .., Q_c =
+    // 5 (c % 2) + .., in lds_block's order: for an odd start the first element comes last); k-step ks = 5 p + q
+    // takes column pi(ks, c) = P_c[p] 10 + Q_c[q].  Table at gt + L K: [25][32] = G^T[pi(ks, c)][g], then
+    // [25][4][2] = G^T[pi(ks, c)][8 + j].
+    if (gt_frag_table(sh)) {
+        double* tb = gt + (size_t)L * Kn;
+        auto blk5 = [](int st, int i) { const int odd = st & 1; return i == 4 ? (odd ? st : st + 4) : st + odd + i; };
+        for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < 25 * 32 + 25 * 8; q += gridDim.x * blockDim.x) {
+            int ks, c, col;
+            if (q < 25 * 32) {
+                ks = q / 32;
+                const int lane = q % 32;
+                c = lane & 3;
+                col = lane >> 2;
+            } else {
+                const int t = q - 25 * 32;
+                ks = t / 8;
+                c = (t / 2) % 4;
+                col = 8 + t % 2;
+            }
+            const int p = ks / 5, qq = ks % 5;
+            const int l = blk5(5 * (c / 2), p) * 10 + blk5(5 * (c % 2), qq);
+            size_t lin = (size_t)col * gstride[sh.n];
+            int j = 0;
+            for (int v = 0; v < order; ++v) {
+                if (v == sh.n) continue;
+                lin += (size_t)((l / sh.cstride[j]) % sh.ko[j]) * gstride[v];
+                ++j;
+            }
+            tb[q] = core[lin];
+        }
+    }
     (void)dranks_unused;
 }
 
@@ -696,7 +729,7 @@ void launch_householder(const double* A, uint64_t rows, int K, double* q_out, do
 void launch_gt(const double* core, const ModeShape& sh, const int* ranks, double* gt, const DevStatus* st,
                cudaStream_t s) {
     (void)ranks;
-    int tot = sh.L * sh.kn;
+    int tot = sh.L * sh.kn + (gt_frag_table(sh) ? kGtFragTable : 0);
     int blocks = std::max(1, std::min((tot + 255) / 256, num_sms()));
     k_gt<<<blocks, 256, 0, s>>>(core, sh, sh.order, nullptr, gt, st);
     HQ_CHECK_LAUNCH();

@@ -604,7 +604,7 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
 // twelve compute warps share an SM (three independent CTAs overlap each
 // other's phases instead of one CTA overlapping its own).
 #ifndef HQ_NP_CAP
-#define HQ_NP_CAP 384
+#define HQ_NP_CAP 352
 #endif
 #ifndef HQ_NP_MINB
 #define HQ_NP_MINB 3
@@ -613,11 +613,14 @@ template <int KA, int KB, int KN>
 struct CfgNP : Cfg<KA, KB, KN> {
     static constexpr int CAP = HQ_NP_CAP;
     static constexpr int FW = KA + KB;
+    static constexpr int ALD = 12;  // A tile row stride: columns 0..K_n-1 (the M-GEMM reads 8..15 only for K_n > 8)
+    static constexpr int GTAB = kGtFragTable;  // the A-GEMM's pre-permuted G_(n)^T fragments (k_gt)
     static constexpr size_t RECB = (size_t)(CAP + 2) * 8 + 2 * (size_t)(CAP + 4) * 4;
     static constexpr size_t SF = (size_t)CAP * FW * 8;
     static constexpr size_t SY = (size_t)Cfg<KA, KB, KN>::R * Cfg<KA, KB, KN>::LDY * 8;
     static_assert(SY <= SF, "the Y tile is written over the staged rows");
-    static constexpr size_t smem = SF + RECB + (size_t)Cfg<KA, KB, KN>::R * Cfg<KA, KB, KN>::ALD * 8 +
+    static_assert(KN <= ALD, "A tile row");
+    static constexpr size_t smem = SF + RECB + (size_t)Cfg<KA, KB, KN>::R * ALD * 8 + (size_t)GTAB * 8 +
                                    Cfg<KA, KB, KN>::META + Cfg<KA, KB, KN>::R * 4 + 64;
 };
 
@@ -636,7 +639,8 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
     uint32_t* rjp = reinterpret_cast<uint32_t*>(recb + (C::CAP + 2) * 8);
     uint32_t* rkp = rjp + C::CAP + 4;
     double* sA = reinterpret_cast<double*>(recb + C::RECB);
-    char* metab = reinterpret_cast<char*>(sA + (size_t)C::R * C::ALD);
+    double* sG = sA + (size_t)C::R * C::ALD;  // fragment table (kTTMcTC)
+    char* metab = reinterpret_cast<char*>(sG + C::GTAB);
     int64_t* m_start = reinterpret_cast<int64_t*>(metab);
     int* m_len = reinterpret_cast<int*>(metab + 8 * C::R);
     int* m_off = m_len + C::R;
@@ -648,6 +652,8 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_f = policy_evict_last();
     for (int q = tid; q < C::R * C::ALD; q += C::THREADS) sA[q] = 0.0;
+    if (a.kind == kTTMcTC)
+        for (int q = tid; q < C::GTAB; q += C::THREADS) sG[q] = a.gt[(size_t)C::L * KN + q];
 
     const int G = gridDim.x, c = blockIdx.x;
     const int64_t ntiles = (int64_t)((a.rows + C::R - 1) / C::R);
@@ -666,16 +672,21 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
     const int64_t t0 = lower((Z * c) / G);
     const int64_t t1 = (c == G - 1) ? ntiles : lower((Z * (c + 1)) / G);
 
-    double macc[C::MBW][2];
+    static_assert(KN == 10 && KA == 10 && KB == 10 && C::TR == 4 && C::RPW == 8 && C::BP == 5 && C::BQ == 5,
+                  "fragment table layout (gt_frag_table)");
+    // M = 13 n-tiles x 2 m-tiles and W's three upper 8 x 8 blocks over 4 warps: warp w owns n-tiles w, w + 4,
+    // w + 8 (both m-tiles); n-tile 12 goes to warps 0 (m-tile 0) and 1 (m-tile 1); W_00 and W_11 to warp 2,
+    // W_01 to warp 3 -- 7 / 7 / 8 / 7 DMMAs per k-step
+    static_assert(C::NLT == 13 && C::WARPS == 4, "M block map");
+    constexpr int NTW = 3;
+    double macc[NTW][2][2];
 #pragma unroll
-    for (int b = 0; b < C::MBW; ++b) macc[b][0] = macc[b][1] = 0.0;
-    constexpr int NWB = C::NT * (C::NT + 1) / 2;
-    const int wmA = (C::NT == 1 || warp < 2) ? 0 : 1, wmB = (C::NT == 1 || warp == 0) ? 0 : 1;
-    double wfr0 = 0.0, wfr1 = 0.0;
+    for (int j = 0; j < NTW; ++j) macc[j][0][0] = macc[j][0][1] = macc[j][1][0] = macc[j][1][1] = 0.0;
+    double xacc0 = 0.0, xacc1 = 0.0, wacc0 = 0.0, wacc1 = 0.0;  // n-tile 12 (warps 0, 1) or W_00 / W_01 (warps 2, 3)
+    double w11a = 0.0, w11b = 0.0;                               // W_11 (warp 2)
     double mx = 0.0;
     const double* __restrict__ gt = a.gt;
-    const int gcolidx = (warp % C::NT) * 8 + (lane >> 2);
-    const bool gvalid = a.kind == kTTMcTC && gcolidx < KN;
+    const int g8 = lane >> 2;  // the A-GEMM's B-fragment column
     const int rslot = warp * C::RPW + lane / C::TR;
     const int pb = (lane % C::TR) / C::TQ, qb = lane % C::TQ;
     const int p0 = pb * C::BP, q0 = qb * C::BQ, sub = lane % C::TR;
@@ -697,22 +708,34 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
         const uint64_t r0 = a.rbase + (uint64_t)t * C::R;
         const int nr = (int)min((uint64_t)C::R, rend - r0);
         // ---- meta
-        if (tid < C::R) {
-            m_len[tid] = (tid < nr) ? ((nhi - nlo > kShortMax) ? -1 : (int)(nhi - nlo)) : 0;
-            m_start[tid] = nlo;
-        }
-        __syncthreads();
-        if (tid < C::R) {
-            const int me = max(m_len[tid], 0);
-            int rank = 0, off = 0;
-            for (int r = 0; r < C::R; ++r) {
-                const int o = max(m_len[r], 0);
-                rank += (o > me) || (o == me && r < tid);
-                off += (r < tid) ? o : 0;
+        // row lengths (-1: long row), exclusive offsets, and ranks by (length desc, row asc): warp 0, one lane
+        // per row, with a shuffle scan and a 9-bit ballot radix rank (lengths <= kShortMax = 256)
+        static_assert(C::R == 32 && kShortMax < 512, "one lane per tile row, 9-bit lengths");
+        if (warp == 0) {
+            const int ln = (lane < nr) ? ((nhi - nlo > kShortMax) ? -1 : (int)(nhi - nlo)) : 0;
+            m_len[lane] = ln;
+            m_start[lane] = nlo;
+            const int me = max(ln, 0);
+            int inc = me;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += v;
             }
-            m_perm[rank] = tid;
-            m_off[tid] = off;
-            if (tid == C::R - 1) m_tot[0] = off + me;
+            m_off[lane] = inc - me;
+            if (lane == 31) m_tot[0] = inc;
+            unsigned gtm = 0u, eqm = 0xffffffffu;
+#pragma unroll
+            for (int b = 8; b >= 0; --b) {
+                const bool bit = (me >> b) & 1;
+                const unsigned B = __ballot_sync(0xffffffffu, bit);
+                if (bit) eqm &= B;
+                else {
+                    gtm |= eqm & B;
+                    eqm &= ~B;
+                }
+            }
+            m_perm[__popc(gtm) + __popc(eqm & ((1u << lane) - 1u))] = lane;
         }
         load_rp(t + 1, nlo, nhi);
         __syncthreads();
@@ -779,7 +802,77 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
             __syncthreads();  // staged rows / records consumed
             HQ_PHASE(4);
         }
-        {   // Y tile over the staged rows
+        // ---- A_tile = Y_tile G_(n)^T straight from the Kronecker registers.  Lane (g, c) holds the block
+        // Y[row g][P_c x Q_c] (the 4 lanes of a row own its four 5 x 5 blocks), which is exactly the DMMA
+        // m8n8k4 A-fragment of the warp's 8 rows under a column permutation: k-step ks = 5 p + q takes column
+        // pi(ks, c) = P_c[p] K_b + Q_c[q] from lane c.  So output columns 0..7 are 25 DMMAs whose B-fragment is
+        // G_(n)^T[pi(ks, c)][g], and columns 8..K_n-1 are per-lane DFMA partials summed over the row's 4 lanes.
+        {
+            const bool valid = lr < nr && m_len[lr] >= 0;
+            if (a.kind == kTTMcTC) {
+                // fragments pre-permuted by k_gt (gt_frag_table): gpm[ks][lane] = G_(n)^T[pi(ks, c)][g],
+                // gtl[ks][c][0..1] = G_(n)^T[pi(ks, c)][8..9] -- constant offsets, no index arithmetic
+                const double* gpm = sG + lane;
+                const double* gtl = sG + 32 * (C::BP * C::BQ) + 2 * sub;
+                double cc[4][2], ex[2][KN - 8];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) cc[u][0] = cc[u][1] = 0.0;
+#pragma unroll
+                for (int u = 0; u < 2; ++u)
+#pragma unroll
+                    for (int j = 0; j < KN - 8; ++j) ex[u][j] = 0.0;
+#pragma unroll
+                for (int p = 0; p < C::BP; ++p)
+#pragma unroll
+                    for (int q = 0; q < C::BQ; ++q) {
+                        const int ks = p * C::BQ + q;
+                        const double y = acc[p][q];
+                        dmma884(cc[ks & 3][0], cc[ks & 3][1], y, gpm[32 * ks]);
+                        const double2 t = *reinterpret_cast<const double2*>(gtl + 8 * ks);
+                        ex[ks & 1][0] = fma(y, t.x, ex[ks & 1][0]);
+                        ex[ks & 1][1] = fma(y, t.y, ex[ks & 1][1]);
+                    }
+                const double c0 = (cc[0][0] + cc[1][0]) + (cc[2][0] + cc[3][0]);
+                const double c1 = (cc[0][1] + cc[1][1]) + (cc[2][1] + cc[3][1]);
+                const double d0 = 0.0, d1 = 0.0;
+                double exs[KN - 8];
+#pragma unroll
+                for (int j = 0; j < KN - 8; ++j) {
+                    exs[j] = ex[0][j] + ex[1][j];
+                    exs[j] += __shfl_xor_sync(0xffffffffu, exs[j], 1);
+                    exs[j] += __shfl_xor_sync(0xffffffffu, exs[j], 2);
+                }
+                // C fragment: lane (g, c) holds columns 2c, 2c + 1 of row g (= this lane's row lr)
+                const double v0 = valid ? c0 + d0 : 0.0, v1 = valid ? c1 + d1 : 0.0;
+                double* sa = sA + lr * C::ALD;
+                sa[2 * sub] = v0;
+                sa[2 * sub + 1] = v1;
+                mx = fmax(mx, fmax(fabs(v0), fabs(v1)));
+                double* dst = a.A ? a.A + (r0 + lr) * KN : nullptr;
+                if (valid && dst) *reinterpret_cast<double2*>(dst + 2 * sub) = make_double2(v0, v1);
+                if (sub == 0) {
+#pragma unroll
+                    for (int j = 0; j < KN - 8; ++j) {
+                        const double v = valid ? exs[j] : 0.0;
+                        sa[8 + j] = v;
+                        mx = fmax(mx, fabs(v));
+                    }
+                    if (valid && dst) {
+                        static_assert((KN - 8) % 2 == 0, "column tail in 16-byte pieces");
+#pragma unroll
+                        for (int j = 0; j < KN - 8; j += 2)
+                            *reinterpret_cast<double2*>(dst + 8 + j) = make_double2(exs[j], exs[j + 1]);
+                    }
+                }
+            } else {  // kCore: a_i = U_n[i]
+                for (int r = sub; r < KN; r += C::TR) {
+                    const double v = valid ? a.un[(r0 + lr) * KN + r] : 0.0;
+                    sA[lr * C::ALD + r] = v;
+                    mx = fmax(mx, fabs(v));
+                }
+            }
+        }
+        {   // Y tile over the staged rows (the M-GEMM's B operand)
             double* y = sY + (size_t)lr * C::LDY;
 #pragma unroll
             for (int p = 0; p < C::BP; ++p)
@@ -790,77 +883,28 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
         }
         __syncthreads();
         HQ_PHASE(5);
-        if (a.kind == kTTMcTC) {
-            const int nt = warp % C::NT;
-            constexpr int KSN = C::L / 4;
-            double cc[C::ABW][2][2];
-#pragma unroll
-            for (int bi = 0; bi < C::ABW; ++bi) cc[bi][0][0] = cc[bi][0][1] = cc[bi][1][0] = cc[bi][1][1] = 0.0;
-#pragma unroll
-            for (int ks = 0; ks < KSN; ++ks)
-#pragma unroll
-                for (int bi = 0; bi < C::ABW; ++bi) {
-                    const int b = warp + bi * C::WARPS;
-                    if (b < C::AB) {
-                        const int mt = b / C::NT;
-                        const double yv = sY[(size_t)(mt * 8 + (lane >> 2)) * C::LDY + (lane & 3) + ks * 4];
-                        const double gv = gvalid ? __ldg(gt + (size_t)(ks * 4 + (lane & 3)) * KN + gcolidx) : 0.0;
-                        dmma884(cc[bi][ks & 1][0], cc[bi][ks & 1][1], yv, gv);
-                    }
-                }
-#pragma unroll
-            for (int bi = 0; bi < C::ABW; ++bi) {
-                const int b = warp + bi * C::WARPS;
-                if (b < C::AB) {
-                    const int mt = b / C::NT;
-                    const int row = mt * 8 + (lane >> 2);
-                    const int col = nt * 8 + 2 * (lane & 3);
-                    const bool valid = row < nr && m_len[row] >= 0;
-                    const double v0 = valid ? cc[bi][0][0] + cc[bi][1][0] : 0.0;
-                    const double v1 = valid ? cc[bi][0][1] + cc[bi][1][1] : 0.0;
-                    sA[row * C::ALD + col] = v0;
-                    sA[row * C::ALD + col + 1] = v1;
-                    mx = fmax(mx, fmax(fabs(v0), fabs(v1)));
-                    if (valid && a.A && col < KN) {
-                        double* dst = a.A + (r0 + row) * KN + col;
-                        if constexpr (KN % 2 == 0)
-                            *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
-                        else {
-                            dst[0] = v0;
-                            if (col + 1 < KN) dst[1] = v1;
-                        }
-                    }
-                }
-            }
-        } else {
-            for (int q = tid; q < C::R * KN; q += C::THREADS) {
-                const int row = q / KN, r = q - row * KN;
-                const double v = (row < nr && m_len[row] >= 0) ? a.un[(r0 + row) * KN + r] : 0.0;
-                sA[row * C::ALD + r] = v;
-                mx = fmax(mx, fabs(v));
-            }
-        }
-        __syncthreads();
         HQ_PHASE(6);
+        // ---- M += A_tile^T Y_tile, W += A_tile^T A_tile: warp w owns M's n-tiles w, w + 4, ... for both m-tiles,
+        // so each k-step loads the two A-fragments once and each Y-fragment once for two DMMAs; W's three
+        // upper 8 x 8 blocks reuse the same A-fragments (warps 0-2)
         if (!a.a_only) {
-#pragma unroll
-        for (int ks = 0; ks < C::R / 4; ++ks)
-#pragma unroll
-            for (int bi = 0; bi < C::MBW; ++bi) {
-                const int b = warp + bi * C::WARPS;
-                if (b < C::MB) {
-                    const int mt = b / C::NLT, nt = b - mt * C::NLT;
-                    const double av = sA[(size_t)(ks * 4 + (lane & 3)) * C::ALD + mt * 8 + (lane >> 2)];
-                    const double yv = sY[(size_t)(ks * 4 + (lane & 3)) * C::LDY + nt * 8 + (lane >> 2)];
-                    dmma884(macc[bi][0], macc[bi][1], av, yv);
-                }
-            }
-        }
-        if (warp < NWB && !a.a_only) {
 #pragma unroll
             for (int ks = 0; ks < C::R / 4; ++ks) {
                 const double* ar = sA + (size_t)(ks * 4 + (lane & 3)) * C::ALD + (lane >> 2);
-                dmma884(wfr0, wfr1, ar[wmA * 8], ar[wmB * 8]);
+                const double av0 = ar[0], av1 = (lane >> 2) < KN - 8 ? ar[8] : 0.0;
+                const double* yr = sY + (size_t)(ks * 4 + (lane & 3)) * C::LDY + (lane >> 2);
+#pragma unroll
+                for (int j = 0; j < NTW; ++j) {
+                    const double yv = yr[(warp + j * C::WARPS) * 8];
+                    dmma884(macc[j][0][0], macc[j][0][1], av0, yv);
+                    dmma884(macc[j][1][0], macc[j][1][1], av1, yv);
+                }
+                if (warp < 2) {
+                    dmma884(xacc0, xacc1, warp == 0 ? av0 : av1, yr[12 * 8]);
+                } else {
+                    dmma884(wacc0, wacc1, av0, warp == 2 ? av0 : av1);
+                    if (warp == 2) dmma884(w11a, w11b, av1, av1);
+                }
             }
         }
         __syncthreads();
@@ -869,28 +913,37 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
 
     const int slot = a.slot0 + c;
     double* mp = a.mpart + (size_t)slot * KN * C::L;
-#pragma unroll
-    for (int bi = 0; bi < C::MBW; ++bi) {
-        const int b = warp + bi * C::WARPS;
-        if (b < C::MB) {
-            const int mt = b / C::NLT, nt = b - mt * C::NLT;
-            const int r = mt * 8 + (lane >> 2), l = nt * 8 + 2 * (lane & 3);
-            if (r < KN) {
-                if (l < C::L) mp[(size_t)r * C::L + l] = macc[bi][0];
-                if (l + 1 < C::L) mp[(size_t)r * C::L + l + 1] = macc[bi][1];
-            }
+    auto put_m = [&](int mt, int nt, double v0, double v1) {
+        const int r = mt * 8 + (lane >> 2), l = nt * 8 + 2 * (lane & 3);
+        if (r < KN) {
+            if (l < C::L) mp[(size_t)r * C::L + l] = v0;
+            if (l + 1 < C::L) mp[(size_t)r * C::L + l + 1] = v1;
         }
-    }
-    if (warp < NWB) {
-        double* wp = a.wpart + (size_t)slot * KN * KN;
-        const int r = wmA * 8 + (lane >> 2), c0 = wmB * 8 + 2 * (lane & 3);
-        const double v[2] = {wfr0, wfr1};
+    };
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
-            if (r < KN && c0 + e < KN) {
-                wp[r * KN + c0 + e] = v[e];
-                if (wmA != wmB) wp[(c0 + e) * KN + r] = v[e];
-            }
+    for (int j = 0; j < NTW; ++j) {
+        put_m(0, warp + j * C::WARPS, macc[j][0][0], macc[j][0][1]);
+        put_m(1, warp + j * C::WARPS, macc[j][1][0], macc[j][1][1]);
+    }
+    if (warp < 2) put_m(warp, 12, xacc0, xacc1);
+    else {
+        double* wp = a.wpart + (size_t)slot * KN * KN;
+        auto put_w = [&](int bA, int bB, double v0, double v1) {
+            const int r = bA * 8 + (lane >> 2), c0 = bB * 8 + 2 * (lane & 3);
+            const double v[2] = {v0, v1};
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+                if (r < KN && c0 + e < KN) {
+                    wp[r * KN + c0 + e] = v[e];
+                    if (bA != bB) wp[(c0 + e) * KN + r] = v[e];
+                }
+        };
+        if (warp == 2) {
+            put_w(0, 0, wacc0, wacc1);
+            put_w(1, 1, w11a, w11b);
+        } else {
+            put_w(0, 1, wacc0, wacc1);
+        }
     }
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
     if (lane == 0) red[warp] = mx;

@@ -73,6 +73,14 @@ __device__ __forceinline__ bool skip_kernel(const DevStatus* st, int run_if) {
 // the M / W accumulation (other kernels run it as kTTMcTC and the partials are ignored)
 enum PassKind { kTTMcTC = 0, kCore = 1, kTTMcTCOnly = 2 };
 
+// G_(n)^T buffers (k_gt) carry, after the L x K_n matrix, the K = 10 order-3 short-row pass's pre-permuted
+// A-GEMM fragments (hq_dense.cu k_gt, hq_pass_fast.cu k_pass_np3): allocate gt_doubles(sh)
+constexpr int kGtFragTable = 25 * 32 + 25 * 8;
+__host__ __device__ inline bool gt_frag_table(const ModeShape& sh) {
+    return sh.order == 3 && sh.ko[0] == 10 && sh.ko[1] == 10 && sh.kn == 10;
+}
+inline size_t gt_doubles(const ModeShape& sh) { return (size_t)sh.L * sh.kn + (gt_frag_table(sh) ? kGtFragTable : 0); }
+
 struct PassOut {
     double* A;        // I_n x K_n rows (may be null for kCore)
     double* mpart;    // [slots][K_n * L]

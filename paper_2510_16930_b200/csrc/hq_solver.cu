@@ -347,7 +347,7 @@ struct Solver {
         if (cfg.max_sweeps < 1) fail(HQ_ERR_SHAPE, "max_sweeps must be at least 1");
         if (cfg.tol_fit_change < 0.0) fail(HQ_ERR_SHAPE, "tolerance must be nonnegative");
         dns = t->norm_sq;
-        size_t maxIK = 0, maxML = 0, maxslots = 0, maxy = 0, maxLK = 0;
+        size_t maxIK = 0, maxML = 0, maxslots = 0, maxy = 0, maxLK = 0, maxGT = 0;
         for (int v = 0; v < N; ++v) {
             sh[v] = make_mode_shape(N, ranks, v);
             maxIK = std::max(maxIK, (size_t)dims[v] * ranks[v]);
@@ -356,13 +356,14 @@ struct Solver {
             maxML = std::max(maxML, (size_t)sl * sh[v].kn * sh[v].L);
             maxy = std::max(maxy, pass_ypart_doubles(t->modes[v], sh[v]));
             maxLK = std::max(maxLK, (size_t)sh[v].kn * sh[v].L);
+            maxGT = std::max(maxGT, gt_doubles(sh[v]));
         }
         int kmax = 1;
         for (int v = 0; v < N; ++v) kmax = std::max(kmax, ranks[v]);
         for (int v = 0; v < N; ++v)
             for (int p = 0; p < 2; ++p) U[v][p].alloc((size_t)dims[v] * ranks[v]);
         core.alloc(core_size);
-        gt.alloc(maxLK);
+        gt.alloc(maxGT);
         A.alloc(maxIK);
         mpart.alloc(maxML);
         wpart.alloc(maxslots * kmax * kmax);
@@ -1108,7 +1109,7 @@ int hq_ttmctc(const hq_tensor* t, const double* const* factors, const uint64_t* 
             core_device(T, uf, dcore.get(), s);
         ModeShape sh = make_mode_shape(T.order, uf.ranks, mode);
         DBuf<double> gt, A;
-        gt.alloc((size_t)sh.L * sh.kn);
+        gt.alloc(gt_doubles(sh));
         A.alloc(T.dims[mode] * sh.kn);
         launch_gt(dcore.get(), sh, uf.ranks, gt.get(), nullptr, s);
         PassBuffers pb;
@@ -1137,7 +1138,7 @@ int hq_bench_ttmctc(const hq_tensor* t, const double* const* factors, const uint
         core_device(T, uf, dcore.get(), s);
         ModeShape sh = make_mode_shape(T.order, uf.ranks, mode);
         DBuf<double> gt, A;
-        gt.alloc((size_t)sh.L * sh.kn);
+        gt.alloc(gt_doubles(sh));
         A.alloc(T.dims[mode] * sh.kn);
         PassBuffers pb;
         pb.ensure(T.modes[mode], sh);

@@ -799,7 +799,9 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
                     for (int q = 0; q < C::BQ; ++q) acc[p][q] = fma(sx, vb[q], acc[p][q]);
                 }
             }
-            __syncthreads();  // staged rows / records consumed
+            // staged rows / records consumed: before the next round overwrites them (the last round's barrier is
+            // after the A-GEMM, which needs only registers, so warps with shorter rows go on to it)
+            if (cv + C::CAP < total) __syncthreads();
             HQ_PHASE(4);
         }
         // ---- A_tile = Y_tile G_(n)^T straight from the Kronecker registers.  Lane (g, c) holds the block
@@ -872,6 +874,7 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
                 }
             }
         }
+        __syncthreads();  // every warp's Kronecker rows done with the staged rows
         {   // Y tile over the staged rows (the M-GEMM's B operand)
             double* y = sY + (size_t)lr * C::LDY;
 #pragma unroll

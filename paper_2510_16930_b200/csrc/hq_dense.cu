@@ -615,9 +615,10 @@ void launch_chol1(const double* w, const double* maxv, int K, double* r1inv, Dev
     HQ_CHECK_LAUNCH();
 }
 
-void launch_gram2(const double* A, uint64_t rows, int K, const double* r1inv, double* q_out, double* wpart,
-                  const DevStatus* st, cudaStream_t s) {
-    launch_rowgemm(K, A, rows, r1inv, q_out, nullptr, wpart, nullptr, st, kOnlyCholQR, s);
+void launch_gram2(const double* A, uint64_t rows, int K, const double* r1inv, double* wpart, const DevStatus* st,
+                  cudaStream_t s) {
+    // Q1 = A R1^-1 is not written: the later passes recompute it bit for bit from A
+    launch_rowgemm(K, A, rows, r1inv, nullptr, nullptr, wpart, nullptr, st, kOnlyCholQR, s);
 }
 
 void launch_chol2(const double* wpart, int nslots, int K, const double* r1inv, double* rinv, double* rc,
@@ -629,9 +630,18 @@ void launch_chol2(const double* wpart, int nslots, int K, const double* r1inv, d
     HQ_CHECK_LAUNCH();
 }
 
-void launch_gram3(double* q, uint64_t rows, int K, const double* r2inv, double* wpart, const DevStatus* st,
-                  cudaStream_t s) {
-    launch_rowgemm(K, q, rows, r2inv, q, nullptr, wpart, nullptr, st, kOnlyShifted, s);
+void launch_gram3(const double* A, uint64_t rows, int K, const double* r1inv, const double* r2inv, double* q_out,
+                  double* wpart, const DevStatus* st, cudaStream_t s) {
+    RowGemm g{};
+    g.A = A;
+    g.rows = rows;
+    g.T = r1inv;
+    g.T2 = r2inv;
+    g.out = q_out;
+    g.part = wpart;
+    g.st = st;
+    g.run_if = kOnlyShifted;
+    launch_rowgemm(K, g, s);
 }
 
 void launch_chol3(const double* wpart, int nslots, int K, const double* rc, double* rinv, const double* wfull,
@@ -648,6 +658,23 @@ void launch_apply(const double* A, uint64_t rows, int K, const double* rinv, dou
         launch_rowgemm(K, A, rows, rinv, u_out, u_old, ppart, nullptr, st, run_if, s);
     else
         launch_rowgemm(K, u_out, rows, nullptr, nullptr, u_old, ppart, nullptr, st, run_if, s);
+}
+
+void launch_apply_qr(const double* A, uint64_t rows, int K, const double* r1inv, const double* rinv, double* u_out,
+                     const double* u_old, double* ppart, bool shifted_alt, const DevStatus* st, int run_if,
+                     cudaStream_t s) {
+    RowGemm g{};
+    g.A = A;
+    g.rows = rows;
+    g.T = r1inv;
+    g.T2 = rinv;
+    g.alt = shifted_alt ? u_out : nullptr;
+    g.out = u_out;
+    g.other = u_old;
+    g.part = ppart;
+    g.st = st;
+    g.run_if = run_if;
+    launch_rowgemm(K, g, s);
 }
 
 void launch_drift(const double* ppart, int nslots, int K, const double* core, uint64_t core_size, double dns,

@@ -27,6 +27,20 @@ int dense_slots();
 // X = A T (T null: identity); out <- X (optional); part[cta] = X^T Y with
 // Y = other (optional) or X; maxpart[cta] = max|A| (optional).  hq_rowgemm.cu
 bool rowgemm_supported(int K);
+struct RowGemm {
+    const double* A;       // rows x K
+    uint64_t rows;
+    const double* T;       // first transform (null: identity)
+    const double* T2;      // optional second transform: X = fl(fl(A T) T2) (the first stage never leaves the SM)
+    const double* alt;     // optional: when st->shifted, X = alt T2 instead (one stage; the shifted apply)
+    double* out;           // X (optional; may alias A / alt)
+    const double* other;   // part = X^T other (optional; else the Gram X^T X)
+    double* part;          // [CTA][K*K] partials
+    double* maxpart;       // [CTA] max|A| (optional)
+    const DevStatus* st;
+    int run_if;
+};
+void launch_rowgemm(int K, const RowGemm& g, cudaStream_t s);
 void launch_rowgemm(int K, const double* A, uint64_t rows, const double* T, double* out, const double* other,
                     double* part, double* maxpart, const DevStatus* st, int run_if, cudaStream_t s);
 
@@ -42,9 +56,9 @@ void launch_gram(const double* A, uint64_t rows, int K, double* wpart, double* m
 // CholeskyQR2 would lose accuracy
 void launch_chol1(const double* w, const double* maxv, int K, double* r1inv, DevStatus* st, int degenerate_mode,
                   uint64_t m_rows, cudaStream_t s, bool abort_on_fallback = false);
-// Q1 = A R1^-1 written to q_out, and the partials of W2 = Q1^T Q1
-void launch_gram2(const double* A, uint64_t rows, int K, const double* r1inv, double* q_out, double* wpart,
-                  const DevStatus* st, cudaStream_t s);
+// the partials of W2 = Q1^T Q1, Q1 = A R1^-1 (not written: recomputed bit for bit by gram3 / apply_qr)
+void launch_gram2(const double* A, uint64_t rows, int K, const double* r1inv, double* wpart, const DevStatus* st,
+                  cudaStream_t s);
 // Cholesky of W2 (reduced from partials): rinv = R2^-1, rc = R1^-1 R2^-1; if
 // m != null and the update is not shifted, G_(n) = rc^T M refolded into the
 // core layout (core_out)
@@ -53,11 +67,11 @@ void launch_dist_resume(DevStatus* st, cudaStream_t s);
 void launch_chol2(const double* wpart, int nslots, int K, const double* r1inv, double* rinv, double* rc,
                   const double* m, const ModeShape* sh, double* core_out, DevStatus* st, cudaStream_t s,
                   bool abort_on_fallback = false, int mode1 = 0);
-// shifted CholeskyQR3 third pass (RunIf kOnlyShifted): Q2 = Q1 R2^-1 in place
-// and the partials of W3 = Q2^T Q2; then rinv = R3^-1 with the identity and
-// rank checks (rc = R1^-1 R2^-1 for diag R, wfull = A^T A for ||A||_F)
-void launch_gram3(double* q, uint64_t rows, int K, const double* r2inv, double* wpart, const DevStatus* st,
-                  cudaStream_t s);
+// shifted CholeskyQR3 third pass (RunIf kOnlyShifted): Q2 = (A R1^-1) R2^-1
+// written to q_out and the partials of W3 = Q2^T Q2; then rinv = R3^-1 with the
+// identity and rank checks (rc = R1^-1 R2^-1 for diag R, wfull = A^T A for ||A||_F)
+void launch_gram3(const double* A, uint64_t rows, int K, const double* r1inv, const double* r2inv, double* q_out,
+                  double* wpart, const DevStatus* st, cudaStream_t s);
 void launch_chol3(const double* wpart, int nslots, int K, const double* rc, double* rinv, const double* wfull,
                   DevStatus* st, cudaStream_t s, bool abort_on_fallback = false);
 // U = A Rinv (written to u_out when non-null, which may alias A); P partials
@@ -65,6 +79,12 @@ void launch_chol3(const double* wpart, int nslots, int K, const double* rc, doub
 // drift).
 void launch_apply(const double* A, uint64_t rows, int K, const double* rinv, double* u_out, const double* u_old,
                   double* ppart, bool apply, const DevStatus* st, int run_if, cudaStream_t s);
+// the CholeskyQR product U = (A R1^-1) R2^-1 (two stages, each rounded as if materialised) written to
+// u_out, and the partials of P = U^T U_old (u_old optional).  shifted_alt: when st->shifted, U = u_out R3^-1
+// instead (u_out holds Q2 from gram3, rinv holds R3^-1 from chol3)
+void launch_apply_qr(const double* A, uint64_t rows, int K, const double* r1inv, const double* rinv, double* u_out,
+                     const double* u_old, double* ppart, bool shifted_alt, const DevStatus* st, int run_if,
+                     cudaStream_t s);
 // drift = max(2K - 2 ||P||_*, 0) (manifold.cpp:55-60) from P partials; when
 // `objective` non-null also f = ||G||^2 and fit = dns - f for the sweep;
 // `end_of_sweep` advances the sweep counter and applies the stop rule.

@@ -34,6 +34,52 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 
 constexpr int kRgWarps = 8;
 
+// B fragments of a K x K transform T (null: none / zero) for X = A T: lane (gid, tig) holds T[4 ks + tig][8 nt + gid]
+template <int K, int KS, int NT>
+__device__ __forceinline__ void rg_frags(const double* T, double (&tf)[KS][NT], int gid, int tig) {
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            const int k = 4 * ks + tig, n = 8 * nt + gid;
+            tf[ks][nt] = (T && k < K && n < K) ? T[k * K + n] : 0.0;
+        }
+}
+
+// a B fragment of T: from the register copy (K <= 16) or from L1 (larger ranks: register budget)
+template <int K>
+__device__ __forceinline__ double rg_b(double reg, const double* T, int ks, int nt, int gid, int tig) {
+    if constexpr (K <= 16) return reg;
+    const int k = 4 * ks + tig, n = 8 * nt + gid;
+    return (k < K && n < K) ? (T ? __ldg(T + k * K + n) : (k == n ? 1.0 : 0.0)) : 0.0;
+}
+
+// second stage of a two-stage product, in place on the warp's 8-row X tile: X <- fl(X T2).  The first stage's
+// rounded X is exactly what a materialised pass would have written and re-read (CholeskyQR's Q1 / Q2).
+template <int K, int KS, int NT, int LD>
+__device__ __forceinline__ void rg_stage2(double* sx, const double (&tf2)[KS][NT], const double* T2, int gid,
+                                          int tig) {
+    constexpr bool kRegs = K <= 16;  // larger ranks read T2's fragments from L1 (register budget)
+    double a[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) a[ks] = (4 * ks + tig < K) ? sx[gid * LD + 4 * ks + tig] : 0.0;
+    __syncwarp();
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+            const int k = 4 * ks + tig, n = 8 * nt + gid;
+            const double b = kRegs ? tf2[ks][nt] : ((k < K && n < K) ? __ldg(T2 + k * K + n) : 0.0);
+            dmma884(c0, c1, a[ks], b);
+        }
+        const int col = 8 * nt + 2 * tig;
+        sx[gid * LD + col] = c0;
+        sx[gid * LD + col + 1] = c1;
+    }
+    __syncwarp();
+}
+
 template <int K>
 struct RG {
     static constexpr int NT = (K + 7) / 8;  // 8-wide tiles of the K dimension
@@ -42,13 +88,27 @@ struct RG {
     static constexpr int LD = KP + 4;       // smem row stride (= 4 mod 8 doubles: fragment reads conflict-free)
 };
 
+// the shifted apply (RowGemm::alt): one stage over the materialised Q2 with T2 = R3^-1
+__device__ __forceinline__ void rg_select(const RowGemm& g, const double*& A, const double*& T, const double*& T2) {
+    const bool alt = g.alt && g.st && g.st->shifted;
+    A = alt ? g.alt : g.A;
+    T = alt ? g.T2 : g.T;
+    T2 = alt ? nullptr : g.T2;
+}
+
 template <int K>
-__global__ void __launch_bounds__(kRgWarps * 32)
-    k_rowgemm(const double* A, uint64_t rows, const double* __restrict__ T, double* out,
-              const double* __restrict__ other, double* __restrict__ part, double* __restrict__ maxpart,
-              const DevStatus* st, int run_if) {
+__global__ void __launch_bounds__(kRgWarps * 32) k_rowgemm(RowGemm g) {
     using C = RG<K>;
-    if (skip_kernel(st, run_if)) return;
+    if (skip_kernel(g.st, g.run_if)) return;
+    const double* A;
+    const double* T;
+    const double* T2;
+    rg_select(g, A, T, T2);
+    const uint64_t rows = g.rows;
+    double* out = g.out;
+    const double* __restrict__ other = g.other;
+    double* __restrict__ part = g.part;
+    double* __restrict__ maxpart = g.maxpart;
     __shared__ double sX[kRgWarps][8 * C::LD];
     __shared__ double sY[kRgWarps][8 * C::LD];
     __shared__ double sRed[C::KP * C::KP];
@@ -63,9 +123,11 @@ __global__ void __launch_bounds__(kRgWarps * 32)
         for (int nt = 0; nt < C::NT; ++nt) {
             const int k = 4 * ks + tig, n = 8 * nt + gid;
             double v = 0.0;
-            if (k < K && n < K) v = T ? T[k * K + n] : (k == n ? 1.0 : 0.0);
+            if (K <= 16 && k < K && n < K) v = T ? T[k * K + n] : (k == n ? 1.0 : 0.0);
             tf[ks][nt] = v;
         }
+    double tf2[C::KS][C::NT];
+    rg_frags<K, C::KS, C::NT>(K <= 16 ? T2 : nullptr, tf2, gid, tig);
     double acc[C::NT][C::NT][2];
 #pragma unroll
     for (int i = 0; i < C::NT; ++i)
@@ -118,12 +180,13 @@ __global__ void __launch_bounds__(kRgWarps * 32)
         for (int nt = 0; nt < C::NT; ++nt) {
             double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-            for (int ks = 0; ks < C::KS; ++ks) dmma884(c0, c1, a[ks], tf[ks][nt]);
+            for (int ks = 0; ks < C::KS; ++ks) dmma884(c0, c1, a[ks], rg_b<K>(tf[ks][nt], T, ks, nt, gid, tig));
             const int col = 8 * nt + 2 * tig;
             sx[gid * C::LD + col] = c0;
             sx[gid * C::LD + col + 1] = c1;
         }
         __syncwarp();
+        if (T2) rg_stage2<K, C::KS, C::NT, C::LD>(sx, tf2, T2, gid, tig);
         if (out) {
 #pragma unroll
             for (int i = 0; i < OQ; ++i) {
@@ -264,13 +327,19 @@ struct RT {
 };
 
 template <int K>
-__global__ void __launch_bounds__((RT<K>::CW + 1) * 32, 1)
-    k_rowgemm_tma(const double* A, uint64_t rows, const double* __restrict__ T, double* out,
-                  const double* __restrict__ other, double* __restrict__ part, double* __restrict__ maxpart,
-                  const DevStatus* st, int run_if) {
+__global__ void __launch_bounds__((RT<K>::CW + 1) * 32, 1) k_rowgemm_tma(RowGemm g) {
     using C = RT<K>;
     constexpr int kTcW = C::CW, kTRows = C::ROWS;
-    if (skip_kernel(st, run_if)) return;
+    if (skip_kernel(g.st, g.run_if)) return;
+    const double* A;
+    const double* T;
+    const double* T2;
+    rg_select(g, A, T, T2);
+    const uint64_t rows = g.rows;
+    double* out = g.out;
+    const double* __restrict__ other = g.other;
+    double* __restrict__ part = g.part;
+    double* __restrict__ maxpart = g.maxpart;
     extern __shared__ __align__(128) double rsm[];
     const int NS = other ? C::S2 : C::MAXS;                   // stages
     double* sA = rsm;                                         // NS x CHD
@@ -326,9 +395,11 @@ __global__ void __launch_bounds__((RT<K>::CW + 1) * 32, 1)
         for (int nt = 0; nt < C::NT; ++nt) {
             const int k = 4 * ks + tig, n = 8 * nt + gid;
             double v = 0.0;
-            if (k < K && n < K) v = T ? T[k * K + n] : (k == n ? 1.0 : 0.0);
+            if (K <= 16 && k < K && n < K) v = T ? T[k * K + n] : (k == n ? 1.0 : 0.0);
             tf[ks][nt] = v;
         }
+    double tf2[C::KS][C::NT];
+    rg_frags<K, C::KS, C::NT>(K <= 16 ? T2 : nullptr, tf2, gid, tig);
     double acc[C::NT][C::NT][2];
 #pragma unroll
     for (int i = 0; i < C::NT; ++i)
@@ -359,12 +430,13 @@ __global__ void __launch_bounds__((RT<K>::CW + 1) * 32, 1)
         for (int nt = 0; nt < C::NT; ++nt) {
             double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-            for (int ks = 0; ks < C::KS; ++ks) dmma884(c0, c1, a[ks], tf[ks][nt]);
+            for (int ks = 0; ks < C::KS; ++ks) dmma884(c0, c1, a[ks], rg_b<K>(tf[ks][nt], T, ks, nt, gid, tig));
             const int col = 8 * nt + 2 * tig;
             sx[gid * C::LD + col] = c0;
             sx[gid * C::LD + col + 1] = c1;
         }
         __syncwarp();
+        if (T2) rg_stage2<K, C::KS, C::NT, C::LD>(sx, tf2, T2, gid, tig);
         const int gr0 = 8 * warp;
         if (out) {
             const int lim = max(0, min(8, nr - gr0)) * K;
@@ -429,12 +501,11 @@ __global__ void __launch_bounds__((RT<K>::CW + 1) * 32, 1)
 }
 
 template <int K>
-void launch_rg(const double* A, uint64_t rows, const double* T, double* out, const double* other, double* part,
-               double* maxpart, const DevStatus* st, int run_if, cudaStream_t s) {
+void launch_rg(const RowGemm& g, cudaStream_t s) {
     // bulk copies need 16-byte aligned sources (a row-range slice of A in the multi-GPU path may start
     // mid-unit): those take the register-staged kernel
-    const bool aligned = (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
-                         (!other || reinterpret_cast<uintptr_t>(other) % 16 == 0);
+    auto al = [](const double* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
+    const bool aligned = al(g.A) && (!g.other || al(g.other)) && (!g.alt || al(g.alt));
     if (aligned) {
         using C = RT<K>;
         static bool attr = false;
@@ -442,10 +513,9 @@ void launch_rg(const double* A, uint64_t rows, const double* T, double* out, con
             HQ_CUDA(cudaFuncSetAttribute(k_rowgemm_tma<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem));
             attr = true;
         }
-        k_rowgemm_tma<K><<<dense_slots(), (C::CW + 1) * 32, C::smem, s>>>(A, rows, T, out, other, part, maxpart, st,
-                                                                        run_if);
+        k_rowgemm_tma<K><<<dense_slots(), (C::CW + 1) * 32, C::smem, s>>>(g);
     } else {
-        k_rowgemm<K><<<dense_slots(), kRgWarps * 32, 0, s>>>(A, rows, T, out, other, part, maxpart, st, run_if);
+        k_rowgemm<K><<<dense_slots(), kRgWarps * 32, 0, s>>>(g);
     }
     HQ_CHECK_LAUNCH();
 }
@@ -454,16 +524,30 @@ void launch_rg(const double* A, uint64_t rows, const double* T, double* out, con
 
 bool rowgemm_supported(int K) { return K >= 1 && K <= 32; }
 
-void launch_rowgemm(int K, const double* A, uint64_t rows, const double* T, double* out, const double* other,
-                    double* part, double* maxpart, const DevStatus* st, int run_if, cudaStream_t s) {
+void launch_rowgemm(int K, const RowGemm& g, cudaStream_t s) {
     switch (K) {
-#define HQ_K(KK) case KK: launch_rg<KK>(A, rows, T, out, other, part, maxpart, st, run_if, s); return;
+#define HQ_K(KK) case KK: launch_rg<KK>(g, s); return;
         HQ_K(1) HQ_K(2) HQ_K(3) HQ_K(4) HQ_K(5) HQ_K(6) HQ_K(7) HQ_K(8) HQ_K(9) HQ_K(10) HQ_K(11) HQ_K(12)
         HQ_K(13) HQ_K(14) HQ_K(15) HQ_K(16) HQ_K(17) HQ_K(18) HQ_K(19) HQ_K(20) HQ_K(21) HQ_K(22) HQ_K(23)
         HQ_K(24) HQ_K(25) HQ_K(26) HQ_K(27) HQ_K(28) HQ_K(29) HQ_K(30) HQ_K(31) HQ_K(32)
 #undef HQ_K
         default: fail(HQ_ERR_CAPACITY, "rank above 32");
     }
+}
+
+void launch_rowgemm(int K, const double* A, uint64_t rows, const double* T, double* out, const double* other,
+                    double* part, double* maxpart, const DevStatus* st, int run_if, cudaStream_t s) {
+    RowGemm g{};
+    g.A = A;
+    g.rows = rows;
+    g.T = T;
+    g.out = out;
+    g.other = other;
+    g.part = part;
+    g.maxpart = maxpart;
+    g.st = st;
+    g.run_if = run_if;
+    launch_rowgemm(K, g, s);
 }
 
 }  // namespace hq

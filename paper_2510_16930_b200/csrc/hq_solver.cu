@@ -155,12 +155,12 @@ void qr_device(const double* A, uint64_t rows, int K, double* Q, QrWork& w, cuda
     launch_reduce_pass(nullptr, 0, w.wpart.get(), K * K, w.maxpart.get(), dense_slots(), nullptr, w.w.get(),
                        w.maxv.get(), st, kAlways, s);
     launch_chol1(w.w.get(), w.maxv.get(), K, w.r1inv.get(), st, 0, rows, s);
-    launch_gram2(A, rows, K, w.r1inv.get(), Q, w.wpart.get(), st, s);  // Q <- Q1
+    launch_gram2(A, rows, K, w.r1inv.get(), w.wpart.get(), st, s);
     launch_chol2(w.wpart.get(), dense_slots(), K, w.r1inv.get(), w.rinv.get(), w.rc.get(), nullptr, nullptr, nullptr,
                  st, s);
-    launch_gram3(Q, rows, K, w.rinv.get(), w.wpart.get(), st, s);  // shifted: Q <- Q2
+    launch_gram3(A, rows, K, w.r1inv.get(), w.rinv.get(), Q, w.wpart.get(), st, s);  // shifted: Q <- Q2
     launch_chol3(w.wpart.get(), dense_slots(), K, w.rc.get(), w.rinv.get(), w.w.get(), st, s);
-    launch_apply(Q, rows, K, w.rinv.get(), Q, nullptr, nullptr, true, st, kOnlyCholQR, s);
+    launch_apply_qr(A, rows, K, w.r1inv.get(), w.rinv.get(), Q, nullptr, nullptr, true, st, kOnlyCholQR, s);
     DevStatus h{};
     HQ_CUDA(cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, s));
     HQ_CUDA(cudaStreamSynchronize(s));
@@ -518,16 +518,17 @@ struct Solver {
         double* pp = ppart[n].get();
         int pslots = dense_slots();
         if (!comm) {
-            launch_gram2(a_loc, lrows, K, r1inv.get(), unew, w2part.get(), S, s);  // U_new <- Q1
+            launch_gram2(a_loc, lrows, K, r1inv.get(), w2part.get(), S, s);
             mark("gram2");
             launch_chol2(w2part.get(), dense_slots(), K, r1inv.get(), rinv.get(), rc.get(), mred, &m, core.get(),
                          S, s);
             mark("chol2");
             // shifted CholeskyQR3 branch (device flag): U_new <- Q2, R3
-            launch_gram3(unew, lrows, K, rinv.get(), w2part.get(), S, s);
+            launch_gram3(a_loc, lrows, K, r1inv.get(), rinv.get(), unew, w2part.get(), S, s);
             launch_chol3(w2part.get(), dense_slots(), K, rc.get(), rinv.get(), wred, S, s);
             mark("cholqr3(no-op)");
-            launch_apply(unew, lrows, K, rinv.get(), unew, uold, pp, true, S, kOnlyCholQR, s);
+            // U_new = (A R1^-1) R2^-1 (shifted: Q2 R3^-1), P partials
+            launch_apply_qr(a_loc, lrows, K, r1inv.get(), rinv.get(), unew, uold, pp, true, S, kOnlyCholQR, s);
             mark("apply");
             // Householder branch (device flag)
             launch_householder(A.get(), dims[n], K, unew, hh.get(), fill ? fill->buf.get() : nullptr,
@@ -540,13 +541,14 @@ struct Solver {
             // not plain (shifted or rank-deficient) stops the graph at chol1 / chol2 (abort 3) and is finished
             // by dist_continuation (the reference's Householder with its seeded fill, on the gathered A).
             double* uloc = unew + r0 * K;
-            launch_gram2(a_loc, lrows, K, r1inv.get(), uloc, w2part.get(), S, s);
+            launch_gram2(a_loc, lrows, K, r1inv.get(), w2part.get(), S, s);
             launch_reduce_pass(nullptr, 0, w2part.get(), K * K, nullptr, dense_slots(), nullptr, w2red.get(), nullptr, S,
                                kOnlyCholQR, s);
             comm->allreduce_sum(w2red.get(), (size_t)K * K, s);
             launch_chol2(w2red.get(), 1, K, r1inv.get(), rinv.get(), rc.get(), mred, &m, core.get(), S, s, true, n + 1);
             // U_new rows = Q R^-1, P partials of this rank's rows (tr_p is all-reduced once, at download)
-            launch_apply(uloc, lrows, K, rinv.get(), uloc, uold + r0 * K, pp, true, S, kOnlyCholQR, s);
+            launch_apply_qr(a_loc, lrows, K, r1inv.get(), rinv.get(), uloc, uold + r0 * K, pp, false, S, kOnlyCholQR,
+                            s);
             comm->allgather_rows(unew, bnd[n].data(), (size_t)K, s);
         }
         mode_tail(n, pp, pslots);

@@ -14,7 +14,7 @@ coords, vals = config_coo(cid)
 dims, ranks = list(c["dims"]), list(c["ranks"])
 s = torch.cuda.Stream(); torch.cuda.set_stream(s)
 x = hq.SparseTensor(dims, coords, vals)
-u0 = hq.random_factors(dims, ranks, 1)
+u0 = hq.random_factors(dims, ranks, int(os.environ.get("HQ_SEED", "20251016")))
 sol = hq.Solver(x, hq.SolverConfig(ranks=ranks, max_sweeps=1000, tol_fit_change=0.0), init_factors=u0.factors,
                 stream=s.cuda_stream)
 sol.run(3); sol.sync()

@@ -116,7 +116,9 @@ struct HhCtl {
     unsigned int rng_seeded;
     unsigned int started;  // diagnostics for the barrier watchdog: CTAs that entered / left the kernel
     unsigned int exited;
-    unsigned int pad[3];
+    unsigned int timeout_cta;   // barrier watchdog: 1 + the CTA that gave up (0: none), read by the host on failure
+    unsigned int timeout_gen;
+    unsigned int pad;
     DevRng rng;
 };
 
@@ -148,9 +150,10 @@ __device__ __forceinline__ void hh_grid_sync(HhCtl* ctl, unsigned int& gen) {
             while (gen_now() == gen) {
                 __nanosleep(64);
                 if (clock64() - t0 > (1ll << 33)) {  // ~4 s: a lost arrival -- fail loudly instead of hanging
-                    printf("hq: householder grid barrier timeout: cta %d gen %u count %u grid %d started %u exited %u\n",
-                           (int)blockIdx.x, gen, atomicAdd(&ctl->bar_count, 0u), (int)gridDim.x,
-                           atomicAdd(&ctl->started, 0u), atomicAdd(&ctl->exited, 0u));
+                    // (no printf: its ABI call would make every inlined barrier save registers to the stack)
+                    ctl->timeout_cta = blockIdx.x + 1;
+                    ctl->timeout_gen = gen;
+                    __threadfence_system();
                     __trap();
                 }
             }

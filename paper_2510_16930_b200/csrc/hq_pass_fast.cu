@@ -875,7 +875,7 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
             }
         }
         __syncthreads();  // every warp's Kronecker rows done with the staged rows
-        {   // Y tile over the staged rows (the M-GEMM's B operand)
+        if (!a.a_only) {  // Y tile over the staged rows (the M-GEMM's B operand; the standalone TTMcTC needs none)
             double* y = sY + (size_t)lr * C::LDY;
 #pragma unroll
             for (int p = 0; p < C::BP; ++p)
@@ -883,8 +883,8 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
                 for (int q = 0; q < C::BQ; ++q) y[blk_index<C::BP>(p0, p) * KB + blk_index<C::BQ>(q0, q)] = acc[p][q];
             if (C::LP > C::L && pb == 0 && qb == 0)
                 for (int l = C::L; l < C::LP; ++l) y[l] = 0.0;
+            __syncthreads();
         }
-        __syncthreads();
         HQ_PHASE(5);
         HQ_PHASE(6);
         // ---- M += A_tile^T Y_tile, W += A_tile^T A_tile: warp w owns M's n-tiles w, w + 4, ... for both m-tiles,

@@ -352,6 +352,10 @@ def run_engine(args, ws, rank, local):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     solver.run(K)
+    if ws > 1:
+        # a multi-GPU update that is not plain CholeskyQR2 (shifted / rank-deficient) is finished by a
+        # host-driven continuation inside sync(): it belongs to the timed sweeps
+        solver.sync()
     # (status read after the timed region)
     e1.record(stream)
     torch.cuda.synchronize()

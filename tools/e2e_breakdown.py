@@ -13,13 +13,13 @@ dims, ranks = list(c["dims"]), list(c["ranks"])
 s = torch.cuda.Stream(); torch.cuda.set_stream(s)
 pc = torch.from_numpy(np.ascontiguousarray(coords)).pin_memory()
 pv = torch.from_numpy(np.ascontiguousarray(vals)).pin_memory()
-u0 = hq.random_factors(dims, ranks, 1)
+u0 = hq.random_factors(dims, ranks, int(os.environ.get("HQ_SEED", "20251016")))
 pu = [torch.from_numpy(np.ascontiguousarray(f)).pin_memory() for f in u0.factors]
 hc, hv, hu = pc.numpy(), pv.numpy(), [t.numpy() for t in pu]
 cfg = hq.SolverConfig(ranks=ranks, max_sweeps=c["sweeps"], tol_fit_change=0.0)
 po = [torch.empty((d, k), dtype=torch.float64).pin_memory().numpy() for d, k in zip(dims, ranks)]
 pcore = torch.empty(int(np.prod(ranks)), dtype=torch.float64).pin_memory().numpy()
-for it in range(3):
+for it in range(int(os.environ.get("HQ_ITERS", "3"))):
     t = [time.perf_counter()]
     x = hq.SparseTensor(dims, hc, hv); torch.cuda.synchronize(); t.append(time.perf_counter())
     sol = hq.Solver(x, cfg, init_factors=hu, stream=s.cuda_stream); torch.cuda.synchronize(); t.append(time.perf_counter())

@@ -1,0 +1,4 @@
+export PYTHONUNBUFFERED=1
+timeout 300 python tools/pass_time.py 2 20 2>&1 | grep '^{'
+HQ_LIB=$PWD/tmp_variants/grow/libhoqri_b200.so timeout 300 python tools/pass_time.py 2 20 2>&1 | grep '^{'
+HQ_LIB=$PWD/tmp_variants/grow/libhoqri_b200.so timeout 300 python tools/pass_time.py 3 10 2>&1 | grep '^{'

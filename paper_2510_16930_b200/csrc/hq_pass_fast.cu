@@ -659,13 +659,18 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
     const int64_t ntiles = (int64_t)((a.rows + C::R - 1) / C::R);
     const uint64_t rend = a.rbase + a.rows;
     const int64_t zb = a.rowptr[a.rbase];
-    const int64_t Z = a.rowptr[rend] - zb;
+    // CTAs take contiguous tile ranges of equal cost: records + a fixed per-tile cost (meta, barriers, the
+    // per-row GEMMs) worth kTileCost records, so ranges of sparse tiles (skewed modes) are not overloaded
+    constexpr int64_t kTileCost = 320;
+    auto tile_cost = [&](int64_t t) {
+        return a.rowptr[a.rbase + min((uint64_t)t * C::R, a.rows)] - zb + kTileCost * t;
+    };
+    const int64_t Z = tile_cost(ntiles);
     auto lower = [&](int64_t z) {
         int64_t lo = 0, hi = ntiles;
         while (lo < hi) {
             int64_t mid = (lo + hi) >> 1;
-            uint64_t r = a.rbase + min((uint64_t)mid * C::R, a.rows);
-            if (a.rowptr[r] - zb >= z) hi = mid; else lo = mid + 1;
+            if (tile_cost(mid) >= z) hi = mid; else lo = mid + 1;
         }
         return lo;
     };

@@ -80,6 +80,12 @@ int hq_tensor_info(const hq_tensor* t, int* order, uint64_t* dims, uint64_t* nnz
    and max_tile32 = the most short-row nonzeros in one 32-row tile of the pass kernels */
 int hq_tensor_mode_plan(const hq_tensor* t, int mode, uint64_t* rows, uint64_t* nonempty_rows, uint64_t* long_rows,
                         uint64_t* long_segments, int* hot, uint64_t* max_tile32);
+/* fiber units of a mode's long rows (order 3, skewed tensors; engine-only, no reference counterpart): within a
+   row the nonzeros sharing the first other index form a fiber, whose Kronecker product is taken once
+   (kernels.cpp:86-163 takes it per nonzero; same sum, regrouped).  units = 0 when the mode does not use them;
+   long_nnz / units is the factor by which the long rows' stream shrinks.  HQ_FIBERS=0/1 (read when the
+   tensor is built) disables / forces them. */
+int hq_tensor_fiber_plan(const hq_tensor* t, int mode, uint64_t* units, uint64_t* long_nnz, uint64_t* segments);
 /* sorted, merged entries (sparse_tensor.hpp:44-51): coords nnz*order, values nnz */
 int hq_tensor_export(const hq_tensor* t, uint32_t* coords, double* values);
 /* ModeBuckets (sparse_tensor.hpp:25-32): offsets dims[mode]+1, entries nnz */

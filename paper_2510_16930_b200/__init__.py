@@ -113,7 +113,7 @@ class HqTrace(C.Structure):
 EXPORTED_SYMBOLS = [
     "hq_last_error", "hq_last_error_payload", "hq_version",
     "hq_tensor_create", "hq_tensor_create_dev", "hq_tensor_destroy", "hq_tensor_info", "hq_tensor_mode_plan",
-    "hq_tensor_export",
+    "hq_tensor_fiber_plan", "hq_tensor_export",
     "hq_tensor_buckets", "hq_tensor_norm_sq",
     "hq_ttmc_core", "hq_ttmctc", "hq_qr_orthonormal", "hq_subspace_distance", "hq_random_factors",
     "hq_config_default", "hq_hoqri", "hq_fit_error",
@@ -151,6 +151,7 @@ def load_library(path: str = None) -> C.CDLL:
     L.hq_tensor_info.argtypes = [vp, C.POINTER(C.c_int), _u64p, C.POINTER(C.c_uint64)]
     L.hq_tensor_mode_plan.argtypes = [vp, C.c_int] + [C.POINTER(C.c_uint64)] * 4 + [C.POINTER(C.c_int),
                                                                                     C.POINTER(C.c_uint64)]
+    L.hq_tensor_fiber_plan.argtypes = [vp, C.c_int] + [C.POINTER(C.c_uint64)] * 3
     L.hq_tensor_export.argtypes = [vp, vp, vp]
     L.hq_tensor_buckets.argtypes = [vp, C.c_int, _u64p, vp]
     L.hq_tensor_norm_sq.argtypes = [vp, C.POINTER(C.c_double)]
@@ -329,6 +330,13 @@ class SparseTensor:
                                                   C.byref(v[4])))
         return dict(rows=v[0].value, nonempty_rows=v[1].value, long_rows=v[2].value, long_segments=v[3].value,
                     hot=bool(hot.value), max_tile32=v[4].value)
+
+    def fiber_plan(self, mode):
+        """Fiber units of one mode's long rows (order 3, skewed tensors): units (0 = not used), long_nnz (the
+        long rows' nonzeros the units cover) and the derived stream's segments."""
+        v = [C.c_uint64() for _ in range(3)]
+        _check(load_library().hq_tensor_fiber_plan(self._h, int(mode), *[C.byref(x) for x in v]))
+        return dict(units=v[0].value, long_nnz=v[1].value, segments=v[2].value)
 
     def _export(self):
         if self._coords is None:

@@ -115,6 +115,30 @@ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 // One mode's view of the tensor: nonzeros in mode-n order (stable counting
 // sort of the lexicographic order == the reference's ModeBuckets.entries,
 // sparse_tensor.cpp:73-89), as SoA streams.
+// Fiber units of a mode's long rows (order 3; hq_pass.cu plan_fibers).  Within a row the stream is sorted by
+// (first other mode, last other mode), so nonzeros sharing the first other index a are contiguous -- a fiber
+// (row, a).  Y_row = sum_fibers U_a[a] (x) t_fiber with t_fiber = sum_{e in fiber} x_e U_b[b_e]: the Kronecker
+// product is formed once per fiber instead of once per nonzero.  Fibers are cut into units of at most
+// kFiberCap nonzeros (bounded work per thread in the unit-sum kernel); the units of a mode form a derived
+// stream (value 1, indices (a, unit id)) that the long-row kernels consume with T = the unit sums as the
+// last factor table.  Built only where it shrinks the long rows' stream by >= 1.5x (skewed tensors).
+constexpr int kFiberCap = 16;
+struct FiberLayout {
+    bool on = false;
+    uint64_t units = 0;
+    uint64_t long_nnz = 0;   // nonzeros of the long rows (units cover exactly these)
+    DBuf<int64_t> start;     // units: stream position of the unit's first nonzero
+    DBuf<uint8_t> len;       // units: nonzeros in the unit (1..kFiberCap)
+    DBuf<int64_t> rowptr;    // rows + 1: unit range of each row (short rows: empty)
+    DBuf<uint32_t> outer;    // units: index into the first other mode's factor
+    DBuf<uint32_t> ident;    // units: 0, 1, 2, ... (the unit's own row of T)
+    DBuf<double> ones;       // units: 1.0
+    uint64_t long_segments = 0;  // the derived stream's long-row plan (same long rows, segments over units)
+    DBuf<int64_t> seg_begin;
+    DBuf<uint32_t> seg_row;
+    DBuf<int64_t> long_seg_ptr;
+};
+
 struct ModeLayout {
     int mode = 0;
     uint64_t rows = 0;                 // I_n
@@ -136,6 +160,7 @@ struct ModeLayout {
     DBuf<int64_t> seg_begin;           // long-row segments: [seg_begin, seg_end) positions
     DBuf<uint32_t> seg_row;            // owning long row (index into long_row_ids)
     DBuf<int64_t> long_seg_ptr;        // long row r owns segments [ptr[r], ptr[r+1])
+    FiberLayout fib;                   // fiber units of the long rows (order 3, skewed tensors)
 };
 
 struct DeviceTensor {

@@ -440,7 +440,7 @@ void build_tensor(DeviceTensor& T, int order, const uint64_t* dims, uint64_t nnz
         HQ_CUDA(cudaStreamSynchronize(s));
         L.nonempty_rows = hc;
         clk.mark("mode streams", m);
-        plan_mode(L, n, s);
+        plan_mode(L, n, order, s);
         clk.mark("mode plan", m);
     }
     HQ_CUDA(cudaStreamSynchronize(s));

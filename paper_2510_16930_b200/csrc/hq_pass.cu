@@ -93,6 +93,124 @@ __global__ void k_long_segments(const int64_t* __restrict__ rowptr, const uint32
     }
 }
 
+
+// ---------------------------------------------------------- fiber units --
+// One CTA per long-row segment (<= kSegLen = 4096 consecutive nonzeros of one row), 16 positions per thread.
+// A position heads a unit when it is the segment's first, when the first other index changes, or every
+// kFiberCap positions inside a fiber.  FILL = false counts the units of each segment; FILL = true writes them
+// at the segment's base (the exclusive scan of the counts): units come out in stream order.
+struct MaxOp {
+    __device__ __forceinline__ int operator()(int a, int b) const { return a > b ? a : b; }
+};
+template <bool FILL>
+__global__ void __launch_bounds__(256) k_fib_units(const int64_t* __restrict__ rowptr, const uint32_t* __restrict__ long_ids,
+                                                   const int64_t* __restrict__ seg_begin, const uint32_t* __restrict__ seg_row,
+                                                   uint64_t nseg, const uint32_t* __restrict__ ia,
+                                                   uint32_t* __restrict__ segcount, const uint32_t* __restrict__ segbase,
+                                                   int64_t* __restrict__ ustart, uint8_t* __restrict__ ulen,
+                                                   uint32_t* __restrict__ outer) {
+    static_assert(kSegLen == 256 * 16, "16 positions per thread");
+    using ScanI = cub::BlockScan<int, 256>;
+    __shared__ typename ScanI::TempStorage tmp;
+    const int t = threadIdx.x;
+    for (uint64_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
+        const int64_t b = seg_begin[sg];
+        const int64_t rend = rowptr[long_ids[seg_row[sg]] + 1];
+        const int n = (int)min((int64_t)kSegLen, rend - b);
+        const int p0 = 16 * t;
+        uint32_t v[17];
+#pragma unroll
+        for (int i = 0; i < 17; ++i) {
+            const int p = p0 + i - 1;
+            v[i] = (p >= 0 && p < n) ? ia[b + p] : 0xffffffffu;
+        }
+        // last fiber head at or before the end of this thread's range (-1: none in range)
+        int last = -1;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int p = p0 + i;
+            if (p < n && (p == 0 || v[i + 1] != v[i])) last = p;
+        }
+        int before;  // last fiber head before this thread's range
+        ScanI(tmp).ExclusiveScan(last, before, -1, MaxOp());
+        __syncthreads();
+        int fstart = before, cnt = 0;
+        unsigned heads = 0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int p = p0 + i;
+            if (p < n) {
+                if (p == 0 || v[i + 1] != v[i]) fstart = p;
+                if ((p - fstart) % kFiberCap == 0) {
+                    heads |= 1u << i;
+                    ++cnt;
+                }
+            }
+        }
+        int base, total;
+        ScanI(tmp).ExclusiveSum(cnt, base, total);
+        __syncthreads();
+        if (!FILL) {
+            if (t == 0) segcount[sg] = (uint32_t)total;
+        } else {
+            // a unit ends at the next head (possibly in a later thread's range) or at the segment end: every
+            // thread publishes its first head position, threads without one forward the next thread's
+            __shared__ int firsthead[257];
+            firsthead[t] = heads ? p0 + (__ffs(heads) - 1) : -1;
+            if (t == 0) firsthead[256] = n;
+            __syncthreads();
+            const size_t ub = (size_t)segbase[sg] + base;
+            int k = 0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                if (heads >> i & 1) {
+                    const int p = p0 + i;
+                    int nx = -1;
+                    const unsigned later = heads >> (i + 1);
+                    if (i < 15 && later) nx = p + __ffs(later);
+                    else {
+                        for (int tt = t + 1; tt <= 256 && nx < 0; ++tt) nx = firsthead[tt];
+                    }
+                    ustart[ub + k] = b + p;
+                    ulen[ub + k] = (uint8_t)(nx - p);
+                    outer[ub + k] = v[i + 1];
+                    ++k;
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+__global__ void k_long_nnz(const int64_t* __restrict__ rowptr, const uint32_t* __restrict__ ids, uint64_t nlong,
+                           unsigned long long* __restrict__ out) {
+    unsigned long long s = 0;
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < nlong; r += (uint64_t)gridDim.x * blockDim.x)
+        s += (unsigned long long)(rowptr[ids[r] + 1] - rowptr[ids[r]]);
+    if (s) atomicAdd(out, s);  // integer: order-independent
+}
+
+// units of long row r = segbase[ptr[r + 1]] - segbase[ptr[r]] -> cnt[row id]; derived segments per long row
+__global__ void k_fib_row_counts(const uint32_t* __restrict__ ids, const int64_t* __restrict__ segptr, uint64_t nlong,
+                                 const uint32_t* __restrict__ segbase, int64_t* __restrict__ cnt,
+                                 uint32_t* __restrict__ nsegf) {
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < nlong; r += (uint64_t)gridDim.x * blockDim.x) {
+        const int64_t c = (int64_t)segbase[segptr[r + 1]] - (int64_t)segbase[segptr[r]];
+        cnt[ids[r]] = c;
+        nsegf[r] = (uint32_t)((c + kSegLen - 1) / kSegLen);
+    }
+}
+__global__ void k_u32_to_i64(const uint32_t* __restrict__ a, uint64_t n, int64_t* __restrict__ b) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        b[i] = (int64_t)a[i];
+}
+__global__ void k_fib_fill(uint64_t n, uint32_t* __restrict__ ident, double* __restrict__ ones) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        ident[i] = (uint32_t)i;
+        ones[i] = 1.0;
+    }
+}
+
 template <class T>
 void exclusive_scan(const T* in, T* out, uint64_t n, cudaStream_t s) {
     size_t tmp = 0;
@@ -107,9 +225,86 @@ inline int grid_for(uint64_t n, int threads = 256) {
     return (int)std::min<uint64_t>(std::max<uint64_t>(b, 1), (uint64_t)num_sms() * 16);
 }
 
+
+// HQ_FIBERS=0 disables the fiber units, =1 builds them whenever a mode has long rows (tests); default: only
+// where they shrink the long rows' stream by >= 1.5x
+int fibers_mode() {
+    const char* e = std::getenv("HQ_FIBERS");
+    if (e && (e[0] == '0' || e[0] == '1')) return e[0] - '0';
+    return -1;
+}
+
+void plan_fibers(ModeLayout& L, cudaStream_t s) {
+    FiberLayout& F = L.fib;
+    F = FiberLayout{};
+    const int fm = fibers_mode();
+    if (fm == 0 || !L.long_rows || !L.idx[0].p) return;
+    const uint64_t nseg = L.long_segments, nlong = L.long_rows;
+    DBuf<uint32_t> segcount, segbase;
+    DBuf<unsigned long long> lnz;
+    segcount.alloc(nseg + 1);
+    segbase.alloc(nseg + 1);
+    lnz.alloc(1);
+    HQ_CUDA(cudaMemsetAsync(lnz.get(), 0, 8, s));
+    HQ_CUDA(cudaMemsetAsync(segcount.get() + nseg, 0, 4, s));
+    k_long_nnz<<<grid_for(nlong), 256, 0, s>>>(L.rowptr.get(), L.long_row_ids.get(), nlong, lnz.get());
+    const int g = (int)std::min<uint64_t>(nseg, (uint64_t)num_sms() * 8);
+    k_fib_units<false><<<g, 256, 0, s>>>(L.rowptr.get(), L.long_row_ids.get(), L.seg_begin.get(), L.seg_row.get(), nseg,
+                                         L.idx[0].get(), segcount.get(), nullptr, nullptr, nullptr, nullptr);
+    HQ_CHECK_LAUNCH();
+    exclusive_scan(segcount.get(), segbase.get(), nseg + 1, s);  // segbase[nseg] = the unit count
+    uint32_t units = 0;
+    unsigned long long long_nnz = 0;
+    HQ_CUDA(cudaMemcpyAsync(&units, segbase.get() + nseg, 4, cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaMemcpyAsync(&long_nnz, lnz.get(), 8, cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaStreamSynchronize(s));
+    if (!units || (fm != 1 && (double)long_nnz < 1.5 * (double)units)) return;
+    F.units = units;
+    F.long_nnz = long_nnz;
+    F.start.alloc(units);
+    F.len.alloc(units);
+    F.outer.alloc((size_t)units + 4);
+    F.ident.alloc((size_t)units + 4);
+    F.ones.alloc((size_t)units + 2);
+    k_fib_units<true><<<g, 256, 0, s>>>(L.rowptr.get(), L.long_row_ids.get(), L.seg_begin.get(), L.seg_row.get(), nseg,
+                                        L.idx[0].get(), nullptr, segbase.get(), F.start.get(), F.len.get(),
+                                        F.outer.get());
+    HQ_CHECK_LAUNCH();
+    k_fib_fill<<<grid_for(units), 256, 0, s>>>(units, F.ident.get(), F.ones.get());
+    // unit range of every row, and the derived stream's segments
+    DBuf<int64_t> cnt;
+    DBuf<uint32_t> nsegf, segposf;
+    cnt.alloc(L.rows + 1);
+    nsegf.alloc(nlong);
+    segposf.alloc(nlong);
+    HQ_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(int64_t) * (L.rows + 1), s));
+    k_fib_row_counts<<<grid_for(nlong), 256, 0, s>>>(L.long_row_ids.get(), L.long_seg_ptr.get(), nlong, segbase.get(),
+                                                    cnt.get(), nsegf.get());
+    HQ_CHECK_LAUNCH();
+    F.rowptr.alloc(L.rows + 1);
+    exclusive_scan(cnt.get(), F.rowptr.get(), L.rows + 1, s);
+    exclusive_scan(nsegf.get(), segposf.get(), nlong, s);
+    uint32_t sp = 0, sn = 0;
+    HQ_CUDA(cudaMemcpyAsync(&sp, segposf.get() + nlong - 1, 4, cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaMemcpyAsync(&sn, nsegf.get() + nlong - 1, 4, cudaMemcpyDeviceToHost, s));
+    HQ_CUDA(cudaStreamSynchronize(s));
+    F.long_segments = (uint64_t)sp + sn;
+    F.long_seg_ptr.alloc(nlong + 1);
+    F.seg_begin.alloc(F.long_segments);
+    F.seg_row.alloc(F.long_segments);
+    k_u32_to_i64<<<grid_for(nlong), 256, 0, s>>>(segposf.get(), nlong, F.long_seg_ptr.get());
+    const int64_t tail = (int64_t)F.long_segments;
+    HQ_CUDA(cudaMemcpyAsync(F.long_seg_ptr.get() + nlong, &tail, 8, cudaMemcpyHostToDevice, s));
+    k_long_segments<<<grid_for(nlong), 256, 0, s>>>(F.rowptr.get(), L.long_row_ids.get(), F.long_seg_ptr.get(), nlong,
+                                                   F.seg_begin.get(), F.seg_row.get());
+    HQ_CHECK_LAUNCH();
+    HQ_CUDA(cudaStreamSynchronize(s));
+    F.on = true;
+}
+
 }  // namespace
 
-void plan_mode(ModeLayout& L, uint64_t nnz, cudaStream_t s) {
+void plan_mode(ModeLayout& L, uint64_t nnz, int order, cudaStream_t s) {
     const uint64_t rows = L.rows;
     DBuf<uint32_t> flag, nseg, pos, segpos;
     DBuf<unsigned long long> hot;
@@ -157,6 +352,8 @@ void plan_mode(ModeLayout& L, uint64_t nnz, cudaStream_t s) {
         HQ_CHECK_LAUNCH();
         HQ_CUDA(cudaStreamSynchronize(s));
     }
+    L.fib = FiberLayout{};
+    if (order == 3) plan_fibers(L, s);
 }
 
 // ------------------------------------------------------- generic kernels --
@@ -384,6 +581,90 @@ void set_smem(const void* fn, size_t bytes) {
     if (bytes > 48 * 1024) HQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
+
+// ---- fiber unit sums: T[u] = sum_{e in unit u} x_e U_b[b_e]  (one thread per unit, <= kFiberCap nonzeros).
+// SM = true: the whole last-mode factor is first copied into shared memory (small extents: every gather
+// is a shared-memory read); otherwise rows are read through L1 (hot rows of a skewed factor stay there).
+template <int KB, bool SM>
+__global__ void __launch_bounds__(SM ? (KB > 10 ? 512 : 1024) : 256)
+    k_unit_sums(const int64_t* __restrict__ ustart, const uint8_t* __restrict__ ulen, const int64_t* __restrict__ rowptr_f,
+                uint64_t rbase, uint64_t rows, const double* __restrict__ val, const uint32_t* __restrict__ ib,
+                const double* __restrict__ ub, uint64_t ub_rows, double* __restrict__ T, const DevStatus* st,
+                int run_if) {
+    if (skip_kernel(st, run_if)) return;
+    extern __shared__ __align__(16) double tab[];
+    if (SM) {
+        const double2* src = reinterpret_cast<const double2*>(ub);
+        double2* dst = reinterpret_cast<double2*>(tab);
+        for (size_t q = threadIdx.x; q < ub_rows * KB / 2; q += blockDim.x) dst[q] = src[q];
+        __syncthreads();
+    }
+    const double* base = SM ? tab : ub;
+    const int64_t u0 = rowptr_f[rbase], u1 = rowptr_f[rbase + rows];
+    for (int64_t u = u0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < u1; u += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e0 = ustart[u];
+        const int n = ulen[u];
+        double t[KB];
+#pragma unroll
+        for (int q = 0; q < KB; ++q) t[q] = 0.0;
+        double x = val[e0];
+        uint32_t r = ib[e0];
+        for (int i = 0; i < n; ++i) {
+            const double xc = x;
+            const double2* row = reinterpret_cast<const double2*>(base + (size_t)r * KB);
+            if (i + 1 < n) {  // next record's stream loads under this record's row loads
+                x = val[e0 + i + 1];
+                r = ib[e0 + i + 1];
+            }
+#pragma unroll
+            for (int q = 0; q < KB / 2; ++q) {
+                const double2 d = SM ? row[q] : __ldg(row + q);
+                t[2 * q] = fma(xc, d.x, t[2 * q]);
+                t[2 * q + 1] = fma(xc, d.y, t[2 * q + 1]);
+            }
+        }
+        double2* o = reinterpret_cast<double2*>(T + (size_t)u * KB);
+#pragma unroll
+        for (int q = 0; q < KB / 2; ++q) o[q] = make_double2(t[2 * q], t[2 * q + 1]);
+    }
+}
+
+template <int KB>
+void launch_unit_sums_k(const ModeLayout& L, uint64_t rbase, uint64_t rows, const double* ub, uint64_t ub_rows,
+                        double* T, const DevStatus* st, int run_if, cudaStream_t s) {
+    const FiberLayout& F = L.fib;
+    const size_t tab = (size_t)ub_rows * KB * sizeof(double);
+    if (tab <= 200 * 1024) {
+        static bool attr = false;
+        if (!attr) {
+            HQ_CUDA(cudaFuncSetAttribute(k_unit_sums<KB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            attr = true;
+        }
+        k_unit_sums<KB, true><<<num_sms(), KB > 10 ? 512 : 1024, tab, s>>>(F.start.get(), F.len.get(), F.rowptr.get(), rbase, rows,
+                                                          L.val.get(), L.idx[1].get(), ub, ub_rows, T, st, run_if);
+    } else {
+        k_unit_sums<KB, false><<<num_sms() * 8, 256, 0, s>>>(F.start.get(), F.len.get(), F.rowptr.get(), rbase, rows,
+                                                            L.val.get(), L.idx[1].get(), ub, ub_rows, T, st, run_if);
+    }
+    HQ_CHECK_LAUNCH();
+}
+
+bool unit_sums_supported(int kb) { return kb == 8 || kb == 10 || kb == 16; }
+
+void launch_unit_sums(int kb, const ModeLayout& L, uint64_t rbase, uint64_t rows, const double* ub, uint64_t ub_rows,
+                      double* T, const DevStatus* st, int run_if, cudaStream_t s) {
+    if (kb == 8) launch_unit_sums_k<8>(L, rbase, rows, ub, ub_rows, T, st, run_if, s);
+    else if (kb == 10) launch_unit_sums_k<10>(L, rbase, rows, ub, ub_rows, T, st, run_if, s);
+    else if (kb == 16) launch_unit_sums_k<16>(L, rbase, rows, ub, ub_rows, T, st, run_if, s);
+    else fail(HQ_ERR_INTERNAL, "no unit-sum kernel for this rank");
+}
+
+// the long rows go through their fiber units when the layout has them and the shape has the kernels
+bool fibers_fit(const ModeLayout& L, const ModeShape& sh) {
+    return L.fib.on && sh.order == 3 && long_fast_supported(sh) && unit_sums_supported(sh.ko[1]);
+}
+bool use_fibers(const ModeLayout& L, const ModeShape& sh) { return fibers_fit(L, sh) && !force_generic(); }
+
 }  // namespace
 
 int tile_grid(const ModeShape& sh) {
@@ -400,7 +681,10 @@ int pass_slots(const ModeLayout& L, const ModeShape& sh) {
     return short_slots(L, sh) + (L.long_rows ? long_grid(L) : 0);
 }
 
-size_t pass_ypart_doubles(const ModeLayout& L, const ModeShape& sh) { return (size_t)L.long_segments * sh.L; }
+// scratch of a pass: the long-row segment partials, then (fiber units) the unit sums T
+size_t pass_ypart_doubles(const ModeLayout& L, const ModeShape& sh) {
+    return (size_t)L.long_segments * sh.L + (fibers_fit(L, sh) ? (size_t)L.fib.units * sh.ko[1] + 2 : 0);
+}
 
 int pass_launch_count(const ModeLayout& L, const ModeShape& sh) {
     return (short_slots(L, sh) ? 1 : 0) + (L.long_rows ? 2 : 0);
@@ -509,6 +793,22 @@ void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const Fac
         la.slot0 = short_slots(L, sh);
         la.st = st;
         la.run_if = run_if;
+        if (use_fibers(L, sh)) {
+            // fiber units: T = the unit sums over the last other mode, then the long-row kernels run on the
+            // derived stream (value 1, indices (first other index, unit id)) with T as the last factor table
+            double* Tu = out.ypart + (size_t)L.long_segments * sh.L;
+            launch_unit_sums(sh.ko[1], L, a.rbase, a.rows, a.uo[1], T.dims[L.others[1]], Tu, st, run_if, s);
+            la.rowptr = L.fib.rowptr.get();
+            la.val = L.fib.ones.get();
+            la.i0 = L.fib.outer.get();
+            la.i1 = L.fib.ident.get();
+            la.u1 = Tu;
+            la.l1_1 = false;
+            la.long_segptr = L.fib.long_seg_ptr.get();
+            la.seg_begin = L.fib.seg_begin.get();
+            la.seg_row = L.fib.seg_row.get();
+            la.nseg = L.fib.long_segments;
+        }
         launch_long_fast(la, sh, long_grid(L), s);
     } else if (L.long_rows) {
         int segs = (int)std::min<uint64_t>(L.long_segments, (uint64_t)num_sms() * 8);

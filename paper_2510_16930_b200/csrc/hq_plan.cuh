@@ -17,7 +17,7 @@ namespace hq {
 constexpr int64_t kShortMax = HQ_SHORT_MAX;
 constexpr int64_t kSegLen = 4096;
 
-void plan_mode(ModeLayout& L, uint64_t nnz, cudaStream_t s);
+void plan_mode(ModeLayout& L, uint64_t nnz, int order, cudaStream_t s);
 
 double device_sum_sq(const double* v, uint64_t n, cudaStream_t s);
 // vals_ready (optional): the values are still arriving (an H2D copy on another stream that records this

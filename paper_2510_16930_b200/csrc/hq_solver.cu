@@ -1002,6 +1002,17 @@ int hq_tensor_mode_plan(const hq_tensor* t, int mode, uint64_t* rows, uint64_t* 
     });
 }
 
+int hq_tensor_fiber_plan(const hq_tensor* t, int mode, uint64_t* units, uint64_t* long_nnz, uint64_t* segments) {
+    return guard([&] {
+        if (mode < 0 || mode >= t->t.order)
+            fail(HQ_ERR_RANGE, "mode " + std::to_string(mode) + " out of range for order " + std::to_string(t->t.order));
+        const FiberLayout& F = t->t.modes[mode].fib;
+        if (units) *units = F.on ? F.units : 0;
+        if (long_nnz) *long_nnz = F.on ? F.long_nnz : 0;
+        if (segments) *segments = F.on ? F.long_segments : 0;
+    });
+}
+
 int hq_tensor_export(const hq_tensor* t, uint32_t* coords, double* values) {
     return guard([&] {
         require_unsharded(t->t, "hq_tensor_export");

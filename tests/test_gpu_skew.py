@@ -86,3 +86,75 @@ def test_all_long_rows_with_empty_rows(oracle, k):
     np.testing.assert_allclose(obj, ro["objective"], rtol=1e-9)
     rel = np.linalg.norm(r.model.core.data - ro["core"].reshape(-1)) / np.linalg.norm(ro["core"])
     assert rel <= 1e-9, rel
+
+
+# ---- fiber units (hq_pass.cu plan_fibers): the long rows' Kronecker products taken once per fiber
+
+
+def _with_fibers(flag, fn):
+    import os
+    old = os.environ.get("HQ_FIBERS")
+    os.environ["HQ_FIBERS"] = flag
+    try:
+        return fn()
+    finally:
+        if old is None:
+            del os.environ["HQ_FIBERS"]
+        else:
+            os.environ["HQ_FIBERS"] = old
+
+
+def test_fiber_units_cover_the_long_rows():
+    coords, vals = zipf_coo(DIMS, 300000, 3)
+    x = _with_fibers("1", lambda: hq.SparseTensor(DIMS, coords, vals))
+    off = _with_fibers("0", lambda: hq.SparseTensor(DIMS, coords, vals))
+    c = x.coords()
+    for m in range(3):
+        p, f = x.mode_plan(m), x.fiber_plan(m)
+        cnt = np.bincount(c[:, m], minlength=DIMS[m])
+        long_nnz = int(cnt[cnt > 256].sum())
+        assert f["long_nnz"] == long_nnz and p["long_rows"] == int((cnt > 256).sum())
+        # units = sum over fibers (row, first other index) of the long rows of ceil(len / 16)
+        o = [v for v in range(3) if v != m][0]
+        sel = cnt[c[:, m]] > 256
+        key = c[sel, m].astype(np.int64) * DIMS[o] + c[sel, o]
+        _, lens = np.unique(key, return_counts=True)
+        lo = int(np.ceil(lens / 16).sum())
+        # a fiber that straddles a 4096-nonzero segment boundary is cut there: at most one more unit per segment
+        assert lo <= f["units"] <= lo + p["long_segments"], (m, f, lo)
+        assert 1 <= f["segments"] <= p["long_segments"]
+        assert off.fiber_plan(m)["units"] == 0
+
+
+@pytest.mark.parametrize("k", [10, 16, 8])
+def test_fiber_units_match_oracle_and_plain_long_rows(oracle, k):
+    coords, vals = zipf_coo(DIMS, 300000, 3)
+    u = hq.random_factors(DIMS, [k] * 3, 21)
+    res = {}
+    for flag in ("1", "0"):
+        x = _with_fibers(flag, lambda: hq.SparseTensor(DIMS, coords, vals))
+        assert (x.fiber_plan(1)["units"] > 0) == (flag == "1")
+        core = hq.ttmc_core(x, u)
+        res[flag] = [core.data] + [hq.ttmctc_elementwise(x, u, m, core) for m in range(3)]
+        if flag == "1":
+            oc = oracle.ttmc_core(DIMS, [k] * 3, x.coords(), x.values(), u.factors).reshape(-1)
+            assert np.abs(core.data - oc).max() <= 1e-11 * max(1.0, np.abs(oc).max())
+            for m in range(3):
+                ao = oracle.ttmctc(DIMS, [k] * 3, x.coords(), x.values(), u.factors, m, core.data)
+                assert np.abs(res[flag][1 + m] - ao).max() <= 1e-11 * max(1.0, np.abs(ao).max()), m
+                assert (res[flag][1 + m] == hq.ttmctc_elementwise(x, u, m, core)).all()  # bitwise repeatable
+    for a, b in zip(res["1"], res["0"]):
+        assert np.abs(a - b).max() <= 1e-11 * max(1.0, np.abs(b).max())
+
+
+def test_fiber_units_hoqri_matches_oracle(oracle):
+    coords, vals = zipf_coo(DIMS, 300000, 3)
+    x = _with_fibers("1", lambda: hq.SparseTensor(DIMS, coords, vals))
+    sweeps = 4
+    u0 = oracle.random_factors(DIMS, [K] * 3, 13)
+    r = hq.hoqri(x, hq.SolverConfig(ranks=[K] * 3, max_sweeps=sweeps, tol_fit_change=0.0), init_factors=u0)
+    ro = oracle.hoqri(DIMS, [K] * 3, x.coords(), x.values(), u0, sweeps)
+    rel = np.linalg.norm(r.model.core.data - ro["core"].reshape(-1)) / np.linalg.norm(ro["core"])
+    assert rel <= 1e-9, rel
+    obj = np.array([s.objective for s in r.trace.sweeps])
+    np.testing.assert_allclose(obj, ro["objective"], rtol=1e-9, atol=0)

@@ -83,9 +83,11 @@ int hq_tensor_mode_plan(const hq_tensor* t, int mode, uint64_t* rows, uint64_t* 
 /* fiber units of a mode's long rows (order 3, skewed tensors; engine-only, no reference counterpart): within a
    row the nonzeros sharing the first other index form a fiber, whose Kronecker product is taken once
    (kernels.cpp:86-163 takes it per nonzero; same sum, regrouped).  units = 0 when the mode does not use them;
-   long_nnz / units is the factor by which the long rows' stream shrinks.  HQ_FIBERS=0/1 (read when the
-   tensor is built) disables / forces them. */
-int hq_tensor_fiber_plan(const hq_tensor* t, int mode, uint64_t* units, uint64_t* long_nnz, uint64_t* segments);
+   long_nnz / units is the factor by which the long rows' stream shrinks; short_max = the mode's long-row
+   threshold (256; 64 for a skewed mode that uses the units).  HQ_FIBERS=0/1 (read when the tensor is built)
+   disables / forces them. */
+int hq_tensor_fiber_plan(const hq_tensor* t, int mode, uint64_t* units, uint64_t* long_nnz, uint64_t* segments,
+                         uint64_t* short_max);
 /* sorted, merged entries (sparse_tensor.hpp:44-51): coords nnz*order, values nnz */
 int hq_tensor_export(const hq_tensor* t, uint32_t* coords, double* values);
 /* ModeBuckets (sparse_tensor.hpp:25-32): offsets dims[mode]+1, entries nnz */

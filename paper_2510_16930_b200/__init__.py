@@ -151,7 +151,7 @@ def load_library(path: str = None) -> C.CDLL:
     L.hq_tensor_info.argtypes = [vp, C.POINTER(C.c_int), _u64p, C.POINTER(C.c_uint64)]
     L.hq_tensor_mode_plan.argtypes = [vp, C.c_int] + [C.POINTER(C.c_uint64)] * 4 + [C.POINTER(C.c_int),
                                                                                     C.POINTER(C.c_uint64)]
-    L.hq_tensor_fiber_plan.argtypes = [vp, C.c_int] + [C.POINTER(C.c_uint64)] * 3
+    L.hq_tensor_fiber_plan.argtypes = [vp, C.c_int] + [C.POINTER(C.c_uint64)] * 4
     L.hq_tensor_export.argtypes = [vp, vp, vp]
     L.hq_tensor_buckets.argtypes = [vp, C.c_int, _u64p, vp]
     L.hq_tensor_norm_sq.argtypes = [vp, C.POINTER(C.c_double)]
@@ -333,10 +333,11 @@ class SparseTensor:
 
     def fiber_plan(self, mode):
         """Fiber units of one mode's long rows (order 3, skewed tensors): units (0 = not used), long_nnz (the
-        long rows' nonzeros the units cover) and the derived stream's segments."""
-        v = [C.c_uint64() for _ in range(3)]
+        long rows' nonzeros the units cover), the derived stream's segments, and short_max (the mode's
+        long-row threshold)."""
+        v = [C.c_uint64() for _ in range(4)]
         _check(load_library().hq_tensor_fiber_plan(self._h, int(mode), *[C.byref(x) for x in v]))
-        return dict(units=v[0].value, long_nnz=v[1].value, segments=v[2].value)
+        return dict(units=v[0].value, long_nnz=v[1].value, segments=v[2].value, short_max=v[3].value)
 
     def _export(self):
         if self._coords is None:

@@ -26,6 +26,7 @@ struct FastArgs {
     int run_if;
     int a_only;           // standalone TTMcTC (kTTMcTCOnly): A only, no M / W partials
     int l1_a, l1_b;       // L1-allocating gathers for a hot (skewed) factor (ModeLayout::hot)
+    int short_max;        // rows with more nonzeros are long rows (ModeLayout::short_max <= kShortMax)
 };
 
 void debug_phase_cycles(unsigned long long* out, int reset);

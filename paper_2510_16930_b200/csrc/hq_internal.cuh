@@ -122,7 +122,10 @@ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 // kFiberCap nonzeros (bounded work per thread in the unit-sum kernel); the units of a mode form a derived
 // stream (value 1, indices (a, unit id)) that the long-row kernels consume with T = the unit sums as the
 // last factor table.  Built only where it shrinks the long rows' stream by >= 1.5x (skewed tensors).
-constexpr int kFiberCap = 16;
+#ifndef HQ_FIBER_CAP
+#define HQ_FIBER_CAP 16
+#endif
+constexpr int kFiberCap = HQ_FIBER_CAP;
 struct FiberLayout {
     bool on = false;
     uint64_t units = 0;
@@ -137,6 +140,7 @@ struct FiberLayout {
     DBuf<int64_t> seg_begin;
     DBuf<uint32_t> seg_row;
     DBuf<int64_t> long_seg_ptr;
+    DBuf<int64_t> seg_cost;  // segments + 1: prefix sums of the segments' cost (units and nonzeros) -- CTA ranges
 };
 
 struct ModeLayout {
@@ -154,6 +158,7 @@ struct ModeLayout {
     bool hot = false;
     uint64_t max_tile32 = 0;  // most short-row nonzeros in one 32-row tile (the pass kernels' tile)
     // work plan (see hq_pass.cu)
+    int64_t short_max = 256;           // rows with more nonzeros are long (kShortMax; lower where fiber units run)
     uint64_t long_rows = 0;
     DBuf<uint32_t> long_row_ids;       // rows with more than kShortMax nonzeros
     uint64_t long_segments = 0;

@@ -21,6 +21,29 @@
 
 #include "hq_long.cuh"
 
+// Debug instrumentation: -DHQ_PHASE_TIMING accumulates per-phase cycles of thread 0 of every k_fibseg CTA
+// (read back with hq_debug_fib_phase_cycles); compiled out otherwise.
+#ifdef HQ_PHASE_TIMING
+__device__ unsigned long long hq_fib_phase_cycles[16];
+#define HQ_FPHASE(i)                                                                   \
+    do {                                                                               \
+        if (threadIdx.x == 0) {                                                        \
+            long long _now = clock64();                                                \
+            atomicAdd(&hq_fib_phase_cycles[i], (unsigned long long)(_now - _ph_t));    \
+            _ph_t = _now;                                                              \
+        }                                                                              \
+    } while (0)
+#else
+#define HQ_FPHASE(i) do { } while (0)
+#endif
+
+#ifndef HQ_FIB_DIVFREE
+#define HQ_FIB_DIVFREE 1
+#endif
+#ifndef HQ_FIB_UNROLL
+#define HQ_FIB_UNROLL 0
+#endif
+
 namespace hq {
 
 namespace {
@@ -338,6 +361,272 @@ __global__ void __launch_bounds__(256) k_longseg_sync(LongArgs a) {
     }
 }
 
+
+// ------------------------------------------------------------ fiber units --
+// Segment kernel over a mode's fiber units (FiberLayout, hq_internal.cuh): a unit is <= kFiberCap consecutive
+// nonzeros of one row that share the first other index a, so
+//   Y_row = sum_units U_a[a] (x) t_unit,   t_unit = sum_{e in unit} x_e U_b[b_e].
+// The Kronecker product costs one DMMA column per unit instead of one per nonzero.  A chunk is the next
+// <= CH units of a segment holding <= NCAP nonzeros (cold fibers: 128 units, hot fibers: NCAP / 16); one
+// chunk at a time per CTA, three CTAs per SM overlap each other's phases:
+//   1. the chunk's nonzeros are one contiguous slice of the value / last-index streams, already staged (it
+//      was requested a chunk ahead, as were the unit records, held in registers);
+//   2. gathers: the units' U_a rows and the nonzeros' U_b rows, all in flight at once (16-byte cp.async);
+//      the next chunk's slice behind them;
+//   3. unit sums from shared memory (one thread per unit and column pair) into the row buffer next to U_a;
+//   4. the DMMA k-steps of k_longseg (S^T V, k = 4 units per step) and its fixed-order reduction into
+//      ypart[segment] at a segment's last chunk.
+template <int K0, int K1>
+struct FS_ {
+    using S = LS_<K0, K1, 0>;
+    static constexpr int CH = 128;    // most units of a chunk
+    static constexpr int NCAP = kFiberCap <= 4 ? 512 : 448;  // most nonzeros of a chunk (three CTAs per SM at K = 10)
+    static constexpr int RW = K0 + K1;
+    static constexpr int FW = RW + (12 - RW % 8) % 8;  // row stride = 4 mod 8 doubles (conflict-free k-step loads)
+    static constexpr int PM0 = K0 / 2, PM1 = K1 / 2;
+    static constexpr size_t row_doubles = (size_t)CH * FW, ub_doubles = (size_t)NCAP * K1;
+    static_assert(NCAP >= kFiberCap && FW % 8 == 4, "chunk / row layout");
+    static_assert(S::red_doubles <= ub_doubles, "the reduction buffer aliases the staged U_b rows");
+    static constexpr size_t smem = (row_doubles + ub_doubles + 2 * (size_t)NCAP) * 8 + 2 * (size_t)NCAP * 4 +
+                                   (size_t)CH * 4 + (size_t)(CH + 4) * 4;
+};
+
+template <int K0, int K1>
+__device__ __forceinline__ void kstep_fib(const double* f, int ks, int n, int gid, int tig,
+                                          double (&acc)[LS_<K0, K1, 0>::MT][LS_<K0, K1, 0>::NTL][2]) {
+    using S = LS_<K0, K1, 0>;
+    constexpr int FW = FS_<K0, K1>::FW;
+    const int e = ks * 4 + tig;
+    const bool ev = e < n;
+    const double* fe = f + (size_t)e * FW;
+    double bv[S::NTL];
+#pragma unroll
+    for (int nt = 0; nt < S::NTL; ++nt) {
+        const int col = nt * 8 + gid;
+        bv[nt] = (ev && col < K1) ? fe[K0 + col] : 0.0;
+    }
+#pragma unroll
+    for (int mt = 0; mt < S::MT; ++mt) {
+        const int col = mt * 8 + gid;
+        const double av = (ev && col < K0) ? fe[col] : 0.0;
+#pragma unroll
+        for (int nt = 0; nt < S::NTL; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], av, bv[nt]);
+    }
+}
+
+template <int K0, int K1>
+__global__ void __launch_bounds__(256) k_fibseg(LongArgs a) {
+    using S = LS_<K0, K1, 0>;
+    using F = FS_<K0, K1>;
+    if (skip_kernel(a.st, a.run_if)) return;
+    extern __shared__ __align__(16) double sm[];
+    double* rowbuf = sm;                                   // [CH][FW]: U_a row, t
+    double* ubuf = rowbuf + F::row_doubles;                // [NCAP][K1] staged U_b rows; then the reduction buffer
+    double* red = ubuf;
+    double* nzx = ubuf + F::ub_doubles;                    // [2][NCAP] staged values
+    uint32_t* nzi = reinterpret_cast<uint32_t*>(nzx + 2 * F::NCAP);  // [2][NCAP] staged last-mode indices
+    uint32_t* rec = nzi + 2 * F::NCAP;                     // [CH] first other index of each unit
+    int* uoff = reinterpret_cast<int*>(rec + F::CH);       // [CH + 1] unit offsets into the staged slice
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gid = lane >> 2, tig = lane & 3;
+    const uint64_t G = gridDim.x, c = blockIdx.x;
+    const uint64_t rend = a.rbase + a.rows;
+    const int64_t nz_end = a.rowptr_nz[rend];
+    // CTAs take contiguous segment ranges of equal cost (units + nonzeros: segments of hot fibers carry up
+    // to kFiberCap times the nonzeros of cold ones)
+    auto lower = [&](int64_t z) {
+        uint64_t lo = 0, hi = a.nseg;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (a.seg_cost[mid] >= z) hi = mid; else lo = mid + 1;
+        }
+        return lo;
+    };
+    const int64_t Z = a.seg_cost[a.nseg], Zq = Z / (int64_t)G, Zr = Z % (int64_t)G;
+    ChunkCursor cc{lower(Zq * (int64_t)c + Zr * (int64_t)c / (int64_t)G),
+                   c + 1 == G ? a.nseg : lower(Zq * (int64_t)(c + 1) + Zr * (int64_t)(c + 1) / (int64_t)G), 0, 0};
+    cc.seek(a, rend);
+    double acc[S::MT][S::NTL][2];
+#pragma unroll
+    for (int i = 0; i < S::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < S::NTL; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    // unit records of a chunk's candidate units (threads < CH), held in registers a chunk ahead
+    struct Units {
+        uint32_t out;
+        int64_t st, base;
+        int ln;
+    };
+    auto load_units = [&](const ChunkCursor& k) {
+        Units r{0u, 0, 0, 0};
+        if (k.valid()) {
+            r.base = a.ustart[k.z0];
+            if (tid < k.n(F::CH)) {
+                r.out = a.i0[k.z0 + tid];
+                r.st = a.ustart[k.z0 + tid];
+                r.ln = a.ulen[k.z0 + tid];
+            }
+        }
+        return r;
+    };
+    auto stage_slice = [&](int64_t base, int b) {  // the next NCAP stream positions from base (clamped to the rows)
+        const int lim = (int)min((int64_t)F::NCAP, nz_end - base);
+        double* x = nzx + (size_t)b * F::NCAP;
+        uint32_t* ix = nzi + (size_t)b * F::NCAP;
+        for (int q = tid; q < lim; q += S::THREADS) {
+            cpa8(x + q, a.val + base + q);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr(ix + q)), "l"(a.i1 + base + q));
+        }
+    };
+    Units cur = load_units(cc);
+    if (cc.valid()) stage_slice(cur.base, 0);
+    cpa_commit();
+    int buf = 0;
+#ifdef HQ_PHASE_TIMING
+    long long _ph_t = clock64();
+#endif
+    while (cc.valid()) {
+        const int cand = cc.n(F::CH);
+        const int off_end = (int)(cur.st + cur.ln - cur.base);
+        const int n = __syncthreads_count(tid < cand && off_end <= F::NCAP);  // >= 1: a unit has <= kFiberCap nonzeros
+        if (tid < n) {
+            rec[tid] = cur.out;
+            uoff[tid] = (int)(cur.st - cur.base);
+            if (tid == n - 1) uoff[n] = off_end;
+        }
+        const bool seg_last = cc.last(n);
+        const uint64_t sg = cc.sg;
+        ChunkCursor nx = cc;
+        nx.advance(a, rend, n);
+        const Units nxt = load_units(nx);
+        HQ_FPHASE(0);
+        cpa_wait<0>();  // this chunk's slice (requested a chunk ahead)
+        __syncthreads();
+        HQ_FPHASE(1);
+        const int nn = uoff[n];
+        const double* x = nzx + (size_t)buf * F::NCAP;
+        const uint32_t* ix = nzi + (size_t)buf * F::NCAP;
+#if HQ_FIB_DIVFREE
+        {  // 16-byte pieces, PM consecutive threads per row; (row, piece) advanced without divisions
+            constexpr int DE0 = S::THREADS / F::PM0, DP0 = S::THREADS % F::PM0;
+            int e = tid / F::PM0, p = tid - e * F::PM0;
+            while (e < n) {
+                double* d = rowbuf + (size_t)e * F::FW + 2 * p;
+                const double* src = a.u0 + (size_t)rec[e] * K0 + 2 * p;
+                if (a.l1_0) cpa16_l1(d, src);
+                else cpa16(d, src);
+                e += DE0;
+                p += DP0;
+                if (p >= F::PM0) {
+                    p -= F::PM0;
+                    ++e;
+                }
+            }
+            constexpr int DE1 = S::THREADS / F::PM1, DP1 = S::THREADS % F::PM1;
+            e = tid / F::PM1;
+            p = tid - e * F::PM1;
+            while (e < nn) {
+                double* d = ubuf + (size_t)e * K1 + 2 * p;
+                const double* src = a.u1 + (size_t)ix[e] * K1 + 2 * p;
+                if (a.l1_1) cpa16_l1(d, src);
+                else cpa16(d, src);
+                e += DE1;
+                p += DP1;
+                if (p >= F::PM1) {
+                    p -= F::PM1;
+                    ++e;
+                }
+            }
+        }
+#else
+        for (int q = tid; q < n * F::PM0; q += S::THREADS) {
+            const int e = q / F::PM0, p = q - e * F::PM0;
+            double* d = rowbuf + (size_t)e * F::FW + 2 * p;
+            const double* src = a.u0 + (size_t)rec[e] * K0 + 2 * p;
+            if (a.l1_0) cpa16_l1(d, src);
+            else cpa16(d, src);
+        }
+        for (int q = tid; q < nn * F::PM1; q += S::THREADS) {
+            const int e = q / F::PM1, p = q - e * F::PM1;
+            double* d = ubuf + (size_t)e * K1 + 2 * p;
+            const double* src = a.u1 + (size_t)ix[e] * K1 + 2 * p;
+            if (a.l1_1) cpa16_l1(d, src);
+            else cpa16(d, src);
+        }
+#endif
+        cpa_commit();
+        HQ_FPHASE(2);
+        if (nx.valid()) stage_slice(nxt.base, buf ^ 1);
+        cpa_commit();
+        HQ_FPHASE(3);
+        cpa_wait<1>();  // the gathers; the next slice stays in flight
+        __syncthreads();
+        HQ_FPHASE(4);
+        for (int w = tid; w < n * F::PM1; w += S::THREADS) {
+            const int u = w / F::PM1, p = w - u * F::PM1;
+            double t0 = 0.0, t1 = 0.0;
+            const int e1 = uoff[u + 1];
+#if HQ_FIB_UNROLL
+            for (int e = uoff[u]; e < e1; e += 4) {  // four nonzeros' loads in flight, summed in stream order
+                double xs[4];
+                double2 ds[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (e + i < e1) {
+                        xs[i] = x[e + i];
+                        ds[i] = *reinterpret_cast<const double2*>(ubuf + (size_t)(e + i) * K1 + 2 * p);
+                    }
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (e + i < e1) {
+                        t0 = fma(xs[i], ds[i].x, t0);
+                        t1 = fma(xs[i], ds[i].y, t1);
+                    }
+            }
+#else
+            for (int e = uoff[u]; e < e1; ++e) {
+                const double xe = x[e];
+                const double2 d = *reinterpret_cast<const double2*>(ubuf + (size_t)e * K1 + 2 * p);
+                t0 = fma(xe, d.x, t0);
+                t1 = fma(xe, d.y, t1);
+            }
+#endif
+            *reinterpret_cast<double2*>(rowbuf + (size_t)u * F::FW + K0 + 2 * p) = make_double2(t0, t1);
+        }
+        __syncthreads();
+        HQ_FPHASE(5);
+        for (int ks = warp; ks < (n + 3) / 4; ks += S::WARPS) kstep_fib<K0, K1>(rowbuf, ks, n, gid, tig, acc);
+        HQ_FPHASE(6);
+        if (seg_last) {
+            double* rw = red + (size_t)warp * S::MT * S::NTL * 64;
+#pragma unroll
+            for (int mt = 0; mt < S::MT; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < S::NTL; ++nt) {
+                    rw[(mt * S::NTL + nt) * 64 + gid * 8 + 2 * tig] = acc[mt][nt][0];
+                    rw[(mt * S::NTL + nt) * 64 + gid * 8 + 2 * tig + 1] = acc[mt][nt][1];
+                    acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+                }
+            __syncthreads();
+            for (int q = tid; q < S::L; q += S::THREADS) {
+                const int sidx = q / S::KL, t = q - sidx * S::KL;
+                const int o = ((sidx / 8) * S::NTL + t / 8) * 64 + (sidx % 8) * 8 + (t % 8);
+                double v = 0.0;
+#pragma unroll
+                for (int w = 0; w < S::WARPS; ++w) v += red[(size_t)w * S::MT * S::NTL * 64 + o];
+                a.ypart[sg * S::L + q] = v;
+            }
+        }
+        __syncthreads();  // row buffer, staged rows and the reduction buffer are free for the next chunk
+        HQ_FPHASE(7);
+        cc = nx;
+        cur = nxt;
+        buf ^= 1;
+    }
+    cpa_wait<0>();
+}
+
 // ---------------------------------------------------------------- fix-up --
 template <int L, int KN>
 struct LF_ {
@@ -554,6 +843,24 @@ void launch_long_t(const LongArgs& a, int fix_grid, cudaStream_t s) {
                                                                   S::smem));
         per_sm = std::max(per_sm, 1);
     }
+    if constexpr (K2 == 0) {
+        if (a.ustart) {  // fiber units
+            using FS = FS_<K0, K1>;
+            static int fib_per_sm = 0;
+            if (!fib_per_sm) {
+                set_smem_attr((const void*)k_fibseg<K0, K1>, FS::smem);
+                HQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fib_per_sm, k_fibseg<K0, K1>, S::THREADS, FS::smem));
+                if (const char* e = std::getenv("HQ_FIB_CTAS")) fib_per_sm = std::min(fib_per_sm, std::atoi(e));
+                fib_per_sm = std::max(fib_per_sm, 1);
+            }
+            const int g = (int)std::min<uint64_t>(a.nseg, (uint64_t)num_sms() * fib_per_sm);
+            k_fibseg<K0, K1><<<g, S::THREADS, FS::smem, s>>>(a);
+            HQ_CHECK_LAUNCH();
+            k_longfix_mma<S::L, KN><<<fix_grid, F::THREADS, F::smem, s>>>(a);
+            HQ_CHECK_LAUNCH();
+            return;
+        }
+    }
     const int seg_grid = (int)std::min<uint64_t>(a.nseg, (uint64_t)num_sms() * per_sm);
     if (sync_var)
         k_longseg_sync<K0, K1, K2><<<seg_grid, S::THREADS, sync_smem, s>>>(a);
@@ -565,6 +872,21 @@ void launch_long_t(const LongArgs& a, int fix_grid, cudaStream_t s) {
 }
 
 }  // namespace
+
+#ifdef HQ_PHASE_TIMING
+void debug_fib_phase_cycles(unsigned long long* out, int reset) {
+    HQ_CUDA(cudaDeviceSynchronize());
+    HQ_CUDA(cudaMemcpyFromSymbol(out, hq_fib_phase_cycles, sizeof(unsigned long long) * 16));
+    if (reset) {
+        unsigned long long z[16] = {0};
+        HQ_CUDA(cudaMemcpyToSymbol(hq_fib_phase_cycles, z, sizeof(z)));
+    }
+}
+#else
+void debug_fib_phase_cycles(unsigned long long* out, int) {
+    for (int i = 0; i < 16; ++i) out[i] = 0;
+}
+#endif
 
 bool long_fast_supported(const ModeShape& sh) {
     if (sh.order == 3) {

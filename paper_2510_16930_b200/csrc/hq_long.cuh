@@ -32,9 +32,16 @@ struct LongArgs {
     const DevStatus* st;
     int run_if;
     int l1_0, l1_1, l1_2;            // L1-allocating gathers for hot (skewed) factors (ModeLayout::hot)
+    // fiber units (order 3, FiberLayout): when ustart is set the segment kernel is k_fibseg -- rowptr, i0 and the
+    // segment plan describe the unit stream, val / i1 stay the mode's nonzero streams, u1 the last factor
+    const int64_t* ustart = nullptr; // units: first nonzero
+    const uint8_t* ulen = nullptr;   // units: nonzeros (<= kFiberCap)
+    const int64_t* rowptr_nz = nullptr;  // the mode's nonzero rowptr (rowptr is the unit rowptr)
+    const int64_t* seg_cost = nullptr;  // nseg + 1 prefix costs: CTAs take segment ranges of equal cost
 };
 
 bool long_fast_supported(const ModeShape& sh);
+void debug_fib_phase_cycles(unsigned long long* out, int reset);  // zeros unless built with -DHQ_PHASE_TIMING
 // segment kernel grid: min(segments, SMs x resident CTAs); fix-up grid given
 void launch_long_fast(const LongArgs& a, const ModeShape& sh, int fix_grid, cudaStream_t s);
 

@@ -45,25 +45,27 @@ ModeShape make_mode_shape(int order, const int* ranks, int n) {
 // ------------------------------------------------------------------ plan --
 namespace {
 
-__global__ void k_long_flags(const int64_t* __restrict__ rowptr, uint64_t rows, uint32_t* __restrict__ flag,
-                             uint32_t* __restrict__ nseg, int64_t hot_len, unsigned long long* __restrict__ hot_nnz) {
+__global__ void k_long_flags(const int64_t* __restrict__ rowptr, uint64_t rows, int64_t short_max,
+                             uint32_t* __restrict__ flag, uint32_t* __restrict__ nseg, int64_t hot_len,
+                             unsigned long long* __restrict__ hot_nnz) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < rows; i += (uint64_t)gridDim.x * blockDim.x) {
         int64_t len = rowptr[i + 1] - rowptr[i];
-        bool lng = len > kShortMax;
+        bool lng = len > short_max;
         flag[i] = lng;
         nseg[i] = lng ? (uint32_t)((len + kSegLen - 1) / kSegLen) : 0u;
         if (len > hot_len) atomicAdd(hot_nnz, (unsigned long long)len);  // integer: order-independent
     }
 }
 
-__global__ void k_tile_max(const int64_t* __restrict__ rowptr, uint64_t rows, unsigned long long* __restrict__ out) {
+__global__ void k_tile_max(const int64_t* __restrict__ rowptr, uint64_t rows, int64_t short_max,
+                           unsigned long long* __restrict__ out) {
     const uint64_t nt = (rows + 31) / 32;
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nt; t += (uint64_t)gridDim.x * blockDim.x) {
         unsigned long long s = 0;
         const uint64_t e = min(rows, t * 32 + 32);
         for (uint64_t i = t * 32; i < e; ++i) {
             const int64_t len = rowptr[i + 1] - rowptr[i];
-            if (len <= kShortMax) s += (unsigned long long)len;
+            if (len <= short_max) s += (unsigned long long)len;
         }
         atomicMax(out, s);
     }
@@ -200,6 +202,22 @@ __global__ void k_fib_row_counts(const uint32_t* __restrict__ ids, const int64_t
         nsegf[r] = (uint32_t)((c + kSegLen - 1) / kSegLen);
     }
 }
+// cost of a derived segment: its units (one DMMA column each) and its nonzeros (one unit-sum term each)
+__global__ void k_fib_seg_cost(const int64_t* __restrict__ rowptr_f, const uint32_t* __restrict__ ids,
+                               const int64_t* __restrict__ seg_begin, const uint32_t* __restrict__ seg_row, uint64_t nseg,
+                               const int64_t* __restrict__ ustart, const uint8_t* __restrict__ ulen,
+                               int64_t* __restrict__ cost) {
+    for (uint64_t sg = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; sg <= nseg; sg += (uint64_t)gridDim.x * blockDim.x) {
+        int64_t c = 0;
+        if (sg < nseg) {
+            const int64_t first = seg_begin[sg];
+            const int64_t last = min(first + (int64_t)kSegLen, rowptr_f[ids[seg_row[sg]] + 1]) - 1;
+            const int64_t nz = ustart[last] + ulen[last] - ustart[first];
+            c = 4 * (last - first + 1) + 2 * nz;
+        }
+        cost[sg] = c;
+    }
+}
 __global__ void k_u32_to_i64(const uint32_t* __restrict__ a, uint64_t n, int64_t* __restrict__ b) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
         b[i] = (int64_t)a[i];
@@ -298,13 +316,26 @@ void plan_fibers(ModeLayout& L, cudaStream_t s) {
     k_long_segments<<<grid_for(nlong), 256, 0, s>>>(F.rowptr.get(), L.long_row_ids.get(), F.long_seg_ptr.get(), nlong,
                                                    F.seg_begin.get(), F.seg_row.get());
     HQ_CHECK_LAUNCH();
-    HQ_CUDA(cudaStreamSynchronize(s));
+    {
+        DBuf<int64_t> cost;
+        cost.alloc(F.long_segments + 1);
+        F.seg_cost.alloc(F.long_segments + 1);
+        k_fib_seg_cost<<<grid_for(F.long_segments + 1), 256, 0, s>>>(F.rowptr.get(), L.long_row_ids.get(),
+                                                                    F.seg_begin.get(), F.seg_row.get(), F.long_segments,
+                                                                    F.start.get(), F.len.get(), cost.get());
+        HQ_CHECK_LAUNCH();
+        exclusive_scan(cost.get(), F.seg_cost.get(), F.long_segments + 1, s);
+        HQ_CUDA(cudaStreamSynchronize(s));
+    }
     F.on = true;
 }
 
 }  // namespace
 
-void plan_mode(ModeLayout& L, uint64_t nnz, int order, cudaStream_t s) {
+namespace {
+
+// long rows (more than short_max nonzeros), their segments, the hot flag and the largest short-row tile
+void plan_long_rows(ModeLayout& L, uint64_t nnz, int64_t short_max, cudaStream_t s) {
     const uint64_t rows = L.rows;
     DBuf<uint32_t> flag, nseg, pos, segpos;
     DBuf<unsigned long long> hot;
@@ -315,12 +346,14 @@ void plan_mode(ModeLayout& L, uint64_t nnz, int order, cudaStream_t s) {
     hot.alloc(1);
     HQ_CUDA(cudaMemsetAsync(hot.get(), 0, sizeof(unsigned long long), s));
     const int64_t hot_len = std::max<int64_t>(64, (int64_t)(32 * (nnz / std::max<uint64_t>(rows, 1))));
-    k_long_flags<<<grid_for(rows), 256, 0, s>>>(L.rowptr.get(), rows, flag.get(), nseg.get(), hot_len, hot.get());
+    L.short_max = short_max;
+    k_long_flags<<<grid_for(rows), 256, 0, s>>>(L.rowptr.get(), rows, L.short_max, flag.get(), nseg.get(), hot_len,
+                                               hot.get());
     HQ_CHECK_LAUNCH();
     DBuf<unsigned long long> tmax;
     tmax.alloc(1);
     HQ_CUDA(cudaMemsetAsync(tmax.get(), 0, sizeof(unsigned long long), s));
-    k_tile_max<<<grid_for((rows + 31) / 32), 256, 0, s>>>(L.rowptr.get(), rows, tmax.get());
+    k_tile_max<<<grid_for((rows + 31) / 32), 256, 0, s>>>(L.rowptr.get(), rows, L.short_max, tmax.get());
     HQ_CHECK_LAUNCH();
     unsigned long long hot_nnz = 0, tile_max = 0;
     HQ_CUDA(cudaMemcpyAsync(&hot_nnz, hot.get(), sizeof(hot_nnz), cudaMemcpyDeviceToHost, s));
@@ -337,6 +370,10 @@ void plan_mode(ModeLayout& L, uint64_t nnz, int order, cudaStream_t s) {
     L.max_tile32 = tile_max;
     L.long_rows = (uint64_t)lp + lf;
     L.long_segments = (uint64_t)sp + sn;
+    L.long_row_ids.release();
+    L.long_seg_ptr.release();
+    L.seg_begin.release();
+    L.seg_row.release();
     if (L.long_rows) {
         L.long_row_ids.alloc(L.long_rows);
         L.long_seg_ptr.alloc(L.long_rows + 1);
@@ -352,8 +389,24 @@ void plan_mode(ModeLayout& L, uint64_t nnz, int order, cudaStream_t s) {
         HQ_CHECK_LAUNCH();
         HQ_CUDA(cudaStreamSynchronize(s));
     }
+}
+
+}  // namespace
+
+void plan_mode(ModeLayout& L, uint64_t nnz, int order, cudaStream_t s) {
+    plan_long_rows(L, nnz, kShortMax, s);
     L.fib = FiberLayout{};
-    if (order == 3) plan_fibers(L, s);
+    if (order != 3 || fibers_mode() == 0) return;
+    if (L.hot) {
+        // a skewed mode: its long rows run through the fiber units where those shrink the stream, and the fiber
+        // kernel outruns the tile kernel (tiles of very unequal rows) from ~50 nonzeros per row on -- plan
+        // with the lower threshold, and go back to the plain plan when the units do not pay
+        plan_long_rows(L, nnz, kSkewedShortMax, s);
+        plan_fibers(L, s);
+        if (!L.fib.on) plan_long_rows(L, nnz, kShortMax, s);
+    } else {
+        plan_fibers(L, s);
+    }
 }
 
 // ------------------------------------------------------- generic kernels --
@@ -383,6 +436,7 @@ struct PassArgs {
     const uint32_t* seg_row;
     uint64_t nlong;
     uint64_t nseg;
+    int64_t short_max;
 };
 
 constexpr int kGenericThreads = 256;
@@ -447,7 +501,7 @@ __global__ void __launch_bounds__(kGenericThreads) k_pass_tiles_generic(PassArgs
             uint64_t i = r0 + lr;
             int64_t s = a.rowptr[i], e = a.rowptr[i + 1];
             double acc = 0.0;
-            if (e - s <= kShortMax) {
+            if (e - s <= a.short_max) {
                 int kidx[kMaxOrder - 1];
                 col_digits(a.sh, col, kidx);
                 for (int64_t p = s; p < e; ++p) acc += kron_entry(a, p, kidx);
@@ -458,7 +512,7 @@ __global__ void __launch_bounds__(kGenericThreads) k_pass_tiles_generic(PassArgs
         for (int q = threadIdx.x; q < nr * Kn; q += blockDim.x) {
             int lr = q / Kn, r = q - lr * Kn;
             uint64_t i = r0 + lr;
-            bool lng = (a.rowptr[i + 1] - a.rowptr[i]) > kShortMax;
+            bool lng = (a.rowptr[i + 1] - a.rowptr[i]) > a.short_max;
             double v = 0.0;
             if (!lng) {
                 if (a.kind == kTTMcTC) {
@@ -722,6 +776,7 @@ void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const Fac
     a.seg_row = L.seg_row.get();
     a.nlong = L.long_rows;
     a.nseg = L.long_segments;
+    a.short_max = L.short_max;
 
     a.R = generic_rows_per_tile(sh);
     a.ntiles = (int64_t)ceil_div(a.rows, a.R);
@@ -754,6 +809,7 @@ void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const Fac
         fa.run_if = run_if;
         fa.l1_a = T.modes[L.others[0]].hot;
         fa.l1_b = T.modes[L.others[1]].hot;
+        fa.short_max = (int)L.short_max;
         launch_fast(fa, sh, tile_grid(sh), s);
     } else {
         size_t smem = sizeof(double) * ((size_t)a.R * sh.L + (size_t)a.R * sh.kn);
@@ -793,7 +849,24 @@ void launch_pass(const DeviceTensor& T, int mode, const ModeShape& sh, const Fac
         la.slot0 = short_slots(L, sh);
         la.st = st;
         la.run_if = run_if;
-        if (use_fibers(L, sh)) {
+        static const bool fused = [] {
+            const char* e = std::getenv("HQ_FIB_FUSED");
+            return !(e && e[0] == '0');
+        }();
+        if (use_fibers(L, sh) && fused) {
+            // fiber units, fused: the segment kernel forms each unit's sum over the last other mode in
+            // shared memory and takes its Kronecker product with the unit's first-other-mode row (k_fibseg)
+            la.rowptr_nz = a.rowptr;
+            la.rowptr = L.fib.rowptr.get();
+            la.i0 = L.fib.outer.get();
+            la.ustart = L.fib.start.get();
+            la.ulen = L.fib.len.get();
+            la.seg_cost = L.fib.seg_cost.get();
+            la.long_segptr = L.fib.long_seg_ptr.get();
+            la.seg_begin = L.fib.seg_begin.get();
+            la.seg_row = L.fib.seg_row.get();
+            la.nseg = L.fib.long_segments;
+        } else if (use_fibers(L, sh)) {
             // fiber units: T = the unit sums over the last other mode, then the long-row kernels run on the
             // derived stream (value 1, indices (first other index, unit id)) with T as the last factor table
             double* Tu = out.ypart + (size_t)L.long_segments * sh.L;

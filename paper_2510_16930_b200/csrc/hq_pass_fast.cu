@@ -276,12 +276,12 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
             int len = 0;
             if (tid < nr) {
                 const int64_t l = st_hi - st_lo;
-                len = (l > kShortMax) ? -1 : (int)l;
+                len = (l > a.short_max) ? -1 : (int)l;
             }
             m_len(mb)[tid] = len;
             m_start(mb)[tid] = st_lo;
         }
-        const int any_long = __syncthreads_or(tid < C::R && tid < nr && st_hi - st_lo > kShortMax);
+        const int any_long = __syncthreads_or(tid < C::R && tid < nr && st_hi - st_lo > a.short_max);
         if (tid < C::R) {
             const int* ln = m_len(mb);
             const int me = max(ln[tid], 0);
@@ -714,10 +714,10 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
         const int nr = (int)min((uint64_t)C::R, rend - r0);
         // ---- meta
         // row lengths (-1: long row), exclusive offsets, and ranks by (length desc, row asc): warp 0, one lane
-        // per row, with a shuffle scan and a 9-bit ballot radix rank (lengths <= kShortMax = 256)
+        // per row, with a shuffle scan and a 9-bit ballot radix rank (lengths <= short_max <= kShortMax = 256)
         static_assert(C::R == 32 && kShortMax < 512, "one lane per tile row, 9-bit lengths");
         if (warp == 0) {
-            const int ln = (lane < nr) ? ((nhi - nlo > kShortMax) ? -1 : (int)(nhi - nlo)) : 0;
+            const int ln = (lane < nr) ? ((nhi - nlo > a.short_max) ? -1 : (int)(nhi - nlo)) : 0;
             m_len[lane] = ln;
             m_start[lane] = nlo;
             const int me = max(ln, 0);

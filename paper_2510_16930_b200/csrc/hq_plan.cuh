@@ -16,6 +16,9 @@ namespace hq {
 #endif
 constexpr int64_t kShortMax = HQ_SHORT_MAX;
 constexpr int64_t kSegLen = 4096;
+// long-row threshold of a skewed order-3 mode whose long rows run through the fiber units (hq_pass.cu
+// plan_mode; measured on config 3: 256 -> 7.8, 128 -> 7.3, 64 -> 7.2, 48 -> 7.1, 32 -> 7.2, 16 -> 7.8 ms / sweep)
+constexpr int64_t kSkewedShortMax = 64;
 
 void plan_mode(ModeLayout& L, uint64_t nnz, int order, cudaStream_t s);
 

@@ -37,6 +37,7 @@
 #include "hq_comm.cuh"
 #include "hq_dense.cuh"
 #include "hq_fast.cuh"
+#include "hq_long.cuh"
 #include "hq_tns.cuh"
 #include "hq_hooi.cuh"
 
@@ -1002,7 +1003,8 @@ int hq_tensor_mode_plan(const hq_tensor* t, int mode, uint64_t* rows, uint64_t* 
     });
 }
 
-int hq_tensor_fiber_plan(const hq_tensor* t, int mode, uint64_t* units, uint64_t* long_nnz, uint64_t* segments) {
+int hq_tensor_fiber_plan(const hq_tensor* t, int mode, uint64_t* units, uint64_t* long_nnz, uint64_t* segments,
+                         uint64_t* short_max) {
     return guard([&] {
         if (mode < 0 || mode >= t->t.order)
             fail(HQ_ERR_RANGE, "mode " + std::to_string(mode) + " out of range for order " + std::to_string(t->t.order));
@@ -1010,6 +1012,7 @@ int hq_tensor_fiber_plan(const hq_tensor* t, int mode, uint64_t* units, uint64_t
         if (units) *units = F.on ? F.units : 0;
         if (long_nnz) *long_nnz = F.on ? F.long_nnz : 0;
         if (segments) *segments = F.on ? F.long_segments : 0;
+        if (short_max) *short_max = (uint64_t)t->t.modes[mode].short_max;
     });
 }
 
@@ -1420,6 +1423,10 @@ int hq_solver_create(const hq_tensor* t, const hq_config* cfg, const double* con
 // with -DHQ_PHASE_TIMING); not part of the public header
 int hq_debug_phase_cycles(unsigned long long* out16, int reset) {
     return guard([&] { debug_phase_cycles(out16, reset); });
+}
+
+int hq_debug_fib_phase_cycles(unsigned long long* out16, int reset) {
+    return guard([&] { debug_fib_phase_cycles(out16, reset); });
 }
 
 int hq_nccl_unique_id(uint8_t* id_out) {

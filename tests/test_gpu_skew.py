@@ -112,11 +112,13 @@ def test_fiber_units_cover_the_long_rows():
     for m in range(3):
         p, f = x.mode_plan(m), x.fiber_plan(m)
         cnt = np.bincount(c[:, m], minlength=DIMS[m])
-        long_nnz = int(cnt[cnt > 256].sum())
-        assert f["long_nnz"] == long_nnz and p["long_rows"] == int((cnt > 256).sum())
+        sm = f["short_max"]
+        assert sm == (64 if p["hot"] else 256) and off.fiber_plan(m)["short_max"] == 256
+        long_nnz = int(cnt[cnt > sm].sum())
+        assert f["long_nnz"] == long_nnz and p["long_rows"] == int((cnt > sm).sum())
         # units = sum over fibers (row, first other index) of the long rows of ceil(len / 16)
         o = [v for v in range(3) if v != m][0]
-        sel = cnt[c[:, m]] > 256
+        sel = cnt[c[:, m]] > sm
         key = c[sel, m].astype(np.int64) * DIMS[o] + c[sel, o]
         _, lens = np.unique(key, return_counts=True)
         lo = int(np.ceil(lens / 16).sum())

@@ -971,6 +971,9 @@ void launch_fast3(const FastArgs& a, int grid, cudaStream_t s) {
         if (!attr3) {
             HQ_CUDA(cudaFuncSetAttribute(k_pass_np3<KA, KB, KN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)CN::smem));
+            int per_sm = 0;  // the grid (fast_grid) and the tile ranges assume HQ_NP_MINB resident CTAs per SM
+            HQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pass_np3<KA, KB, KN>, 128, CN::smem));
+            if (per_sm < HQ_NP_MINB) fail(HQ_ERR_INTERNAL, "k_pass_np3: fewer resident CTAs per SM than planned");
             attr3 = true;
         }
         k_pass_np3<KA, KB, KN><<<grid, 128, CN::smem, s>>>(a);

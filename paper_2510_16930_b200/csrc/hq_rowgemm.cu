@@ -54,6 +54,11 @@ __device__ __forceinline__ double rg_b(double reg, const double* T, int ks, int 
     return (k < K && n < K) ? (T ? __ldg(T + k * K + n) : (k == n ? 1.0 : 0.0)) : 0.0;
 }
 
+// Every transform of a mode update (R1^-1, R2^-1, R3^-1, their products, the identity) is upper triangular, so
+// T[k][n] = 0 for k > n: the 8-column tile nt of X = A T needs only the k-steps with 4 ks <= 8 nt + 7.  The
+// skipped products are exact zeros, so the result has the same bits.
+__device__ __forceinline__ constexpr int rg_ksteps(int KS, int nt) { return KS < 2 * (nt + 1) ? KS : 2 * (nt + 1); }
+
 // second stage of a two-stage product, in place on the warp's 8-row X tile: X <- fl(X T2).  The first stage's
 // rounded X is exactly what a materialised pass would have written and re-read (CholeskyQR's Q1 / Q2).
 template <int K, int KS, int NT, int LD>
@@ -68,7 +73,7 @@ __device__ __forceinline__ void rg_stage2(double* sx, const double (&tf2)[KS][NT
     for (int nt = 0; nt < NT; ++nt) {
         double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
+        for (int ks = 0; ks < rg_ksteps(KS, nt); ++ks) {
             const int k = 4 * ks + tig, n = 8 * nt + gid;
             const double b = kRegs ? tf2[ks][nt] : ((k < K && n < K) ? __ldg(T2 + k * K + n) : 0.0);
             dmma884(c0, c1, a[ks], b);
@@ -180,7 +185,8 @@ __global__ void __launch_bounds__(kRgWarps * 32) k_rowgemm(RowGemm g) {
         for (int nt = 0; nt < C::NT; ++nt) {
             double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-            for (int ks = 0; ks < C::KS; ++ks) dmma884(c0, c1, a[ks], rg_b<K>(tf[ks][nt], T, ks, nt, gid, tig));
+            for (int ks = 0; ks < rg_ksteps(C::KS, nt); ++ks)
+                dmma884(c0, c1, a[ks], rg_b<K>(tf[ks][nt], T, ks, nt, gid, tig));
             const int col = 8 * nt + 2 * tig;
             sx[gid * C::LD + col] = c0;
             sx[gid * C::LD + col + 1] = c1;
@@ -430,7 +436,8 @@ __global__ void __launch_bounds__((RT<K>::CW + 1) * 32, 1) k_rowgemm_tma(RowGemm
         for (int nt = 0; nt < C::NT; ++nt) {
             double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-            for (int ks = 0; ks < C::KS; ++ks) dmma884(c0, c1, a[ks], rg_b<K>(tf[ks][nt], T, ks, nt, gid, tig));
+            for (int ks = 0; ks < rg_ksteps(C::KS, nt); ++ks)
+                dmma884(c0, c1, a[ks], rg_b<K>(tf[ks][nt], T, ks, nt, gid, tig));
             const int col = 8 * nt + 2 * tig;
             sx[gid * C::LD + col] = c0;
             sx[gid * C::LD + col + 1] = c1;

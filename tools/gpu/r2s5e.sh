@@ -1,0 +1,6 @@
+export PYTHONUNBUFFERED=1
+for v in default gu4 gu8 gu4pf; do
+  if [ $v = default ]; then unset HQ_LIB; else export HQ_LIB=tmp_variants/$v/libhoqri_b200.so; fi
+  timeout 600 python tools/pass_time.py 2 2>&1 | grep -v Warn | tail -1
+done
+HQ_LIB=tmp_variants/phase/libhoqri_b200.so timeout 600 python tools/phase_timing.py 2 2>&1 | grep -v Warn

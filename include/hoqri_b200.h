@@ -53,6 +53,10 @@ typedef enum hq_status {
 const char* hq_last_error(void);
 int64_t hq_last_error_payload(void);
 const char* hq_version(void);
+/* Device buffers freed by tensors / solvers are kept on the engine's free lists for the next solve (no driver
+   allocation in steady state; HQ_POOL_RELEASE_GB caps them).  This returns them to the driver; *freed_bytes (may be
+   NULL) receives the amount.  Engine-only (the reference is a CPU library and has no counterpart). */
+int hq_release_cached_memory(uint64_t* freed_bytes);
 
 /* ---------------------------------------------------------------- tensor --
  * Device-resident mirror of tucker::SparseTensor.  Creation validates the

@@ -111,7 +111,7 @@ class HqTrace(C.Structure):
 
 
 EXPORTED_SYMBOLS = [
-    "hq_last_error", "hq_last_error_payload", "hq_version",
+    "hq_last_error", "hq_last_error_payload", "hq_version", "hq_release_cached_memory",
     "hq_tensor_create", "hq_tensor_create_dev", "hq_tensor_destroy", "hq_tensor_info", "hq_tensor_mode_plan",
     "hq_tensor_fiber_plan", "hq_tensor_export",
     "hq_tensor_buckets", "hq_tensor_norm_sq",
@@ -372,6 +372,15 @@ class SparseTensor:
         ent = np.empty(max(1, self._nnz), np.uint64)
         _check(load_library().hq_tensor_buckets(self._h, mode, off, ent.ctypes.data))
         return off, ent[: self._nnz]
+
+
+def release_cached_memory() -> int:
+    """Returns the device buffers the engine keeps for its next solve to the driver; the bytes freed
+    (hq_release_cached_memory)."""
+    L = load_library()
+    freed = C.c_uint64(0)
+    _check(L.hq_release_cached_memory(C.byref(freed)))
+    return int(freed.value)
 
 
 def norm_sq(x):

@@ -4,7 +4,12 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
+#include <iterator>
+#include <map>
+#include <mutex>
 
 #include <cstdint>
 #include <stdexcept>
@@ -37,28 +42,71 @@ struct Error : std::runtime_error {
 #define HQ_CHECK_LAUNCH() HQ_CUDA(cudaGetLastError())
 
 // ---------------------------------------------------------------- memory --
-// RAII device buffer (stream-ordered allocation).
-// Device buffers come from the device's stream-ordered memory pool with a
-// high release threshold: a solve's buffers freed by one solver are re-used
-// by the next without unmapping / remapping (cudaMalloc / cudaFree cost
-// milliseconds per large buffer in an end-to-end solve).
-inline void device_pool_init() {
-    static int once = [] {
+// Device buffers come from a size-keyed cache of cudaMalloc blocks (a caching allocator, like the host
+// frameworks'): a freed block goes onto a free list and the next request of (nearly) the same size takes it, so
+// a solve that follows another of the same shape makes no driver allocation at all.  The CUDA stream-ordered
+// pool this replaced re-used blocks only most of the time: about one config-2 solve in three paid a fresh
+// 40-160 MB mapping (1-450 ms inside cudaMallocAsync, measured with HQ_ALLOC_TIMING on this pool's boxes),
+// which was the whole of the end-to-end variance.  HQ_POOL_RELEASE_GB caps the bytes kept on the free lists;
+// hq_release_cached_memory() returns them to the driver; an out-of-memory cudaMalloc frees them and retries.
+struct DeviceCache {
+    std::mutex mu;
+    std::multimap<size_t, void*> blocks[16];  // per device: free blocks by size
+    size_t cached = 0;
+    size_t cap = ~size_t(0);
+    DeviceCache() {
+        if (const char* e = std::getenv("HQ_POOL_RELEASE_GB")) cap = (size_t)std::strtoull(e, nullptr, 10) << 30;
+    }
+    static size_t round_up(size_t bytes) { return (bytes + 511) & ~size_t(511); }
+    static int device() {
         int dev = 0;
         cudaGetDevice(&dev);
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            // freed blocks stay mapped in the pool (like a caching allocator): re-mapping
-            // tens of GB between solves costs 100+ ms.  HQ_POOL_RELEASE_GB caps what is kept.
-            uint64_t thr = ~0ull;
-            if (const char* e = std::getenv("HQ_POOL_RELEASE_GB")) thr = std::strtoull(e, nullptr, 10) << 30;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        return dev & 15;
+    }
+    // a free block of at least `bytes` and at most 1/8 more (so odd-sized leftovers do not pin large blocks)
+    void* take(size_t bytes, size_t* got) {
+        std::lock_guard<std::mutex> g(mu);
+        auto& m = blocks[device()];
+        auto it = m.lower_bound(bytes);
+        if (it == m.end() || it->first > bytes + bytes / 8) return nullptr;
+        void* p = it->second;
+        *got = it->first;
+        cached -= it->first;
+        m.erase(it);
+        return p;
+    }
+    void put(void* p, size_t bytes) {
+        std::lock_guard<std::mutex> g(mu);
+        auto& m = blocks[device()];
+        m.emplace(bytes, p);
+        cached += bytes;
+        while (cached > cap && !m.empty()) {  // over the cap: the largest blocks go back to the driver
+            auto it = std::prev(m.end());
+            cudaFree(it->second);
+            cached -= it->first;
+            m.erase(it);
         }
-        return 0;
-    }();
-    (void)once;
+    }
+    size_t release_all() {
+        std::lock_guard<std::mutex> g(mu);
+        size_t freed = 0;
+        for (auto& m : blocks) {
+            for (auto& kv : m) {
+                cudaFree(kv.second);
+                freed += kv.first;
+            }
+            m.clear();
+        }
+        cached = 0;
+        return freed;
+    }
+};
+inline DeviceCache& device_cache() {
+    static DeviceCache* c = new DeviceCache();  // never destroyed: the CUDA context may be gone at exit
+    return *c;
 }
 
+// RAII device buffer.
 template <class T>
 struct DBuf {
     T* p = nullptr;
@@ -66,12 +114,17 @@ struct DBuf {
     // a rank's slice [off, off + n) of a conceptually longer array (sharded mode streams): get() returns the
     // base the kernels index with global positions, p - off; only the slice is allocated
     size_t off = 0;
+    size_t cap = 0;  // bytes of the underlying block
     DBuf() = default;
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
-    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), off(o.off) { o.p = nullptr; o.n = 0; o.off = 0; }
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), off(o.off), cap(o.cap) { o.p = nullptr; o.n = 0; o.off = 0; o.cap = 0; }
     DBuf& operator=(DBuf&& o) noexcept {
-        if (this != &o) { release(); p = o.p; n = o.n; off = o.off; o.p = nullptr; o.n = 0; o.off = 0; }
+        if (this != &o) {
+            release();
+            p = o.p; n = o.n; off = o.off; cap = o.cap;
+            o.p = nullptr; o.n = 0; o.off = 0; o.cap = 0;
+        }
         return *this;
     }
     ~DBuf() { release(); }
@@ -80,20 +133,39 @@ struct DBuf {
         off = 0;
         n = count;
         if (count) {
-            device_pool_init();
-            HQ_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, 0));
-            HQ_CUDA(cudaStreamSynchronize(0));  // usable from every stream
+            const size_t want = DeviceCache::round_up(sizeof(T) * count);
+            DeviceCache& c = device_cache();
+            void* q = c.take(want, &cap);
+            if (!q) {
+#ifdef HQ_ALLOC_TIMING
+                const auto t0 = std::chrono::steady_clock::now();
+#endif
+                cudaError_t e = cudaMalloc(&q, want);
+                if (e == cudaErrorMemoryAllocation) {  // give the cached blocks back and try once more
+                    cudaGetLastError();
+                    cudaDeviceSynchronize();
+                    c.release_all();
+                    e = cudaMalloc(&q, want);
+                }
+                HQ_CUDA(e);
+                cap = want;
+#ifdef HQ_ALLOC_TIMING
+                std::fprintf(stderr, "[alloc] %zu bytes from the driver: %.2f ms\n", want,
+                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+#endif
+            }
+            p = static_cast<T*>(q);
         }
     }
     void release() {
         if (p) {
-            cudaDeviceSynchronize();  // like cudaFree: no pending work may still use it
-            cudaFreeAsync(p, 0);
-            cudaStreamSynchronize(0);
+            cudaDeviceSynchronize();  // like cudaFree: no pending work may still use the block
+            device_cache().put(p, cap);
         }
         p = nullptr;
         n = 0;
         off = 0;
+        cap = 0;
     }
     T* get() const { return p ? p - off : nullptr; }
     size_t bytes() const { return sizeof(T) * n; }

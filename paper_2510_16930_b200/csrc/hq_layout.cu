@@ -340,6 +340,7 @@ void build_tensor(DeviceTensor& T, int order, const uint64_t* dims, uint64_t nnz
         p1.alloc(nnz);
         k_iota<<<grid_for(nnz), 256, 0, s>>>(p0.get(), nnz);
         HQ_CHECK_LAUNCH();
+        clk.mark("sort buffers");
         for (int w = 0; w < ks.nwords; ++w) {
             int wbits = (w < ks.nwords - 1) ? 64 : total_bits - 64 * (ks.nwords - 1);
             if (wbits <= 0) continue;
@@ -352,6 +353,7 @@ void build_tensor(DeviceTensor& T, int order, const uint64_t* dims, uint64_t nnz
             std::swap(p0, p1);
         }
         perm = std::move(p0);
+        clk.mark("radix sort");
         if (vals_ready) {  // the values have landed: their check, then the first bad entry (if any) is reported
             HQ_CUDA(cudaStreamWaitEvent(s, vals_ready, 0));
             k_validate<<<grid_for(nnz), 256, 0, s>>>(nullptr, vals_in, nnz, order, ddims.get(), bad.get());

@@ -1419,6 +1419,14 @@ int hq_solver_create(const hq_tensor* t, const hq_config* cfg, const double* con
     });
 }
 
+int hq_release_cached_memory(uint64_t* freed_bytes) {
+    return guard([&] {
+        HQ_CUDA(cudaDeviceSynchronize());
+        const size_t f = device_cache().release_all();
+        if (freed_bytes) *freed_bytes = (uint64_t)f;
+    });
+}
+
 // debug: per-phase cycle counters of the specialised pass (zeros unless built
 // with -DHQ_PHASE_TIMING); not part of the public header
 int hq_debug_phase_cycles(unsigned long long* out16, int reset) {

@@ -243,11 +243,13 @@ int hq_solver_sync(hq_solver* s);
 int hq_solver_launch_mode_pass(hq_solver* s, int mode);
 /* launches only the TTMcTC kernel for `mode` (A written to device scratch) */
 int hq_solver_launch_ttmctc(hq_solver* s, int mode);
-/* device status word after a sync (out: 6 slots): out[0] sweeps completed,
+/* device status word after a sync (out: 8 slots): out[0] sweeps completed,
  * out[1] mode updates that took the Householder fallback, out[2] abort code
- * (0 running, 1 degenerate, 2 stopped, 3 multi-GPU fallback), out[3]
+ * (0 running, 1 degenerate, 2 stopped, 3 multi-GPU fallback pending), out[3]
  * degenerate mode, out[4] mode updates that ran shifted CholeskyQR3, out[5]
- * multi-GPU rank-deficient updates kept on the shifted basis (no seeded fill) */
+ * multi-GPU updates finished by the host-driven Householder continuation,
+ * out[6] 1 when the multi-GPU apply stores U_new straight into the other
+ * ranks' replicas over peer memory (fused apply + all-gather), out[7] 0 */
 int hq_solver_status(hq_solver* s, int64_t* out);
 /* number of device kernels one sweep launches */
 int hq_solver_launches_per_sweep(const hq_solver* s, uint64_t* out);

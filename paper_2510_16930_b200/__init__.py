@@ -823,11 +823,12 @@ class Solver:
 
     def status(self):
         """Device status word: sweeps done, Householder fallbacks, abort code, degenerate mode, shifted
-        CholeskyQR3 updates, and (multi-GPU) updates finished by the host-driven Householder continuation."""
-        out = (C.c_int64 * 6)()
+        CholeskyQR3 updates, (multi-GPU) updates finished by the host-driven Householder continuation, and
+        whether the multi-GPU apply writes U_new into the other ranks' replicas over peer memory."""
+        out = (C.c_int64 * 8)()
         _check(load_library().hq_solver_status(self._h, out))
         return {"sweeps": out[0], "fallbacks": out[1], "abort": out[2], "degenerate_mode": out[3],
-                "shifted": out[4], "dist_householder": out[5]}
+                "shifted": out[4], "dist_householder": out[5], "peer_apply": out[6]}
 
     def launch_mode_pass(self, mode):
         """The fused sparse pass of a mode update (A, M, W, max|A|), on the solver's stream."""

@@ -240,6 +240,15 @@ void Comm::allgather_rows(double* buf, const uint64_t* bounds, size_t row_elems,
     HQ_NCCL(nccl().GroupEnd());
 }
 
+void Comm::barrier(cudaStream_t s) const {
+    if (world <= 1 || (!host && !comm)) return;
+    if (!bar.p) {
+        bar.alloc(1);
+        HQ_CUDA(cudaMemsetAsync(bar.get(), 0, sizeof(double), s));
+    }
+    allreduce_sum(bar.get(), 1, s);
+}
+
 void nccl_unique_id(uint8_t* out128) {
     ncclUniqueId id;
     HQ_NCCL(nccl().GetUniqueId(&id));

@@ -29,6 +29,10 @@ struct Comm {
     void allreduce_max(double* buf, size_t count, cudaStream_t s) const;
     // every rank's rows [bounds[r], bounds[r+1]) of a row-major buffer, broadcast from their owner
     void allgather_rows(double* buf, const uint64_t* bounds, size_t row_elems, cudaStream_t s) const;
+    // every rank's work enqueued on its stream before this point is complete before any rank's work after it
+    // starts (an 8-byte all-reduce): orders the peer-memory stores of the fused apply against their readers
+    void barrier(cudaStream_t s) const;
+    mutable DBuf<double> bar;  // the barrier's operand
 };
 
 void nccl_unique_id(uint8_t* out128);

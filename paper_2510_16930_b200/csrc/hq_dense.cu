@@ -665,8 +665,11 @@ void launch_apply(const double* A, uint64_t rows, int K, const double* rinv, dou
 
 void launch_apply_qr(const double* A, uint64_t rows, int K, const double* r1inv, const double* rinv, double* u_out,
                      const double* u_old, double* ppart, bool shifted_alt, const DevStatus* st, int run_if,
-                     cudaStream_t s) {
+                     cudaStream_t s, double* const* peer_out, int npeer) {
     RowGemm g{};
+    if (npeer > kMaxPeers) fail(HQ_ERR_CAPACITY, "more peer replicas than the apply kernel takes");
+    for (int r = 0; r < npeer; ++r) g.peer_out[r] = peer_out[r];
+    g.npeer = npeer;
     g.A = A;
     g.rows = rows;
     g.T = r1inv;

@@ -27,6 +27,7 @@ int dense_slots();
 // X = A T (T null: identity); out <- X (optional); part[cta] = X^T Y with
 // Y = other (optional) or X; maxpart[cta] = max|A| (optional).  hq_rowgemm.cu
 bool rowgemm_supported(int K);
+constexpr int kMaxPeers = 15;  // other ranks of one node
 struct RowGemm {
     const double* A;       // rows x K
     uint64_t rows;
@@ -39,6 +40,11 @@ struct RowGemm {
     double* maxpart;       // [CTA] max|A| (optional)
     const DevStatus* st;
     int run_if;
+    // multi-GPU: the same rows of X also stored straight into the other ranks' replicas of the factor (peer
+    // memory mapped through CUDA IPC: NVLink / NVSwitch stores) -- the apply and the all-gather of U_new in one
+    // kernel, the transfer overlapping the row products chunk by chunk.  Pointers are to the same row as `out`.
+    double* peer_out[kMaxPeers];
+    int npeer;
 };
 void launch_rowgemm(int K, const RowGemm& g, cudaStream_t s);
 void launch_rowgemm(int K, const double* A, uint64_t rows, const double* T, double* out, const double* other,
@@ -84,7 +90,8 @@ void launch_apply(const double* A, uint64_t rows, int K, const double* rinv, dou
 // instead (u_out holds Q2 from gram3, rinv holds R3^-1 from chol3)
 void launch_apply_qr(const double* A, uint64_t rows, int K, const double* r1inv, const double* rinv, double* u_out,
                      const double* u_old, double* ppart, bool shifted_alt, const DevStatus* st, int run_if,
-                     cudaStream_t s);
+                     cudaStream_t s,
+                     double* const* peer_out = nullptr, int npeer = 0);
 // drift = max(2K - 2 ||P||_*, 0) (manifold.cpp:55-60) from P partials; when
 // `objective` non-null also f = ||G||^2 and fit = dns - f for the sweep;
 // `end_of_sweep` advances the sweep counter and applies the stop rule.

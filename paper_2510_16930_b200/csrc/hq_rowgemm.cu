@@ -111,6 +111,8 @@ __global__ void __launch_bounds__(kRgWarps * 32) k_rowgemm(RowGemm g) {
     rg_select(g, A, T, T2);
     const uint64_t rows = g.rows;
     double* out = g.out;
+    const int npeer = out ? g.npeer : 0;
+    const RowGemm& gp = g;
     const double* __restrict__ other = g.other;
     double* __restrict__ part = g.part;
     double* __restrict__ maxpart = g.maxpart;
@@ -200,7 +202,9 @@ __global__ void __launch_bounds__(kRgWarps * 32) k_rowgemm(RowGemm g) {
                 const uint64_t e = g * 8 * K + q;
                 if (q < 8 * K && e < rows * K) {
                     const int r = q / K, cc = q - r * K;
-                    out[e] = sx[r * C::LD + cc];
+                    const double v = sx[r * C::LD + cc];
+                    out[e] = v;
+                    for (int pr = 0; pr < npeer; ++pr) gp.peer_out[pr][e] = v;
                 }
             }
         }
@@ -343,6 +347,8 @@ __global__ void __launch_bounds__((RT<K>::CW + 1) * 32, 1) k_rowgemm_tma(RowGemm
     rg_select(g, A, T, T2);
     const uint64_t rows = g.rows;
     double* out = g.out;
+    const int npeer = out ? g.npeer : 0;
+    const RowGemm& gp = g;
     const double* __restrict__ other = g.other;
     double* __restrict__ part = g.part;
     double* __restrict__ maxpart = g.maxpart;
@@ -448,9 +454,12 @@ __global__ void __launch_bounds__((RT<K>::CW + 1) * 32, 1) k_rowgemm_tma(RowGemm
         if (out) {
             const int lim = max(0, min(8, nr - gr0)) * K;
             double* og = out + (r0 + gr0) * K;
+            const uint64_t ob = (r0 + gr0) * K;
             for (int q = lane; q < lim; q += 32) {
                 const int r = q / K, cc = q - r * K;
-                og[q] = sx[r * C::LD + cc];
+                const double v = sx[r * C::LD + cc];
+                og[q] = v;
+                for (int pr = 0; pr < npeer; ++pr) gp.peer_out[pr][ob + q] = v;
             }
         }
         // X^T Y: k = the group's rows.  Rows past the chunk end are zero in sx (A fragments were zeroed).

@@ -285,6 +285,12 @@ struct Solver {
     DBuf<double> w2red, pred;  // all-reduced K x K Gram / drift product (distributed path)
     DBuf<double> core_alt;     // conditional core recompute (distributed path)
     std::shared_ptr<const FillTable> fill;  // Householder fill stream (rank-deficient QR)
+    // multi-GPU: the other ranks' replicas of every factor buffer, mapped through CUDA IPC (peer_u[n][q][i] is
+    // U[n][q] of the i-th other rank).  When every rank could map every peer, the apply stores its rows of U_new
+    // into all replicas itself (k_rowgemm's peer_out) and a barrier replaces the all-gather.
+    std::vector<double*> peer_u[kMaxOrder][2];
+    std::vector<void*> peer_maps;  // cudaIpcOpenMemHandle results (closed in the destructor)
+    bool peer_apply = false;
     uint64_t rb(int n) const { return comm ? bnd[n][comm->rank] : 0; }
     uint64_t re(int n) const { return comm ? bnd[n][comm->rank + 1] : dims[n]; }
     DBuf<DevStatus> st;
@@ -306,6 +312,10 @@ struct Solver {
     }
 
     ~Solver() {
+        if (!peer_maps.empty()) {
+            cudaDeviceSynchronize();  // no kernel of this rank may still be storing into a peer's replica
+            close_peers();
+        }
         for (auto& g : graph)
             if (g) cudaGraphExecDestroy(g);
         for (auto e : ev) cudaEventDestroy(e);
@@ -433,6 +443,7 @@ struct Solver {
         st.alloc(1);
         HQ_CUDA(cudaMemsetAsync(st.get(), 0, sizeof(DevStatus), s));
 
+        setup_peers();
         // ---- initial factors (solvers.cpp:182-215)
         {
             double* u0[kMaxOrder];
@@ -450,6 +461,78 @@ struct Solver {
         HQ_CUDA(cudaMemcpyAsync(fit_prev.get(), &fp, 8, cudaMemcpyHostToDevice, s));
         HQ_CUDA(cudaStreamSynchronize(s));
         host_parity = 0;
+    }
+
+    // Multi-GPU: exchange CUDA IPC handles of the factor buffers and map every other rank's replicas.  The
+    // handles travel through the communicator's own all-reduce (each byte as a double in the rank's segment of
+    // a zeroed array: exact sums), so both transports carry them.  HQ_PEER_APPLY=0 keeps the all-gather.
+    void setup_peers() {
+        peer_apply = false;
+        if (!comm || comm->world <= 1 || comm->world - 1 > kMaxPeers) return;
+        const char* e = std::getenv("HQ_PEER_APPLY");
+        const int W = comm->world, R = comm->rank;
+        const int nb = 2 * N, hb = (int)sizeof(cudaIpcMemHandle_t);
+        const size_t len = (size_t)W * nb * hb + W;  // handles, then one "mapped all peers" flag per rank
+        std::vector<double> h(len, 0.0);
+        bool ok = !(e && e[0] == '0');
+        for (int v = 0; v < N && ok; ++v)
+            for (int q = 0; q < 2 && ok; ++q) {
+                cudaIpcMemHandle_t mh;
+                if (cudaIpcGetMemHandle(&mh, U[v][q].p) != cudaSuccess) {
+                    cudaGetLastError();
+                    ok = false;
+                    break;
+                }
+                const unsigned char* b = reinterpret_cast<const unsigned char*>(&mh);
+                for (int i = 0; i < hb; ++i) h[((size_t)R * nb + 2 * v + q) * hb + i] = (double)b[i];
+            }
+        DBuf<double> d;
+        d.alloc(len);
+        auto exchange = [&] {
+            HQ_CUDA(cudaMemcpyAsync(d.get(), h.data(), sizeof(double) * len, cudaMemcpyHostToDevice, s));
+            comm->allreduce_sum(d.get(), len, s);
+            HQ_CUDA(cudaMemcpyAsync(h.data(), d.get(), sizeof(double) * len, cudaMemcpyDeviceToHost, s));
+            HQ_CUDA(cudaStreamSynchronize(s));
+        };
+        h[(size_t)W * nb * hb + R] = ok ? 1.0 : 0.0;
+        exchange();
+        bool all = true;
+        for (int r = 0; r < W; ++r) all = all && h[(size_t)W * nb * hb + r] == 1.0;
+        std::vector<double*> maps[kMaxOrder][2];
+        bool mapped = all;
+        for (int r = 0; r < W && mapped; ++r) {
+            if (r == R) continue;
+            for (int v = 0; v < N && mapped; ++v)
+                for (int q = 0; q < 2 && mapped; ++q) {
+                    cudaIpcMemHandle_t mh;
+                    unsigned char* b = reinterpret_cast<unsigned char*>(&mh);
+                    for (int i = 0; i < hb; ++i) b[i] = (unsigned char)h[((size_t)r * nb + 2 * v + q) * hb + i];
+                    void* ptr = nullptr;
+                    if (cudaIpcOpenMemHandle(&ptr, mh, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                        cudaGetLastError();
+                        mapped = false;
+                        break;
+                    }
+                    peer_maps.push_back(ptr);
+                    maps[v][q].push_back(static_cast<double*>(ptr));
+                }
+        }
+        // second round: every rank mapped every replica, or nobody uses them
+        std::fill(h.begin(), h.end(), 0.0);
+        h[(size_t)W * nb * hb + R] = mapped ? 1.0 : 0.0;
+        exchange();
+        for (int r = 0; r < W; ++r) mapped = mapped && h[(size_t)W * nb * hb + r] == 1.0;
+        if (mapped) {
+            for (int v = 0; v < N; ++v)
+                for (int q = 0; q < 2; ++q) peer_u[v][q] = maps[v][q];
+            peer_apply = true;
+        } else {
+            close_peers();
+        }
+    }
+    void close_peers() {
+        for (void* m : peer_maps) cudaIpcCloseMemHandle(m);
+        peer_maps.clear();
     }
 
     // core = X x {U^T} with the parity-p factors, via the mode-0 pass
@@ -548,9 +631,20 @@ struct Solver {
             comm->allreduce_sum(w2red.get(), (size_t)K * K, s);
             launch_chol2(w2red.get(), 1, K, r1inv.get(), rinv.get(), rc.get(), mred, &m, core.get(), S, s, true, n + 1);
             // U_new rows = Q R^-1, P partials of this rank's rows (tr_p is all-reduced once, at download)
-            launch_apply_qr(a_loc, lrows, K, r1inv.get(), rinv.get(), uloc, uold + r0 * K, pp, false, S, kOnlyCholQR,
-                            s);
-            comm->allgather_rows(unew, bnd[n].data(), (size_t)K, s);
+            if (peer_apply) {
+                // the apply stores its rows into every rank's replica of U_new over peer memory; the barrier
+                // orders those stores before the next pass's gathers on every rank
+                double* po[kMaxPeers];
+                const auto& pu = peer_u[n][1 - p];
+                for (size_t i = 0; i < pu.size(); ++i) po[i] = pu[i] + r0 * K;
+                launch_apply_qr(a_loc, lrows, K, r1inv.get(), rinv.get(), uloc, uold + r0 * K, pp, false, S,
+                                kOnlyCholQR, s, po, (int)pu.size());
+                comm->barrier(s);
+            } else {
+                launch_apply_qr(a_loc, lrows, K, r1inv.get(), rinv.get(), uloc, uold + r0 * K, pp, false, S,
+                                kOnlyCholQR, s);
+                comm->allgather_rows(unew, bnd[n].data(), (size_t)K, s);
+            }
         }
         mode_tail(n, pp, pslots);
     }
@@ -1532,6 +1626,8 @@ int hq_solver_status(hq_solver* s, int64_t* out) {
         out[3] = h.degenerate_mode;
         out[4] = h.shifted_count;
         out[5] = h.dist_hh_count;
+        out[6] = s->impl->peer_apply ? 1 : 0;
+        out[7] = 0;
     });
 }
 

@@ -5,7 +5,9 @@ H2D, so no kernel waits on another rank and both ranks may share the one GPU
 gpurun provides).  Row-partitioned pass, all-reduced Grams / M / W, owner
 row gather of every new factor, the host-driven Householder continuation
 with the reference's seeded fill on rank-deficient updates, and the sharded
-storage (hq_tensor_shard: each rank keeps only its rows' streams).  Every
+storage (hq_tensor_shard: each rank keeps only its rows' streams), and the
+fused apply + all-gather (the apply kernel stores its rows of U_new into the
+other rank's replica, mapped through CUDA IPC; a barrier follows).  Every
 sweep is checked against the oracle (the C restatement of the reference's
 solve loop, oracle/hq_oracle.c) and the final state against the single-GPU
 engine."""
@@ -54,14 +56,15 @@ RANK_SCRIPT = textwrap.dedent("""
 """)
 
 
-def _world2(tmp_path, dims, ranks, coords, vals, u0, sweeps, shard):
+def _world2(tmp_path, dims, ranks, coords, vals, u0, sweeps, shard, peer=True):
     case = tmp_path / "case.npz"
     np.savez(case, dims=np.asarray(dims), ranks=np.asarray(ranks), sweeps=sweeps, coords=coords, vals=vals,
              **{f"U0_{m}": u for m, u in enumerate(u0)})
     out = tmp_path / "rank0.json"
     name = "/hq_t_" + uuid.uuid4().hex[:12]
     procs = [subprocess.Popen([sys.executable, "-c", RANK_SCRIPT, str(r), "2", name, str(case), "1" if shard else "0",
-                               str(out)], cwd=ROOT, env={**os.environ, "HQ_HOST_BARRIER_S": "90"}, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+                               str(out)], cwd=ROOT, env={**os.environ, "HQ_HOST_BARRIER_S": "90", "HQ_PEER_APPLY": "1" if peer else "0"},
+                              stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
              for r in range(2)]
     logs = []
     for p in procs:
@@ -117,6 +120,15 @@ def test_world2_engine_matches_oracle(tmp_path, oracle, case, shard):
             assert np.linalg.norm(ug @ ug.T - ur @ ur.T) <= 1e-8, (s, m)
         g, gr = np.array(r["core"]), ref["core_snap"][s].reshape(-1)
         assert np.linalg.norm(g - gr) <= 1e-9 * np.linalg.norm(gr), s
+    # the apply stored U_new straight into the other rank's replica (CUDA IPC peer memory; fused apply +
+    # all-gather), and the all-gather path (HQ_PEER_APPLY=0) gives the same bits
+    assert out["status"]["peer_apply"] == 1, out["status"]
+    if case == "uniform" and not shard:
+        out0 = _world2(tmp_path, dims, ranks, coords, vals, u0, sweeps, shard, peer=False)
+        assert out0["status"]["peer_apply"] == 0
+        for m in range(N):
+            assert np.array_equal(np.array(out0["res"][-1]["factors"][m]), np.array(out["res"][-1]["factors"][m]))
+        assert np.array_equal(np.array(out0["res"][-1]["core"]), np.array(out["res"][-1]["core"]))
     # the single-GPU engine on the same inputs ends in the same state
     x = hq.SparseTensor(dims, coords, vals)
     r1 = hq.hoqri(x, hq.SolverConfig(ranks=ranks, max_sweeps=sweeps, tol_fit_change=0.0), init_factors=u0)

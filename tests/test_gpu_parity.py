@@ -354,3 +354,26 @@ def test_hoqri_gradient_trace_matches_reference(name):
     sw = np.array([s.grad_norm_sq for s in r.trace.sweeps]).reshape(-1)
     np.testing.assert_allclose(sw, gr, rtol=0, atol=0)
     np.testing.assert_allclose([s.objective for s in r.trace.sweeps], g[f"{name}_objective"], rtol=1e-9)
+
+
+def test_cached_device_memory_is_reused_and_released():
+    """Device buffers of a destroyed tensor stay on the engine's free lists (no driver allocation for the next
+    tensor of the same shape) until hq_release_cached_memory hands them back."""
+    import torch
+    from paper_2510_16930_b200.workloads import uniform_coo
+    dims = [3000, 2500, 2000]
+    coords, vals = uniform_coo(dims, 200000, 3)
+    hq.release_cached_memory()
+    x = hq.SparseTensor(dims, coords, vals)
+    n1 = hq.norm_sq(x)
+    del x
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    x = hq.SparseTensor(dims, coords, vals)  # same sizes: served from the free lists
+    assert hq.norm_sq(x) == n1
+    assert torch.cuda.mem_get_info()[0] == free0, "the second build allocated from the driver"
+    del x
+    freed = hq.release_cached_memory()
+    assert freed >= coords.nbytes + vals.nbytes
+    assert torch.cuda.mem_get_info()[0] >= free0 + freed // 2
+    assert hq.release_cached_memory() == 0

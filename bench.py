@@ -442,7 +442,7 @@ def run_engine(args, ws, rank, local):
             del se, xe
             return r
 
-        for _ in range(2):  # warm: the first solves also grow the device memory pool to its working set
+        for _ in range(2):  # warm: the first solves also fill the engine's device block cache with the working set
             r = e2e_step()
         torch.cuda.synchronize()
         if ws > 1:

@@ -274,6 +274,26 @@ def reference_mode_updates(coords, vals, dims, ranks, factors, steps, warmup, sa
     return dict(steps_s=steps_s, phases=phases, t_build=t_build, t_init=t_init, nnz=t.nnz)
 
 
+def bench_config(c, dims, ranks, nnz, ws):
+    """The `config` / `data` entries of the JSON line -- the same for both arms (the reference arm measures the
+    engine arm's workload; what one of its timed steps covers is its `sample_step`)."""
+    N = len(dims)
+    config = {"workload": c["name"], "dims": dims, "ranks": ranks, "draws": c["draws"], "nnz_merged": int(nnz),
+              "step": "one HOQRI sweep (N mode updates)",
+              "parallelism": (f"row-partitioned x{ws} (NCCL all-reduces; QR apply + all-gather of the new factor "
+                              f"fused over peer memory)") if ws > 1 else "single GPU",
+              "l2": "%s (mode streams %.0f MB + factors %.0f MB vs 126 MB L2)" %
+                    ("inputs larger than L2" if nnz * (4 * (N - 1) + 8) * N > 126e6 else
+                     "inputs SMALLER than L2: a parity-test size, not a bench configuration",
+                     nnz * (4 * (N - 1) + 8) * N / 1e6, sum(d * k for d, k in zip(dims, ranks)) * 8 * 2 / 1e6)}
+    kind = {"uniform": "uniform int32 coords, U(0,1) values",
+            "lognormal": "Zipf(%s) mode indices over seeded permutations, lognormal(0,1) values" % c.get("zipf_s"),
+            "planted": "uniform int32 coords, planted rank-%d Tucker model + %g Gaussian noise" %
+                       (ranks[0], c.get("noise", 0.0))}[c["values"]]
+    data = "synthetic (BASELINE %s: %s; seeded PCG64; duplicates merged)" % (c["name"].split("_")[0], kind)
+    return config, data
+
+
 def run_reference(args, ws, rank):
     """--impl reference: the reference's own CPU implementation of the path
     (oracle/_ref = the unmodified reference library), rank 0 only.  A step is
@@ -292,14 +312,14 @@ def run_reference(args, ws, rank):
     value = (K / N) / total
     model, ncpu = host_desc()
     ttm = [p["ttmctc"] for p in r["phases"]]
+    config, data = bench_config(c, dims, ranks, r["nnz"], ws)
     line = {"impl": "reference", "metric": METRIC.format(cfg=args.config), "value": value, "unit": "iter/s",
             "n_gpus": ws, "steps": K, "warmup": W, "ms_per_step": total / K * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (BASELINE config %d, seeded PCG64)" % args.config,
-            "config": {"workload": c["name"], "dims": dims, "ranks": ranks, "nnz_merged": int(r["nnz"]),
-                       "step": f"one full-size mode update of tucker::hoqri's loop (1/{N} of a sweep): "
-                               "ttmctc_elementwise(core given) + max_abs + qr_orthonormal + subspace_distance + "
-                               "ttmc_core on every nonzero"},
+            "data": data, "config": config,
+            "sample_step": f"a timed step of this arm is one full-size mode update of tucker::hoqri's loop (1/{N} of "
+                           "a sweep): ttmctc_elementwise(core given) + max_abs + qr_orthonormal + "
+                           "subspace_distance + ttmc_core on every nonzero; value = sweeps/s over the timed steps",
             "cpu_baseline": {"value": value, "unit": "iter/s", "cores": 1, "kind": "reference",
                              "sample": f"none: {K} full-size mode updates ({K / N:.2f} sweeps) of the unmodified "
                                        f"reference, each timed as it ran (steady_clock); the reference is "
@@ -477,16 +497,11 @@ def run_engine(args, ws, rank, local):
     if rank != 0:
         return
     model, ncpu = host_desc()
+    config, data = bench_config(c, dims, ranks, nnz, ws)
     line = {
         "metric": METRIC.format(cfg=args.config), "value": value, "unit": "iter/s", "n_gpus": ws, "steps": K, "warmup": W,
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (BASELINE config %d: uniform int32 coords, U(0,1) values, seeded PCG64; duplicates "
-                "merged on device)" % args.config,
-        "config": {"workload": c["name"], "dims": dims, "ranks": ranks, "draws": c["draws"], "nnz_merged": nnz,
-                   "step": "one HOQRI sweep (N mode updates)",
-                   "parallelism": f"row-partitioned x{ws} (NCCL all-reduce + owner broadcast)" if ws > 1 else "single GPU",
-                   "l2": "inputs larger than L2 (mode streams %.0f MB + factors %.0f MB vs 126 MB L2)" %
-                         (nnz * (4 * (N - 1) + 8) * N / 1e6, sum(d * k for d, k in zip(dims, ranks)) * 8 * 2 / 1e6)},
+        "data": data, "config": config,
         "ttmctc": {"value": nnz / (statistics.mean(ttm_ms) * 1e-3), "unit": "nnz/s",
                    "per_mode_ms": ttm_ms,
                    "note": "SURVEY 8(d): standalone TTMcTC (core given; G_(n)^T unfold + A only), median of 10 "

@@ -214,7 +214,7 @@ __device__ __forceinline__ double pick(const double (&row)[KM], int k) {
 }
 
 template <int KM>
-__global__ void __launch_bounds__(kHhThreads) k_householder_mc(const double* __restrict__ A, uint64_t m, int n,
+__global__ void __launch_bounds__(kHhThreads, 1) k_householder_mc(const double* __restrict__ A, uint64_t m, int n,
                                                                double* __restrict__ q, double* __restrict__ work,
                                                                const double* __restrict__ table, uint64_t table_len,
                                                                const DevStatus* st, int run_if) {
@@ -449,15 +449,15 @@ __global__ void __launch_bounds__(kHhThreads) k_householder_mc(const double* __r
             double vi[KM];
 #pragma unroll
             for (int k = 0; k < KM; ++k) vi[k] = (k < n && i >= (uint64_t)k) ? refl[(uint64_t)k * m + i] : 0.0;
+            // (the j loop is left rolled: unrolled, its KM x KM loads of C are hoisted and spill registers)
+#pragma unroll 1
+            for (int j = 0; j < n; ++j) {
+                double v = (i == (uint64_t)j) ? 1.0 : 0.0;
 #pragma unroll
-            for (int j = 0; j < KM; ++j)
-                if (j < n) {
-                    double v = (i == (uint64_t)j) ? 1.0 : 0.0;
-#pragma unroll
-                    for (int k = 0; k < KM; ++k)
-                        if (k < n) v -= vi[k] * sC[k][j];
-                    q[i * n + j] = v;
-                }
+                for (int k = 0; k < KM; ++k)
+                    if (k < n) v -= vi[k] * sC[k][j];
+                q[i * n + j] = v;
+            }
         }
     }
     // R_kk >= 0: flip the columns whose alpha was negative

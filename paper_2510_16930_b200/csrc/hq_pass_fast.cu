@@ -603,15 +603,22 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
 // written over the staged rows -- so a CTA needs ~74 KB of shared memory and
 // twelve compute warps share an SM (three independent CTAs overlap each
 // other's phases instead of one CTA overlapping its own).
+// Records per gather round.  368 is what three CTAs per SM leave room for (3 x (76.7 KB + 1 KB reserved) of the
+// SM's 228 KB, 96 bytes to spare): a config-2 tile holds 320 +- 18 records, so 0.4 % of the tiles need a second
+// round (3.6 % at 352: pass 0.617 -> 0.609 ms; the rows' sums keep their stream order, same bits).  If the
+// device grants fewer than three CTAs per SM at 368, the 352-record instance is used.
 #ifndef HQ_NP_CAP
-#define HQ_NP_CAP 352
+#define HQ_NP_CAP 368
+#endif
+#ifndef HQ_NP_CAP_SMALL
+#define HQ_NP_CAP_SMALL 352
 #endif
 #ifndef HQ_NP_MINB
 #define HQ_NP_MINB 3
 #endif
-template <int KA, int KB, int KN>
+template <int KA, int KB, int KN, int CAPV>
 struct CfgNP : Cfg<KA, KB, KN> {
-    static constexpr int CAP = HQ_NP_CAP;
+    static constexpr int CAP = CAPV;
     static constexpr int FW = KA + KB;
     static constexpr int ALD = 12;  // A tile row stride: columns 0..K_n-1 (the M-GEMM reads 8..15 only for K_n > 8)
     static constexpr int GTAB = kGtFragTable;  // the A-GEMM's pre-permuted G_(n)^T fragments (k_gt)
@@ -624,9 +631,9 @@ struct CfgNP : Cfg<KA, KB, KN> {
                                    Cfg<KA, KB, KN>::META + Cfg<KA, KB, KN>::R * 4 + 64;
 };
 
-template <int KA, int KB, int KN>
+template <int KA, int KB, int KN, int CAPV>
 __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
-    using C = CfgNP<KA, KB, KN>;
+    using C = CfgNP<KA, KB, KN, CAPV>;
     if (skip_kernel(a.st, a.run_if)) return;
 #ifdef HQ_PHASE_TIMING
     long long _ph_t = clock64();
@@ -966,17 +973,21 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
 template <int KA, int KB, int KN>
 void launch_fast3(const FastArgs& a, int grid, cudaStream_t s) {
     if constexpr (KA == 10 && KB == 10 && KN == 10) {  // grid = 3 CTAs per SM (fast_grid), one partial slot per CTA
-        using CN = CfgNP<KA, KB, KN>;
-        static bool attr3 = false;
-        if (!attr3) {
-            HQ_CUDA(cudaFuncSetAttribute(k_pass_np3<KA, KB, KN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)CN::smem));
-            int per_sm = 0;  // the grid (fast_grid) and the tile ranges assume HQ_NP_MINB resident CTAs per SM
-            HQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pass_np3<KA, KB, KN>, 128, CN::smem));
-            if (per_sm < HQ_NP_MINB) fail(HQ_ERR_INTERNAL, "k_pass_np3: fewer resident CTAs per SM than planned");
-            attr3 = true;
+        using CL = CfgNP<KA, KB, KN, HQ_NP_CAP>;
+        using CS = CfgNP<KA, KB, KN, HQ_NP_CAP_SMALL>;
+        static int large = -1;  // which instance: decided once from the device's occupancy answer
+        if (large < 0) {
+            HQ_CUDA(cudaFuncSetAttribute(k_pass_np3<KA, KB, KN, HQ_NP_CAP>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CL::smem));
+            HQ_CUDA(cudaFuncSetAttribute(k_pass_np3<KA, KB, KN, HQ_NP_CAP_SMALL>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CS::smem));
+            int per_sm = 0;  // the grid (fast_grid) plans HQ_NP_MINB resident CTAs per SM
+            HQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pass_np3<KA, KB, KN, HQ_NP_CAP>, 128,
+                                                                  CL::smem));
+            large = per_sm >= HQ_NP_MINB ? 1 : 0;
         }
-        k_pass_np3<KA, KB, KN><<<grid, 128, CN::smem, s>>>(a);
+        if (large) k_pass_np3<KA, KB, KN, HQ_NP_CAP><<<grid, 128, CL::smem, s>>>(a);
+        else k_pass_np3<KA, KB, KN, HQ_NP_CAP_SMALL><<<grid, 128, CS::smem, s>>>(a);
         HQ_CHECK_LAUNCH();
         return;
     } else {  // K = 16 / 8: the software-pipelined two-CTAs-per-SM kernel

@@ -3,6 +3,7 @@
 //   0: two tables, 80 B rows                    1: two tables, 64 B heads only (64-byte aligned rows)
 //   2: two tables, 16 B tails only (2 x 16 MB)   3: one table, 80 B rows (both gathers from table A)
 //   4: two tables, 32 B rows (one sector)
+// -DPF=64/128/256 adds the L2 prefetch-size qualifier to the copies.
 // Run under ncu --metrics dram__bytes_read.sum,lts__t_sector_hit_rate.pct for the bytes.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench_fetch tools/microbench_fetch.cu
 #include <cuda_runtime.h>
@@ -12,8 +13,19 @@
 #include <vector>
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s line %d\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+#ifndef PF
+#define PF 0
+#endif
 __device__ __forceinline__ void cp16(void* d, const void* s) {
+#if PF == 64
+    asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16;" :: "r"(sa(d)), "l"(s));
+#elif PF == 128
+    asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;" :: "r"(sa(d)), "l"(s));
+#elif PF == 256
+    asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;" :: "r"(sa(d)), "l"(s));
+#else
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(sa(d)), "l"(s));
+#endif
 }
 template <int MODE>
 __global__ void __launch_bounds__(128) bench(const double* A, const double* B, const uint2* idx, long n, double* out) {

@@ -89,9 +89,20 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// factor-row pieces: a miss fetches the 64-byte pair of sectors (.L2::64B) -- the row's next piece usually needs
+// the other one; 20 % less DRAM read traffic on random 80-byte rows in isolation (tools/microbench_fetch.cu
+// -DPF=64) and the config-2 pass 0.609 -> 0.605 ms
+#ifndef HQ_CP_PF64
+#define HQ_CP_PF64 1
+#endif
 __device__ __forceinline__ void cp16(void* dst, const void* src, uint64_t pol) {
+#if HQ_CP_PF64
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint.L2::64B [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
+                 "l"(pol));
+#else
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src),
                  "l"(pol));
+#endif
 }
 // L1-allocating variant for the rows of a hot (skewed) factor: repeats are served by L1 instead of one L2 slice
 __device__ __forceinline__ void cp16_l1(void* dst, const void* src, uint64_t pol) {

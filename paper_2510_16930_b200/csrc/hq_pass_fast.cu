@@ -624,6 +624,13 @@ __global__ void __launch_bounds__(Cfg<KA, KB, KN>::THREADS, Cfg<KA, KB, KN>::MIN
 #ifndef HQ_NP_CAP_SMALL
 #define HQ_NP_CAP_SMALL 352
 #endif
+// records per unrolled step of the Kronecker-row loop (shared loads of the next records behind the DFMAs of this
+// one; 2 -> 4: config-2 pass 0.605 -> 0.598 ms; 8 spills)
+#ifndef HQ_NP_KU
+#define HQ_NP_KU 4
+#endif
+#define HQ_PRAGMA_(x) _Pragma(#x)
+#define HQ_UNROLL(n) HQ_PRAGMA_(unroll n)
 #ifndef HQ_NP_MINB
 #define HQ_NP_MINB 3
 #endif
@@ -808,7 +815,7 @@ __global__ void __launch_bounds__(128, HQ_NP_MINB) k_pass_np3(FastArgs a) {
             __syncthreads();
             HQ_PHASE(3);
             const int e0 = max(voff, cv) - cv, e1 = min(voff + len, cv + C::CAP) - cv;
-#pragma unroll 2
+HQ_UNROLL(HQ_NP_KU)
             for (int e = e0; e < e1; ++e) {
                 const double x = rxp[e];
                 const double* f = sF + (size_t)e * C::FW;

@@ -1,0 +1,5 @@
+export PYTHONUNBUFFERED=1
+for v in default ku1 ku3 ku4 default; do
+  if [ $v = default ]; then unset HQ_LIB; else export HQ_LIB=tmp_variants/$v/libhoqri_b200.so; fi
+  timeout 600 python tools/pass_time.py 2 2>&1 | grep -v Warn | tail -1
+done

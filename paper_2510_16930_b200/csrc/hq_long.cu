@@ -37,6 +37,13 @@ __device__ unsigned long long hq_fib_phase_cycles[16];
 #define HQ_FPHASE(i) do { } while (0)
 #endif
 
+// k-steps per unrolled step of a warp's share of a full chunk (4 = all of it: the fragment loads of the next
+// k-steps behind the DMMAs of this one; config 4 pass 2.197 -> 2.173 ms, config 5 11.67 -> 11.52 ms)
+#ifndef HQ_LS_KU
+#define HQ_LS_KU 4
+#endif
+#define HQ_PRAGMA_(x) _Pragma(#x)
+#define HQ_UNROLL(n) HQ_PRAGMA_(unroll n)
 #ifndef HQ_FIB_DIVFREE
 #define HQ_FIB_DIVFREE 1
 #endif
@@ -255,7 +262,7 @@ __global__ void __launch_bounds__(256) k_longseg_mma(LongArgs a) {
         const int n = cc.n(S::CH);
         const double* f = rowbuf + (size_t)(ch & 1) * S::row_doubles;
         if (n == S::CH) {
-#pragma unroll 2
+HQ_UNROLL(HQ_LS_KU)
             for (int ks = warp; ks < S::CH / 4; ks += S::WARPS) kstep<K0, K1, K2, S, true>(f, ks, n, gid, tig, acc);
         } else {
             for (int ks = warp; ks < (n + 3) / 4; ks += S::WARPS) kstep<K0, K1, K2, S, false>(f, ks, n, gid, tig, acc);
@@ -329,7 +336,7 @@ __global__ void __launch_bounds__(256) k_longseg_sync(LongArgs a) {
         cpa_wait<0>();
         __syncthreads();
         if (n == S::CH) {
-#pragma unroll 2
+HQ_UNROLL(HQ_LS_KU)
             for (int ks = warp; ks < S::CH / 4; ks += S::WARPS) kstep<K0, K1, K2, S, true>(rowbuf, ks, n, gid, tig, acc);
         } else {
             for (int ks = warp; ks < (n + 3) / 4; ks += S::WARPS)

@@ -1,0 +1,7 @@
+export PYTHONUNBUFFERED=1
+for c in 4 5; do
+for v in default lsku1 lsku4 default; do
+  if [ $v = default ]; then unset HQ_LIB; else export HQ_LIB=tmp_variants/$v/libhoqri_b200.so; fi
+  timeout 600 python tools/pass_time.py $c 8 2>&1 | grep -v Warn | tail -1
+done
+done
